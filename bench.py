@@ -1,0 +1,326 @@
+"""bench.py -- trained seed nodes/sec of the A3GNN data-parallel mini-batch hot
+path on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+A step = one batch of the workload through the whole path:
+  k-hop locality-aware sampling -> cached feature gather + mean aggregation ->
+  2-layer mean-GCN forward/backward -> [NCCL allreduce] -> SGD.
+Default workload = BASELINE.json configs[1] (Reddit-shaped synthetic graph,
+233K nodes / 112.8M edges, 602-d f32 features, fanout [15,10,5], batch 1024
+per GPU, full feature cache), generated bit-identically to the reference's
+generate_power_law(233000, 165, 2.5, 602, seed 1).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+For N>1 launch under torchrun (one rank per GPU, NCCL).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (n, min_degree, feat_dim, fanouts, batch, cache_frac, description)
+    "c2": (233_000, 165, 602, [15, 10, 5], 1024, 1.0,
+           "reddit-shaped synthetic 233K nodes / 112.8M edges, 602-d f32, fanout [15,10,5], batch 1024/GPU, "
+           "full feature cache"),
+    "c1": (100_000, 3, 128, [10, 5], 1024, 0.2,
+           "power-law synthetic 100K nodes / 0.9M edges, 128-d f32, fanout [10,5], batch 1024/GPU, 20% cache"),
+    "c3": (2_450_000, 9, 100, [15, 10, 5], 4096, 0.2,
+           "ogbn-products-shaped synthetic 2.45M nodes / 65M edges, 100-d f32, fanout [15,10,5], batch 4096/GPU, "
+           "20% cache"),
+}
+HIDDEN, CLASSES, LR, BASE_SEED = 16, 4, 0.2, 1
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", choices=list(CONFIGS), default="c2")
+    p.add_argument("--gamma", type=float, default=8.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-units", type=int, default=3, help="batches in the bounded cpu_baseline sample")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_graph(cfg_name):
+    from paper_2511_07421_b200 import graph as G
+    n, m, F, fan, B, frac, _ = CONFIGS[cfg_name]
+    return G.generate_power_law(n, m, 2.5, F, BASE_SEED)
+
+
+def step_batches(g, B, world, steps, offset=0):
+    """Global batches of world*B seeds (epoch plans, trainer.cpp:330-343) and
+    their step seeds sampling_seed(base, epoch, step, 0) (trainer.cpp:345)."""
+    from paper_2511_07421_b200 import train as T
+    gb = B * world
+    tn = g.train_nodes
+    per_epoch = len(tn) // gb
+    out, seeds = [], []
+    cache = {}
+    for i in range(offset, offset + steps):
+        e, s = divmod(i, per_epoch)
+        if e not in cache:  # plan seed hash2(base, worker 0) (trainer.cpp:378-379)
+            cache[e] = T.plan_epoch_order(tn, e, _hash2(BASE_SEED, 0))
+        out.append(cache[e][s * gb:(s + 1) * gb])
+        seeds.append(T.sampling_seed(BASE_SEED, e, s, 0))
+    return np.stack(out), np.array(seeds, dtype=np.uint64)
+
+
+def _mix64(z):
+    M = (1 << 64) - 1
+    z ^= z >> 30
+    z = (z * 0xbf58476d1ce4e5b9) & M
+    z ^= z >> 27
+    z = (z * 0x94d049bb133111eb) & M
+    z ^= z >> 31
+    return z
+
+
+def _hash2(a, b):
+    return _mix64(a ^ _mix64((b + 0x9e3779b97f4a7c15) & ((1 << 64) - 1)))
+
+
+def cpu_reference_run(g, cfg_name, gamma, units, producers, tmpdir="/tmp"):
+    """Time the reference's own CPU path (oracle/_ref, the unmodified reference
+    compiled in place) on `units` batches of the same workload."""
+    import oracle
+    if not oracle.ref_available():
+        return None
+    from paper_2511_07421_b200 import graph as G
+    n, m, F, fan, B, frac, _ = CONFIGS[cfg_name]
+    path = os.path.join(tmpdir, f"a3g_bench_{cfg_name}_{os.getpid()}.a3g")
+    G.save_graph(g, path)
+    ref = oracle.RefLib()
+    rg = ref.load(path)
+    os.remove(path)
+    dm = ref.build_static_cache(rg, int(frac * n) * F * 4, 1)
+    secs, seeds = ref.bench_steps(rg, dm, fan, gamma, BASE_SEED, B, HIDDEN, CLASSES, LR, units, producers, 8)
+    return dict(seconds=secs, seeds=seeds, seeds_per_s=seeds / secs if secs > 0 else 0.0)
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    n, m, F, fan, B, frac, desc = CONFIGS[args.config]
+    import oracle
+    base = {"metric": "trained seed nodes/sec", "unit": "seeds/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "dtype": "f64", "data": "synthetic", "vs_baseline": None,
+            "config": {"workload": args.config, "description": desc, "global_batch": B, "fanouts": fan,
+                       "gamma": args.gamma, "hidden": HIDDEN, "classes": CLASSES}}
+    if not oracle.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref (reference compiled in place) not built"}))
+        return 0
+    g = make_graph(args.config)
+    cores = os.cpu_count() or 1
+    producers = max(1, cores - 1)
+    units = max(1, args.steps)
+    r = cpu_reference_run(g, args.config, args.gamma, units, producers)
+    v = r["seeds_per_s"]
+    base.update({"value": v, "ms_per_step": 1e3 * r["seconds"] / units,
+                 "cpu_baseline": {"value": v, "unit": "seeds/s", "cores": cores, "kind": "reference",
+                                  "sample": f"{units} consecutive batches of epoch 0, pmode1 schedule, "
+                                            f"{producers} sampler threads + 1 trainer thread"},
+                 "e2e": {"value": v, "unit": "seeds/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+    print(json.dumps(base))
+    return 0
+
+
+def run_ours(args):
+    rank, world, local = dist_env()
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2511_07421_b200 import cache as CA, train as T
+    n, m, F, fan, B, frac, desc = CONFIGS[args.config]
+    t0 = time.time()
+    g = make_graph(args.config)
+    gen_s = time.time() - t0
+    cache = CA.build_static_cache(g, CA.CacheConfig(int(frac * n) * F * 4 // 1, 1), device=local)
+    tr = T.Trainer(g, cache, T.ModelSpec(F, HIDDEN, CLASSES, learning_rate=LR), fan, max_seeds=B, device=local)
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(T.Comm.unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        comm = T.Comm(bytes(uid.cpu().numpy().tobytes()), world, rank, local)
+        tr.set_comm(comm)
+    W, K = args.warmup, args.steps
+    gbatches, gseeds = step_batches(g, B, world, W + 2 * K)
+    mine = np.ascontiguousarray(gbatches[:, rank * B:(rank + 1) * B])
+    # ---- warmup (untimed)
+    tr.steps(mine[:W], gseeds[:W], args.gamma, 0)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed: inputs resident in HBM (device seeds), device time via events
+    dev_seeds = torch.from_numpy(mine[W:W + K].astype(np.int32)).cuda()
+    barrier()
+    with ClockSampler(local) as clk:
+        losses = _steps_device(tr, dev_seeds, gseeds[W:W + K], args.gamma)
+        barrier()
+    tm = tr.timing()
+    dev_ms = tm["total_ms"]
+    # ---- e2e: host seeds through the C-ABI (H2D in the region, losses D2H)
+    barrier()
+    t1 = time.perf_counter()
+    losses_e2e = tr.steps(mine[W + K:W + 2 * K], gseeds[W + K:W + 2 * K], args.gamma, 0)
+    barrier()
+    e2e_s = time.perf_counter() - t1
+    tm2 = tr.timing()
+    if world > 1:
+        import torch.distributed as dist
+        x = torch.tensor([dev_ms, e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        dev_ms, e2e_s = float(x[0]), float(x[1])
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+    seeds_total = world * B * K
+    value = seeds_total / (dev_ms / 1e3)
+    e2e = seeds_total / e2e_s
+    hbm, peak_kind = measured_peaks()
+    agg_ms, agg_bytes = tm["agg_ms"], tm["agg_bytes"]
+    achieved = agg_bytes / (agg_ms * 1e-3) / 1e9 if agg_ms > 0 else 0.0
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "agg_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get(args.config)
+    out = {
+        "metric": "trained seed nodes/sec", "value": value, "unit": "seeds/s", "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": dev_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (generate_power_law, bit-identical to the reference generator)",
+        "config": {"workload": args.config, "description": desc, "global_batch": world * B, "batch_per_gpu": B,
+                   "fanouts": fan, "gamma": args.gamma, "model": "2-layer mean-GCN (reference trainer), H=16, C=4",
+                   "hidden": HIDDEN, "classes": CLASSES, "parallelism": f"dp{world}",
+                   "l2": "inputs larger than L2 (CSR %.0f MB + features %.0f MB)" % (
+                       g.num_edges * 4 / 1e6, n * F * 4 / 1e6), "graph_gen_s": round(gen_s, 1)},
+        "roofline": {"kernel": "k_agg1 (fused gather + mean aggregation + W1 update)", "bound": "hbm",
+                     "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": traffic, "bytes_per_launch": agg_bytes,
+                     "ms_per_launch": agg_ms},
+        "e2e": {"value": e2e, "unit": "seeds/s", "h2d_bytes_per_step": B * 4, "d2h_bytes_per_step": 8},
+        "gpu_launches": int(tm["launches_per_step"]) * K,
+        "clocks": clk.summary(),
+        "loss_first_last": [float(losses[0]), float(losses_e2e[-1])],
+    }
+    if not args.no_cpu_baseline and world == 1:
+        r = cpu_reference_run(g, args.config, args.gamma, args.cpu_units, 0)
+        if r:
+            out["cpu_baseline"] = {"value": r["seeds_per_s"], "unit": "seeds/s", "cores": 1, "kind": "reference",
+                                   "sample": f"{args.cpu_units} batches of epoch 0 (B={B}), sequential mode, "
+                                             f"{r['seconds']:.1f} s"}
+    print(json.dumps(out))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def _steps_device(tr, dev_seeds, rng_seeds, gamma):
+    """a3g_train_steps with seeds already resident in HBM (seeds_on_device=1)."""
+    import ctypes as C
+    from paper_2511_07421_b200._lib import check, f64p, lib, ptr, u64p
+    K, B = dev_seeds.shape
+    rs = np.ascontiguousarray(rng_seeds, dtype=np.uint64)
+    losses = np.empty(K, dtype=np.float64)
+    check(lib().a3g_train_steps(tr.h, C.cast(C.c_void_p(dev_seeds.data_ptr()), C.POINTER(C.c_uint32)), B, K,
+                                ptr(rs, u64p), float(gamma), 0, 1, ptr(losses, f64p)))
+    return losses
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,209 @@
+/*
+ * a3g.h -- C-ABI of the B200-native A3GNN data-parallel mini-batch hot path.
+ *
+ * Plain pointers and sizes only; every call returns an a3g_status and, on
+ * failure, a thread-local message via a3g_last_error(). The status codes map
+ * 1:1 onto the reference's exception types (proj/include/a3gnn/common.hpp:14-40)
+ * so the C++ drop-in (include/a3gnn_b200.hpp) can rethrow the same exception.
+ *
+ * The reference is a C++ library with no FFI of its own; each entry point below
+ * cites the reference declaration it replaces (proj/include/a3gnn/...). The
+ * reference-side binding a maintainer would add is in INTEGRATION.md.
+ *
+ * Threading: handles are owned by the creating thread; calls on distinct
+ * samplers/trainers (distinct arenas and streams) may run concurrently, which
+ * mirrors the reference's concurrent producers (pipeline_exec.cpp:235-256).
+ * Streams are passed explicitly as `void*` (a cudaStream_t; NULL = the
+ * handle's own stream).
+ */
+#ifndef A3G_H_
+#define A3G_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum a3g_status {
+  A3G_OK = 0,
+  A3G_ERR_PARAMETER = 1, /* a3gnn::ParameterError (common.hpp:14) */
+  A3G_ERR_LOOKUP = 2,    /* a3gnn::LookupError    (common.hpp:20) */
+  A3G_ERR_CONFIG = 3,    /* a3gnn::ConfigError    (common.hpp:26) */
+  A3G_ERR_IO = 4,        /* a3gnn::IoError        (common.hpp:37) */
+  A3G_ERR_CUDA = 5,
+  A3G_ERR_NCCL = 6,
+  A3G_ERR_OOM = 7
+} a3g_status;
+
+enum { A3G_SAMPLER_WEIGHTED = 0, A3G_SAMPLER_UNIFORM = 1 }; /* sampler.hpp:18-21 */
+enum { A3G_FEAT_F32 = 0, A3G_FEAT_BF16 = 1 };
+
+typedef struct a3g_host_graph {
+  /* graph.hpp:14-36 layout, host memory owned by the library */
+  uint64_t num_nodes;
+  uint64_t num_edges;
+  uint32_t feat_dim;
+  uint64_t* row_offsets; /* n+1 */
+  uint32_t* col_indices; /* m, ascending per row (graph.cpp:66) */
+  float* features;       /* n x feat_dim, row-major */
+  uint32_t* labels;      /* n */
+  uint8_t* train_mask;   /* n */
+  uint8_t* test_mask;    /* n */
+} a3g_host_graph;
+
+typedef struct a3g_graph a3g_graph;     /* device-resident CSR + feature store */
+typedef struct a3g_cache a3g_cache;     /* static hotness cache state */
+typedef struct a3g_sampler a3g_sampler; /* k-hop sampler arena (one batch in flight) */
+typedef struct a3g_trainer a3g_trainer; /* model, grads, streams, pipeline */
+typedef struct a3g_comm a3g_comm;       /* NCCL communicator (data-parallel sync) */
+
+const char* a3g_last_error(void);
+const char* a3g_version(void);
+
+/* ---------------------------------------------------------------- host --- */
+/* generators.cpp:79-149 generate_power_law, bit-identical, multithreaded. */
+a3g_status a3g_host_graph_power_law(uint64_t num_nodes, uint32_t min_degree, double exponent,
+                                    uint32_t feat_dim, uint64_t seed, int threads,
+                                    a3g_host_graph** out);
+/* graph_io.cpp:40-87 A3G1 load/save (graph_io.hpp:3-7 format). */
+a3g_status a3g_host_graph_load(const char* path, a3g_host_graph** out);
+a3g_status a3g_host_graph_save(const a3g_host_graph* g, const char* path);
+/* graph.cpp:59-84 from_edges (sorts (src,dst)); features zero. */
+a3g_status a3g_host_graph_from_edges(uint64_t num_nodes, const uint32_t* src, const uint32_t* dst,
+                                     uint64_t num_edges, uint32_t feat_dim, a3g_host_graph** out);
+void a3g_host_graph_free(a3g_host_graph* g);
+
+/* trainer.cpp:345-348 */
+uint64_t a3g_sampling_seed(uint64_t base, uint32_t epoch, uint32_t step, uint32_t worker);
+/* trainer.cpp:330-343: shuffled order of train_nodes; batch i = order[i*B, (i+1)*B). */
+void a3g_plan_epoch_order(const uint32_t* train_nodes, uint64_t n, uint32_t epoch, uint64_t seed,
+                          uint32_t* order_out);
+
+/* --------------------------------------------------------------- graph --- */
+/* Uploads CSR (+ optional features/labels) to `device`. features may be NULL
+ * (topology-only sampling). feat_dtype A3G_FEAT_BF16 rounds the f32 input to
+ * bf16 rows in HBM. Rows are pitched to 32 bytes. Replaces the shared,
+ * immutable graph::Graph (graph.hpp:3-4). */
+a3g_status a3g_graph_create(int device, uint64_t num_nodes, uint64_t num_edges, uint32_t feat_dim,
+                            const uint64_t* row_offsets, const uint32_t* col_indices,
+                            const float* features, int feat_dtype, const uint32_t* labels,
+                            a3g_graph** out);
+void a3g_graph_destroy(a3g_graph* g);
+
+/* --------------------------------------------------------------- cache --- */
+/* cache.cpp:12-46 build_static_cache: (out-degree desc, id asc), round-robin
+ * over num_devices, floor(volume_bytes / (F*4)) nodes per device.
+ * device_map_out (i32[n], -1 = miss) may be NULL. */
+a3g_status a3g_cache_build(a3g_graph* g, uint64_t volume_bytes, uint32_t num_devices,
+                           int32_t* device_map_out, a3g_cache** out);
+/* A CacheState given explicitly (test fixtures: test_sampler.cpp:15-25). */
+a3g_status a3g_cache_from_map(a3g_graph* g, const int32_t* device_map, uint32_t num_devices,
+                              a3g_cache** out);
+uint64_t a3g_cache_total_cached(const a3g_cache* c);
+void a3g_cache_destroy(a3g_cache* c);
+
+/* ------------------------------------------------------------- sampler --- */
+/* Arena for batches of <= max_seeds seeds with the given fanouts (outermost
+ * first, sampler.hpp:24). */
+a3g_status a3g_sampler_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds,
+                              const uint32_t* fanouts, uint32_t num_layers, a3g_sampler** out);
+void a3g_sampler_destroy(a3g_sampler* s);
+
+/* sampler.hpp:62-63 sample_khop, device-resident result. seeds are host
+ * memory (copied inside) unless seeds_on_device. kind: A3G_SAMPLER_*.
+ * Validation order/semantics as sampler.cpp:91-94,110 and assign_weights :62. */
+a3g_status a3g_sample_khop(a3g_sampler* s, const uint32_t* seeds, uint32_t n_seeds,
+                           int seeds_on_device, double bias_rate, int kind, uint64_t rng_seed,
+                           void* stream);
+
+/* Sizes of the last batch (synchronises the sampler stream).
+ * layer_edges: u64[num_layers]. */
+a3g_status a3g_batch_sizes(a3g_sampler* s, uint64_t* num_unique, uint64_t* num_seed_unique,
+                           uint64_t* num_duplicates_removed, uint64_t* layer_edges);
+/* Copies the last batch into host buffers sized by a3g_batch_sizes:
+ * SampleBatch (sampler.hpp:30-46) as unique_nodes and per-layer
+ * (dst_idx, src_idx) pairs in the reference's edge order. NULL skips. */
+a3g_status a3g_batch_copy(a3g_sampler* s, uint32_t* unique_nodes, uint32_t* const* layer_dst,
+                          uint32_t* const* layer_src);
+
+/* cache.hpp:78-80 retrieve_features for the last batch: gathers the
+ * unique_nodes' f32 rows into `out` (host, or device if out_on_device),
+ * counts cache hits/misses (cache.cpp:48-68) and returns B (cache.cpp:84). */
+a3g_status a3g_retrieve_features(a3g_sampler* s, float* out, int out_on_device, uint64_t* hits,
+                                 uint64_t* misses, uint64_t* batch_bytes, void* stream);
+
+/* cache.cpp:48-68 lookup + kernels_scalar.cpp:95-101 gather_rows for an
+ * explicit id list (host ids, host f32 out n x F; hits/misses counted). */
+a3g_status a3g_gather_rows(a3g_graph* g, a3g_cache* c, const uint32_t* ids, uint64_t n, float* out,
+                           uint64_t* hits, uint64_t* misses);
+
+/* sampler.cpp:9-42 / 44-58 on one explicit neighbour list, on the device
+ * (test hook; weights arbitrary > 0). Draws start at counter ctr0+1 of
+ * stream key `key` (rng.hpp:43-46). Returns the reservoir in slot order. */
+a3g_status a3g_weighted_reservoir(const uint32_t* nbrs, const double* weights, uint64_t n,
+                                  uint32_t m, uint64_t key, uint64_t ctr0, uint32_t* out,
+                                  uint64_t* count);
+a3g_status a3g_uniform_reservoir(const uint32_t* nbrs, uint64_t n, uint32_t m, uint64_t key,
+                                 uint64_t ctr0, uint32_t* out, uint64_t* count);
+
+/* ------------------------------------------------------------- trainer --- */
+/* trainer.cpp:12-28 init_model (Glorot-uniform from RngStream(seed, 0x6a10)). */
+a3g_status a3g_init_model(uint32_t feat_dim, uint32_t hidden_dim, uint32_t num_classes, uint64_t seed,
+                          double* w1, double* w2);
+
+/* 2-layer mean-GCN (trainer.hpp:24-60) in fp32 on the device. Weights are
+ * initialised as init_model (trainer.cpp:12-28) from model_seed. */
+a3g_status a3g_trainer_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds,
+                              const uint32_t* fanouts, uint32_t num_layers, uint32_t hidden_dim,
+                              uint32_t num_classes, double learning_rate, uint64_t model_seed,
+                              a3g_trainer** out);
+void a3g_trainer_destroy(a3g_trainer* t);
+/* Set/get weights (row-major W1 FxH, W2 HxC) as f64 host arrays. */
+a3g_status a3g_trainer_set_weights(a3g_trainer* t, const double* w1, const double* w2);
+a3g_status a3g_trainer_get_weights(a3g_trainer* t, double* w1, double* w2);
+/* Attach a communicator for the data-parallel gradient sum (NULL detaches). */
+a3g_status a3g_trainer_set_comm(a3g_trainer* t, a3g_comm* comm);
+
+/* One step on one batch: sample_khop -> gather+aggregate -> forward ->
+ * backward -> [allreduce] -> sgd (trainer.cpp:385-406). lr < 0 uses the
+ * trainer's learning rate; lr = 0 computes gradients only. loss_out (host)
+ * may be NULL (no sync). */
+a3g_status a3g_train_step(a3g_trainer* t, const uint32_t* seeds, uint32_t n_seeds,
+                          int seeds_on_device, double bias_rate, int kind, uint64_t rng_seed,
+                          double lr, double* loss_out);
+
+/* K pipelined steps: batch i = seeds[i*B .. (i+1)*B) (host), step seed
+ * rng_seeds[i]; sampling of batch i+1 overlaps compute of batch i on a second
+ * stream (the CUDA-stream replacement of pipeline_exec.cpp:229-276).
+ * losses_out: host f64[K] (read back once at the end). */
+a3g_status a3g_train_steps(a3g_trainer* t, const uint32_t* seeds, uint32_t batch_size,
+                           uint32_t num_steps, const uint64_t* rng_seeds, double bias_rate,
+                           int kind, int seeds_on_device, double* losses_out);
+
+/* Debug/parity copy-out of the last step (host f64 buffers; NULL skips):
+ * gradients (F*H, H*C), and ForwardResult arrays (trainer.hpp:49-60). */
+a3g_status a3g_trainer_last_grads(a3g_trainer* t, double* gw1, double* gw2);
+a3g_status a3g_trainer_last_forward(a3g_trainer* t, uint64_t* n_inner, double* logits,
+                                    double* agg_inner, double* h1, double* agg_outer);
+a3g_sampler* a3g_trainer_sampler(a3g_trainer* t, int slot);
+
+/* Device-time breakdown of the last a3g_train_steps call (CUDA events on the
+ * launching streams): total ms, and the average per-launch ms of the
+ * gather+aggregation kernel (the roofline kernel) with its algorithmic bytes. */
+a3g_status a3g_trainer_timing(a3g_trainer* t, double* total_ms, double* agg_kernel_ms,
+                              double* agg_bytes_per_launch, uint64_t* launches_per_step);
+
+/* ---------------------------------------------------------------- comm --- */
+/* NCCL communicator for data-parallel gradient sync (trainer.cpp:213-229 ->
+ * allreduce(sum) of n_k-weighted gradients). unique_id is 128 opaque bytes. */
+a3g_status a3g_comm_unique_id(uint8_t unique_id[128]);
+a3g_status a3g_comm_create(const uint8_t unique_id[128], int nranks, int rank, int device,
+                           a3g_comm** out);
+void a3g_comm_destroy(a3g_comm* c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* A3G_H_ */

@@ -1,0 +1,99 @@
+// a3g_internal.cuh -- shared device/host definitions of the B200 hot path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/a3g.h"
+
+namespace a3g {
+
+// ------------------------------------------------------------ errors -------
+struct Error : std::runtime_error {
+  a3g_status status;
+  Error(a3g_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+[[noreturn]] inline void raise(a3g_status s, const std::string& m) { throw Error(s, m); }
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    raise(e == cudaErrorMemoryAllocation ? A3G_ERR_OOM : A3G_ERR_CUDA,
+          std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+#define A3G_CUDA(x) ::a3g::cuda_check((x), #x)
+#define A3G_LAUNCH_CHECK(name) ::a3g::cuda_check(cudaGetLastError(), name)
+
+// ------------------------------------------------------------ RNG ----------
+// include/a3gnn/rng.hpp:13-55, bit-exact on the device.
+constexpr uint64_t kPhi = 0x9e3779b97f4a7c15ull;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xbf58476d1ce4e5b9ull;
+  z ^= z >> 27;
+  z *= 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  return z;
+}
+__host__ __device__ __forceinline__ uint64_t hash2(uint64_t a, uint64_t b) {
+  return mix64(a ^ mix64(b + kPhi));
+}
+__host__ __device__ __forceinline__ uint64_t hash3(uint64_t a, uint64_t b, uint64_t c) {
+  return hash2(hash2(a, b), c);
+}
+// i-th draw (1-based) of stream `key` (rng.hpp:43-46)
+__host__ __device__ __forceinline__ uint64_t draw(uint64_t key, uint64_t i) {
+  return mix64(key + i * kPhi);
+}
+// next_unit (rng.hpp:49): 53-bit uniform in [0,1)
+__host__ __device__ __forceinline__ double unit_of(uint64_t x) {
+  return (double)(x >> 11) * 0x1.0p-53;
+}
+
+// ------------------------------------------------------------ limits -------
+constexpr int kMaxLayers = 8;
+constexpr uint32_t kInv = 0xffffffffu;
+
+// Device-resident per-batch counters (one struct per sampler arena).
+struct BatchCounters {
+  uint32_t nfront[kMaxLayers + 1];  // frontier size of layer l (nfront[0] = unique seeds)
+  uint32_t ucount[kMaxLayers + 1];  // |unique| after phase p (p=0 seeds, p=l+1 after layer l)
+  uint32_t edges[kMaxLayers];       // E_l
+  uint32_t work[kMaxLayers];        // dynamic row counters of the sampling kernels
+  uint32_t n_seeds;                 // seeds given (incl. duplicates)
+  uint32_t hits, misses;            // retrieve_features accounting
+  uint32_t pad;
+};
+
+}  // namespace a3g
+
+// ---------------------------------------------------------- handles --------
+struct a3g_graph {
+  int device = 0;
+  uint64_t n = 0, m = 0;
+  uint32_t F = 0;
+  uint32_t pitch = 0;  // feature row pitch in elements (multiple of 8)
+  int feat_dtype = A3G_FEAT_F32;
+  uint64_t* d_ro = nullptr;
+  uint32_t* d_col = nullptr;
+  void* d_feat = nullptr;  // n x pitch (f32 or bf16), zero padded
+  uint32_t* d_labels = nullptr;
+  std::vector<uint64_t> h_ro;       // host copy (validation, degrees)
+  std::vector<uint32_t> h_labels;   // host copy
+  bool has_features = false;
+};
+
+struct a3g_cache {
+  a3g_graph* g = nullptr;
+  std::vector<int32_t> device_map;
+  uint32_t num_devices = 1;
+  uint64_t total_cached = 0;
+  uint32_t* d_bits = nullptr;  // n bits: cached on any device
+  bool all_cached = false, none_cached = true;
+};
+
+struct a3g_comm;

@@ -1,0 +1,67 @@
+// sampler.cuh -- k-hop sampler arena (device twin of sampling::SampleBatch,
+// sampler.hpp:30-46) and its launch entry points.
+#pragma once
+
+#include "a3g_internal.cuh"
+
+namespace a3g {
+
+// Per-layer CSR block, padded: row k (frontier node k) owns slots
+// [k*f, k*f + cnt[k]). The reference's edge list of layer l is the row-major
+// walk over valid slots (sampler.cpp:125-127).
+struct LayerArena {
+  uint32_t f = 0;           // fanout
+  uint64_t cap_rows = 0;    // frontier capacity
+  uint32_t* front = nullptr;      // frontier node ids            [cap_rows]
+  uint32_t* front_idx = nullptr;  // unique index of frontier node [cap_rows]
+  uint32_t* cnt = nullptr;        // sampled count per row          [cap_rows]
+  uint32_t* S = nullptr;          // sampled node ids               [cap_rows*f]
+  uint32_t* sidx = nullptr;       // unique index of sampled node   [cap_rows*f]
+  double* scratch = nullptr;      // reservoir keys for f > 32 rows [cap_rows*f]
+};
+
+struct SamplerState {
+  a3g_graph* g = nullptr;
+  a3g_cache* c = nullptr;
+  uint32_t max_seeds = 0;
+  uint32_t L = 0;
+  std::vector<uint32_t> fanouts;
+  LayerArena layer[kMaxLayers];
+  uint64_t cap_unique = 0;
+  uint64_t cap_inner = 0;
+  uint32_t* d_seeds = nullptr;     // [max_seeds]
+  uint32_t* d_front0 = nullptr;    // unique seeds (frontier 0)
+  uint32_t* d_unique = nullptr;    // [cap_unique]
+  int32_t* d_inv1 = nullptr;       // unique idx (< n_inner) -> row in layer-1 frontier, -1 if none
+  uint64_t* d_first = nullptr;     // [n] tagged first position (tag<<32 | ~pos)
+  uint64_t* d_gidx = nullptr;      // [n] tagged global index   (gtag<<32 | idx)
+  uint4* d_blk = nullptr;          // block partials of the finalize scans
+  uint64_t blk_cap = 0;
+  BatchCounters* d_ctr = nullptr;
+  BatchCounters* h_ctr = nullptr;  // pinned mirror
+  uint32_t* h_seeds = nullptr;     // pinned staging of host seeds
+  uint32_t tag = 0;                // first-position tag (per phase)
+  uint32_t gtag = 0;               // interner tag (per batch)
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  // last batch parameters
+  uint32_t last_n_seeds = 0;
+  bool has_batch = false;
+  int sm_count = 148;
+};
+
+// Launch the whole k-hop sample for seeds already in s.d_seeds (n_seeds on host).
+void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, uint64_t rng_seed,
+                   cudaStream_t st);
+// Single explicit neighbour list (test hook for a3g_*_reservoir).
+void launch_reservoir_list(const uint32_t* d_nb, const double* d_w, uint64_t deg, uint32_t m,
+                           uint64_t key, uint64_t c0, int kind, uint32_t* d_out, double* d_keys,
+                           cudaStream_t st);
+// Gather unique rows to `out` (device f32, F contiguous) and count hits/misses.
+void launch_gather_unique(SamplerState& s, float* out, cudaStream_t st);
+
+}  // namespace a3g
+
+struct a3g_sampler {
+  a3g::SamplerState st;
+};

@@ -1,0 +1,57 @@
+// trainer.cuh -- device state of the 2-layer mean-GCN step (trainer.hpp:24-60).
+#pragma once
+
+#include "sampler.cuh"
+
+namespace a3g {
+
+struct TrainerState {
+  a3g_graph* g = nullptr;
+  a3g_cache* c = nullptr;
+  a3g_sampler* smp[2] = {nullptr, nullptr};  // ping-pong arenas (pipeline depth 2)
+  uint32_t F = 0, H = 0, C = 0, pitch = 0, L = 0, max_seeds = 0;
+  double lr = 0.2;
+  uint64_t cap_inner = 0;
+  float* d_w1 = nullptr;   // F x H
+  float* d_w2 = nullptr;   // H x C
+  float* d_gw = nullptr;   // [F*H | H*C | n_k | loss*n_k]  (packed for the allreduce)
+  float* d_agg_inner = nullptr;  // cap_inner x pitch
+  float* d_h1 = nullptr;         // cap_inner x H (post-ReLU)
+  float* d_dh1 = nullptr;        // cap_inner x H
+  float* d_agg_outer = nullptr;  // max_seeds x H
+  float* d_logits = nullptr;     // max_seeds x C
+  float* d_dlogits = nullptr;    // max_seeds x C
+  float* d_loss_s = nullptr;     // max_seeds
+  float* d_part = nullptr;       // nparts x F x H
+  uint32_t nparts = 0;
+  double* d_losses = nullptr;    // per-step losses of train_steps
+  uint64_t losses_cap = 0;
+  unsigned long long* d_agg_bytes = nullptr;  // algorithmic bytes moved by k_agg1 (accumulated)
+  uint32_t* d_seed_buf = nullptr;  // device copy of all batches' seeds (train_steps)
+  uint64_t seed_buf_cap = 0;
+  uint32_t* h_seed_stage = nullptr;  // pinned staging
+  uint64_t h_seed_cap = 0;
+  double* h_losses = nullptr;        // pinned
+  cudaStream_t s_comp = nullptr, s_samp = nullptr;
+  cudaEvent_t ev_sampled[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
+  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
+  std::vector<cudaEvent_t> ev_agg;  // pairs around k_agg1 launches (timing)
+  bool timing = true;
+  double last_total_ms = 0, last_agg_ms = 0, last_agg_bytes = 0;
+  uint64_t last_agg_launches = 0;
+  a3g_comm* comm = nullptr;
+  int sm_count = 148;
+  size_t agg_smem = 0;
+  bool fused_gemm = true;
+};
+
+// Compute part of one step on s_comp for the batch in arena `smp`
+// (gather+aggregate -> forward -> backward -> [allreduce] -> sgd).
+void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* d_loss_slot,
+                          cudaStream_t st, bool record_timing);
+
+}  // namespace a3g
+
+struct a3g_trainer {
+  a3g::TrainerState st;
+};

@@ -64,6 +64,8 @@ struct BatchCounters {
   uint32_t ucount[kMaxLayers + 1];  // |unique| after phase p (p=0 seeds, p=l+1 after layer l)
   uint32_t edges[kMaxLayers];       // E_l
   uint32_t work[kMaxLayers];        // dynamic row counters of the sampling kernels
+  uint32_t hubs[kMaxLayers];        // hub rows registered per layer
+  uint32_t segs[kMaxLayers];        // hub segments reserved per layer
   uint32_t n_seeds;                 // seeds given (incl. duplicates)
   uint32_t hits, misses;            // retrieve_features accounting
   uint32_t pad;

@@ -110,6 +110,23 @@ void sampler_alloc(SamplerState& s, a3g_graph* g, a3g_cache* c, uint32_t max_see
   A3G_CUDA(cudaMemset(s.d_first, 0, n * sizeof(uint64_t)));
   A3G_CUDA(cudaMemset(s.d_gidx, 0, n * sizeof(uint64_t)));
   s.d_blk = dalloc<uint4>(s.blk_cap);
+  // hub-splitting arena: every frontier row could be a hub; the segment pool
+  // covers sum(deg)/kSeg of a layer's hubs up to 64K segments (rows beyond
+  // capacity fall back to the in-row warp replay, still exact).
+  uint64_t max_rows = 0;
+  for (uint32_t l = 0; l < L; ++l) max_rows = std::max<uint64_t>(max_rows, s.layer[l].cap_rows);
+  HubArena& hb = s.hub;
+  hb.hub_cap = static_cast<uint32_t>(std::max<uint64_t>(1, max_rows));
+  hb.seg_cap = static_cast<uint32_t>(std::min<uint64_t>(65536, std::max<uint64_t>(1, g->m / kSeg + max_rows)));
+  hb.row = dalloc<uint32_t>(hb.hub_cap);
+  hb.seg0 = dalloc<uint32_t>(hb.hub_cap);
+  hb.nseg = dalloc<uint32_t>(hb.hub_cap);
+  hb.seg_hub = dalloc<uint32_t>(hb.seg_cap);
+  hb.rec_cnt = dalloc<uint32_t>(hb.seg_cap);
+  hb.tau = dalloc<double>(hb.seg_cap);
+  hb.rec_id = dalloc<uint32_t>(static_cast<size_t>(hb.seg_cap) * kRecCap);
+  hb.rec_key = dalloc<double>(static_cast<size_t>(hb.seg_cap) * kRecCap);
+  hb.slot_last = dalloc<uint32_t>(static_cast<size_t>(hb.seg_cap) * 32);
   s.d_ctr = dalloc<BatchCounters>(1);
   A3G_CUDA(cudaMallocHost(&s.h_ctr, sizeof(BatchCounters)));
   A3G_CUDA(cudaMallocHost(&s.h_seeds, max_seeds * sizeof(uint32_t)));
@@ -133,6 +150,15 @@ void sampler_free(SamplerState& s) {
   dfree(s.d_first);
   dfree(s.d_gidx);
   dfree(s.d_blk);
+  dfree(s.hub.row);
+  dfree(s.hub.seg0);
+  dfree(s.hub.nseg);
+  dfree(s.hub.seg_hub);
+  dfree(s.hub.rec_cnt);
+  dfree(s.hub.tau);
+  dfree(s.hub.rec_id);
+  dfree(s.hub.rec_key);
+  dfree(s.hub.slot_last);
   dfree(s.d_ctr);
   if (s.h_ctr) cudaFreeHost(s.h_ctr);
   if (s.h_seeds) cudaFreeHost(s.h_seeds);
@@ -598,7 +624,7 @@ a3g_status a3g_trainer_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds, co
         sampler_alloc(t.smp[i]->st, g, c, max_seeds, fanouts, L);
       }
       t.cap_inner = std::max<uint64_t>(1, t.smp[0]->st.cap_inner);
-      t.agg_smem = (static_cast<size_t>(t.F) * H + 8ull * g->pitch) * sizeof(float);
+      t.agg_smem = ((static_cast<size_t>(t.F) * H + 7) / 8 * 8 + 8ull * g->pitch) * sizeof(float);
       if (t.agg_smem > 227 * 1024)
         raise(A3G_ERR_PARAMETER, "trainer: feat_dim*hidden_dim too large for the fused aggregation");
       t.d_w1 = dalloc<float>(static_cast<size_t>(t.F) * H);

@@ -7,15 +7,22 @@
 // relabelling (Interner, sampler.cpp:72-85) and per-layer first-seen frontiers
 // (sampler.cpp:113-131).
 //
-// Per phase (seeds, then each layer):
-//   k_sample_layer  warp per frontier row (dynamic chunks): reservoir in
-//                   registers (slot = lane), writes padded row + atomicMax of
-//                   the tagged first position of every sampled node;
-//   k_fin_count     per 2048-position tile: #valid, #first-in-layer, #new;
-//   k_fin_emit      tile prefix from the block partials + ballot scans: emits
-//                   next frontier (first-seen order), new unique nodes
-//                   (global first-seen order) and their tagged indices.
-// Counts stay on the device, so no host sync inside a batch.
+// Per layer:
+//   k_sample_rows   warp per frontier row (dynamic chunks of rows). deg <= m:
+//                   copy; m < deg <= kSeg: in-warp exact replay (slot = lane,
+//                   ballot of keys > current min, 4-chunk prefetch); deg > kSeg
+//                   ("hubs", up to n-1 neighbours): registered for splitting.
+//   k_hub_segments  warp per kSeg-long segment of a hub row: local replay from
+//                   an empty reservoir, emitting every local insertion
+//                   ("record") and the segment's exact m-th largest key tau_s.
+//                   Every global insertion is a local record of its segment.
+//   k_hub_merge     block per hub: records of segment s with key <= max_{s'<s}
+//                   tau_{s'} can never beat the global minimum and are dropped
+//                   in parallel; warp 0 replays the survivors in order, which
+//                   reproduces the sequential slot history exactly.
+//   k_fin_count / k_fin_emit: first-seen dedup + relabel (tagged atomicMax of
+//                   the first position, tile partials, ballot scans).
+// Counts stay on the device: no host sync inside a batch.
 #include <cmath>
 
 #include "sampler.cuh"
@@ -25,6 +32,7 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kRowChunk = 4;  // rows claimed per atomic by a warp
+constexpr int kPrefetch = 4;  // 32-key chunks loaded ahead per replay step
 
 __device__ __forceinline__ void warp_argmin(double& k, int& idx) {
 #pragma unroll
@@ -61,6 +69,9 @@ struct SampleArgs {
   uint64_t* first;
   uint32_t* work;
   double* scratch;  // [cap_rows*f] keys, only for f > 32 serial path
+  HubArena hub;
+  uint32_t* hub_count;
+  uint32_t* seg_count;
   uint64_t seed;
   double gamma, inv_gamma;
   uint32_t f, layer, tag;
@@ -72,8 +83,150 @@ __device__ __forceinline__ bool is_gamma(const SampleArgs& a, uint32_t v) {
   return a.wmode == 1 || (a.wmode == 2 && ((__ldg(a.bits + (v >> 5)) >> (v & 31)) & 1u));
 }
 
+// Weight of neighbour j (node v): assign_weights (sampler.cpp:60-68).
+struct BitmapWeight {
+  const SampleArgs* a;
+  __device__ __forceinline__ bool unit(uint32_t v, uint64_t) const { return !is_gamma(*a, v); }
+  __device__ __forceinline__ double inv_w(uint32_t, uint64_t) const { return a->inv_gamma; }
+};
+struct ListWeight {  // explicit weights (test hook a3g_weighted_reservoir)
+  const double* w;
+  __device__ __forceinline__ bool unit(uint32_t, uint64_t j) const { return w[j] == 1.0; }
+  __device__ __forceinline__ double inv_w(uint32_t, uint64_t j) const { return 1.0 / w[j]; }
+};
+
+// Reservoir state of one warp: slot = lane (m <= 32), lanes >= m hold +inf.
+struct WState {
+  double my_key;
+  uint32_t my_id;
+  double thr;  // current minimum key (keys[min_pos])
+  int mp;      // min_pos: first slot holding the minimum (std::min_element)
+};
+
+struct NoEmit {
+  __device__ __forceinline__ void operator()(uint32_t, double, int) const {}
+};
+
+// Fill slots [0, nf) from positions j0 + lane (sampler.cpp:30-33); every fill
+// is an insertion. Draw number of position j is c0 + j + 1.
+template <typename WF, typename Emit>
+__device__ __forceinline__ void fill_slots(const uint32_t* nb, uint64_t j0, uint32_t nf, uint64_t key,
+                                           uint64_t c0, int lane, const WF& wf, WState& s, const Emit& emit) {
+  s.my_key = INFINITY;
+  s.my_id = 0;
+  if (lane < static_cast<int>(nf)) {
+    const uint64_t j = j0 + lane;
+    const uint32_t v = __ldg(nb + j);
+    const double u = unit_of(draw(key, c0 + j + 1));
+    s.my_key = wf.unit(v, j) ? u : pow(u, wf.inv_w(v, j));
+    s.my_id = v;
+    emit(v, s.my_key, lane);
+  }
+  s.thr = s.my_key;
+  s.mp = lane;
+  warp_argmin(s.thr, s.mp);
+}
+
+// Replay positions [jb, je) against a full reservoir (sampler.cpp:34-39):
+// a key replaces slot min_pos iff strictly greater than keys[min_pos]; then
+// min_pos = first minimum. Chunks of 32 keys, kPrefetch chunks in flight.
+// With a single non-unit weight (use_filter) a gamma-key is only evaluated
+// (pow) when u >= thr^gamma*(1-1e-6): below that, pow(u,1/gamma) < thr for any
+// <= 2-ulp pow, so no decision can change.
+template <typename WF, typename Emit>
+__device__ __forceinline__ void replay_range(const uint32_t* nb, uint64_t jb, uint64_t je, uint64_t key,
+                                             uint64_t c0, int lane, const WF& wf, bool use_filter,
+                                             double gamma, WState& s, const Emit& emit) {
+  double lo = use_filter ? gamma_lo(s.thr, gamma) : 0.0;
+  for (uint64_t b = jb; b < je; b += 32 * kPrefetch) {
+    uint32_t v[kPrefetch];
+    double kk[kPrefetch];
+#pragma unroll
+    for (int q = 0; q < kPrefetch; ++q) {
+      const uint64_t j = b + q * 32 + lane;
+      v[q] = j < je ? __ldg(nb + j) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < kPrefetch; ++q) {
+      const uint64_t j = b + q * 32 + lane;
+      kk[q] = -1.0;
+      if (j < je) {
+        const double u = unit_of(draw(key, c0 + j + 1));
+        if (wf.unit(v[q], j)) {
+          kk[q] = u;
+        } else if (u >= lo) {
+          kk[q] = pow(u, wf.inv_w(v[q], j));
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kPrefetch; ++q) {
+      unsigned mask = __ballot_sync(kFull, kk[q] > s.thr);
+      if (mask) {
+        while (mask) {
+          const int src = __ffs(mask) - 1;
+          const double kv = __shfl_sync(kFull, kk[q], src);
+          const uint32_t iv = __shfl_sync(kFull, v[q], src);
+          if (lane == s.mp) {
+            s.my_key = kv;
+            s.my_id = iv;
+          }
+          emit(iv, kv, src);
+          s.thr = s.my_key;
+          s.mp = lane;
+          warp_argmin(s.thr, s.mp);
+          mask &= __ballot_sync(kFull, kk[q] > s.thr) & ~((2u << src) - 1u);
+        }
+        if (use_filter) lo = gamma_lo(s.thr, gamma);
+      }
+    }
+  }
+}
+
+// Weighted reservoir of one whole row by one warp, m <= 32 < deg.
+template <typename WF>
+__device__ __forceinline__ uint32_t weighted_row_warp(const uint32_t* nb, uint64_t deg, uint32_t m,
+                                                      uint64_t key, int lane, const WF& wf,
+                                                      bool use_filter, double gamma, uint64_t c0 = 0) {
+  WState s;
+  fill_slots(nb, 0, m, key, c0, lane, wf, s, NoEmit{});
+  replay_range(nb, m, deg, key, c0, lane, wf, use_filter, gamma, s, NoEmit{});
+  return s.my_id;
+}
+
+// Algorithm R (sampler.cpp:44-58) by one warp over positions [jb, je), jb >=
+// m: slot r of position j is replaced iff r = next_below(j+1) < m (draw number
+// c0 + j - m + 1); candidates applied in position order.
+__device__ __forceinline__ void uniform_range(const uint32_t* nb, uint64_t jb, uint64_t je, uint32_t m,
+                                              uint64_t key, int lane, uint64_t c0, uint32_t& my_id) {
+  for (uint64_t b = jb; b < je; b += 32) {
+    const uint64_t j = b + lane;
+    const bool valid = j < je;
+    uint32_t r = kInv, v = 0;
+    if (valid) {
+      r = static_cast<uint32_t>(__umul64hi(draw(key, c0 + j - m + 1), j + 1));
+      if (r < m) v = __ldg(nb + j);
+    }
+    unsigned mask = __ballot_sync(kFull, valid && r < m);
+    while (mask) {
+      const int src = __ffs(mask) - 1;
+      const uint32_t slot = __shfl_sync(kFull, r, src);
+      const uint32_t iv = __shfl_sync(kFull, v, src);
+      if (lane == static_cast<int>(slot)) my_id = iv;
+      mask &= mask - 1;
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t uniform_row_warp(const uint32_t* nb, uint64_t deg, uint32_t m,
+                                                     uint64_t key, int lane, uint64_t c0 = 0) {
+  uint32_t my_id = lane < static_cast<int>(m) ? __ldg(nb + lane) : 0u;
+  uniform_range(nb, m, deg, m, key, lane, c0, my_id);
+  return my_id;
+}
+
 // Thread-serial exact reservoir for rows with f > 32 (rare; e.g. exhaustive
-// fanouts). Writes S/scratch of the row directly.
+// fanouts). Writes the row's slots and keys directly.
 __device__ void serial_row(const SampleArgs& a, const uint32_t* nb, uint64_t deg, uint64_t key,
                            uint32_t* out, double* keys) {
   const uint32_t m = a.f;
@@ -108,102 +261,26 @@ __device__ void serial_row(const SampleArgs& a, const uint32_t* nb, uint64_t deg
   }
 }
 
-// Weight of neighbour j (node v): assign_weights (sampler.cpp:60-68).
-struct BitmapWeight {
-  const SampleArgs* a;
-  __device__ __forceinline__ bool unit(uint32_t v, uint64_t) const { return !is_gamma(*a, v); }
-  __device__ __forceinline__ double inv_w(uint32_t, uint64_t) const { return a->inv_gamma; }
-};
-struct ListWeight {  // explicit weights (test hook a3g_weighted_reservoir)
-  const double* w;
-  __device__ __forceinline__ bool unit(uint32_t, uint64_t j) const { return w[j] == 1.0; }
-  __device__ __forceinline__ double inv_w(uint32_t, uint64_t j) const { return 1.0 / w[j]; }
-};
-
-// Weighted reservoir of one neighbour list by one warp, m <= 32 < deg
-// (sampler.cpp:24-40): slot = lane; fill the first m, then replay the
-// "record" insertions chunk by chunk: ballot of keys > current minimum
-// (strict), apply in neighbour order, argmin ties -> lowest slot
-// (std::min_element). With a single non-unit weight gamma (use_filter), a
-// gamma-key is only evaluated (pow) when u >= thr^gamma*(1-1e-6): below that
-// bound pow(u,1/gamma) < thr for any <= 2-ulp pow, so no decision changes.
-// Returns the slot content of this lane.
-template <typename WF>
-__device__ __forceinline__ uint32_t weighted_row_warp(const uint32_t* nb, uint64_t deg, uint32_t m,
-                                                      uint64_t key, int lane, const WF& wf,
-                                                      bool use_filter, double gamma, uint64_t c0 = 0) {
-  uint32_t my_id = 0;
-  double my_key = INFINITY;
+// Whole row by one warp (m <= 32 < deg); writes slots + first-position marks.
+__device__ __forceinline__ void row_by_warp(const SampleArgs& a, const uint32_t* nb, uint64_t deg, uint64_t key,
+                                            uint32_t k, int lane) {
+  const uint32_t m = a.f;
+  uint32_t my_id;
+  if (a.kind == A3G_SAMPLER_UNIFORM) {
+    my_id = uniform_row_warp(nb, deg, m, key, lane);
+  } else {
+    const BitmapWeight wf{&a};
+    my_id = weighted_row_warp(nb, deg, m, key, lane, wf, a.wmode != 0, a.gamma);
+  }
+  const uint64_t row0 = static_cast<uint64_t>(k) * m;
   if (lane < static_cast<int>(m)) {
-    const uint32_t v = __ldg(nb + lane);
-    const double u = unit_of(draw(key, c0 + lane + 1));
-    my_key = wf.unit(v, lane) ? u : pow(u, wf.inv_w(v, lane));
-    my_id = v;
+    a.S[row0 + lane] = my_id;
+    mark_first(a.first, my_id, a.tag, static_cast<uint32_t>(row0 + lane));
   }
-  double thr = my_key;
-  int mp = lane;
-  warp_argmin(thr, mp);
-  double lo = use_filter ? gamma_lo(thr, gamma) : 0.0;
-  for (uint64_t b = m; b < deg; b += 32) {
-    const uint64_t j = b + lane;
-    double kk = -1.0;
-    uint32_t v = 0;
-    if (j < deg) {
-      v = __ldg(nb + j);
-      const double u = unit_of(draw(key, c0 + j + 1));
-      if (wf.unit(v, j)) {
-        kk = u;
-      } else if (u >= lo) {
-        kk = pow(u, wf.inv_w(v, j));
-      }
-    }
-    unsigned mask = __ballot_sync(kFull, kk > thr);
-    if (mask) {
-      while (mask) {
-        const int src = __ffs(mask) - 1;
-        const double kv = __shfl_sync(kFull, kk, src);
-        const uint32_t iv = __shfl_sync(kFull, v, src);
-        if (lane == mp) {
-          my_key = kv;
-          my_id = iv;
-        }
-        thr = my_key;
-        mp = lane;
-        warp_argmin(thr, mp);
-        mask &= __ballot_sync(kFull, kk > thr) & ~((2u << src) - 1u);
-      }
-      if (use_filter) lo = gamma_lo(thr, gamma);
-    }
-  }
-  return my_id;
+  if (lane == 0) a.cnt[k] = m;
 }
 
-// Algorithm R (sampler.cpp:44-58) by one warp, m <= 32 < deg: slot r of
-// neighbour j >= m is replaced iff r = next_below(j+1) < m, draw number j-m+1.
-__device__ __forceinline__ uint32_t uniform_row_warp(const uint32_t* nb, uint64_t deg, uint32_t m,
-                                                     uint64_t key, int lane, uint64_t c0 = 0) {
-  uint32_t my_id = lane < static_cast<int>(m) ? __ldg(nb + lane) : 0u;
-  for (uint64_t b = m; b < deg; b += 32) {
-    const uint64_t j = b + lane;
-    const bool valid = j < deg;
-    uint32_t r = kInv, v = 0;
-    if (valid) {
-      r = static_cast<uint32_t>(__umul64hi(draw(key, c0 + j - m + 1), j + 1));
-      if (r < m) v = __ldg(nb + j);
-    }
-    unsigned mask = __ballot_sync(kFull, valid && r < m);
-    while (mask) {
-      const int src = __ffs(mask) - 1;
-      const uint32_t slot = __shfl_sync(kFull, r, src);
-      const uint32_t iv = __shfl_sync(kFull, v, src);
-      if (lane == static_cast<int>(slot)) my_id = iv;
-      mask &= mask - 1;
-    }
-  }
-  return my_id;
-}
-
-__global__ void __launch_bounds__(256) k_sample_layer(SampleArgs a) {
+__global__ void __launch_bounds__(256) k_sample_rows(SampleArgs a) {
   const int lane = threadIdx.x & 31;
   const uint32_t nrows = *a.nrows;
   const uint32_t m = a.f;
@@ -236,19 +313,247 @@ __global__ void __launch_bounds__(256) k_sample_layer(SampleArgs a) {
         if (lane == 0) a.cnt[k] = m;
         continue;
       }
-      uint32_t my_id = 0;
-      if (a.kind == A3G_SAMPLER_UNIFORM) {
-        my_id = uniform_row_warp(nb, deg, m, key, lane);
-      } else {
-        const BitmapWeight wf{&a};
-        my_id = weighted_row_warp(nb, deg, m, key, lane, wf, a.wmode != 0, a.gamma);
+      if (deg > kSeg) {  // hub: register for the segmented path
+        const uint32_t nseg = static_cast<uint32_t>((deg + kSeg - 1) / kSeg);
+        uint32_t h = 0, s0 = 0;
+        if (lane == 0) {
+          h = atomicAdd(a.hub_count, 1u);
+          s0 = atomicAdd(a.seg_count, nseg);
+          const bool ok = h < a.hub.hub_cap && s0 + static_cast<uint64_t>(nseg) <= a.hub.seg_cap;
+          if (h < a.hub.hub_cap) {
+            a.hub.row[h] = k;
+            a.hub.seg0[h] = s0;
+            a.hub.nseg[h] = ok ? nseg : 0u;  // 0 = handled here (capacity exceeded)
+          }
+          if (!ok) h = kInv;
+        }
+        h = __shfl_sync(kFull, h, 0);
+        s0 = __shfl_sync(kFull, s0, 0);
+        if (h != kInv) {
+          for (uint32_t i = lane; i < nseg; i += 32) a.hub.seg_hub[s0 + i] = h;
+          continue;
+        }
       }
-      if (lane < m) {
-        a.S[row0 + lane] = my_id;
-        mark_first(a.first, my_id, a.tag, static_cast<uint32_t>(row0 + lane));
+      row_by_warp(a, nb, deg, key, k, lane);
+    }
+  }
+}
+
+// Local replay of one hub segment [sb, se) from an empty reservoir; records =
+// every local insertion (id, key) in order; tau = segment's m-th largest key.
+struct SegEmit {
+  uint32_t* rid;
+  double* rkey;
+  uint32_t* cnt;  // warp-uniform counter (register, by reference)
+  uint32_t cap;
+  int lane;
+  __device__ __forceinline__ void operator()(uint32_t id, double key, int src) const {
+    const uint32_t c = *cnt;
+    if (lane == src && c < cap) {
+      rid[c] = id;
+      rkey[c] = key;
+    }
+    *cnt = c + 1;
+  }
+};
+struct FillEmit {  // fills: lane i writes record i (records 0..nf-1)
+  uint32_t* rid;
+  double* rkey;
+  uint32_t cap;
+  __device__ __forceinline__ void operator()(uint32_t id, double key, int lane) const {
+    if (static_cast<uint32_t>(lane) < cap) {
+      rid[lane] = id;
+      rkey[lane] = key;
+    }
+  }
+};
+
+__global__ void __launch_bounds__(256) k_hub_segments(SampleArgs a) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nhub = min(*a.hub_count, a.hub.hub_cap);
+  const uint32_t nseg_total = min(*a.seg_count, a.hub.seg_cap);
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t m = a.f;
+  for (uint32_t s = gw; s < nseg_total; s += nw) {
+    const uint32_t h = a.hub.seg_hub[s];
+    if (h >= nhub) continue;  // stale entry
+    const uint32_t s0 = a.hub.seg0[h], ns = a.hub.nseg[h];
+    if (s < s0 || s >= s0 + ns) continue;
+    const uint32_t k = a.hub.row[h];
+    const uint32_t dst = a.front[k];
+    const uint64_t beg = a.ro[dst], deg = a.ro[dst + 1] - beg;
+    const uint32_t* nb = a.col + beg;
+    const uint64_t key = hash2(a.seed, hash2(a.layer, dst));
+    const uint64_t sb = static_cast<uint64_t>(s - s0) * kSeg, se = min(deg, sb + kSeg);
+    if (a.kind == A3G_SAMPLER_UNIFORM) {
+      // last position per slot within the segment (positions >= m)
+      uint32_t last = kInv;  // lane = slot
+      const uint64_t jb = sb > m ? sb : static_cast<uint64_t>(m);
+      for (uint64_t b = jb; b < se; b += 32) {
+        const uint64_t j = b + lane;
+        uint32_t r = kInv;
+        if (j < se) r = static_cast<uint32_t>(__umul64hi(draw(key, j - m + 1), j + 1));
+        unsigned mask = __ballot_sync(kFull, j < se && r < m);
+        while (mask) {
+          const int src = __ffs(mask) - 1;
+          const uint32_t slot = __shfl_sync(kFull, r, src);
+          if (lane == static_cast<int>(slot)) last = static_cast<uint32_t>(b + src);
+          mask &= mask - 1;
+        }
+      }
+      a.hub.slot_last[static_cast<uint64_t>(s) * 32 + lane] = last;
+      continue;
+    }
+    const BitmapWeight wf{&a};
+    uint32_t* rid = a.hub.rec_id + static_cast<uint64_t>(s) * kRecCap;
+    double* rkey = a.hub.rec_key + static_cast<uint64_t>(s) * kRecCap;
+    const uint32_t nf = static_cast<uint32_t>(se - sb < m ? se - sb : m);
+    WState st;
+    fill_slots(nb, sb, nf, key, 0, lane, wf, st, FillEmit{rid, rkey, kRecCap});
+    uint32_t cnt = nf;
+    double tau = -1.0;
+    if (se - sb >= m) {
+      SegEmit em{rid, rkey, &cnt, kRecCap, lane};
+      replay_range(nb, sb + m, se, key, 0, lane, wf, a.wmode != 0, a.gamma, st, em);
+      tau = st.thr;
+    }
+    if (lane == 0) {
+      a.hub.rec_cnt[s] = cnt;
+      a.hub.tau[s] = tau;
+    }
+  }
+}
+
+constexpr int kMergeWarps = 8;
+
+__global__ void __launch_bounds__(kMergeWarps * 32) k_hub_merge(SampleArgs a) {
+  __shared__ uint32_t s_id[kMergeWarps][kRecCap];
+  __shared__ double s_key[kMergeWarps][kRecCap];
+  __shared__ uint32_t s_n[kMergeWarps];
+  __shared__ double s_lrun;
+  __shared__ int s_overflow;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t nhub = min(*a.hub_count, a.hub.hub_cap);
+  const uint32_t m = a.f;
+  for (uint32_t h = blockIdx.x; h < nhub; h += gridDim.x) {
+    const uint32_t ns = a.hub.nseg[h];
+    if (ns == 0) continue;  // processed by k_sample_rows
+    const uint32_t s0 = a.hub.seg0[h], k = a.hub.row[h];
+    const uint32_t dst = a.front[k];
+    const uint64_t beg = a.ro[dst], deg = a.ro[dst + 1] - beg;
+    const uint32_t* nb = a.col + beg;
+    const uint64_t key = hash2(a.seed, hash2(a.layer, dst));
+    const uint64_t row0 = static_cast<uint64_t>(k) * m;
+    if (a.kind == A3G_SAMPLER_UNIFORM) {
+      if (warp == 0) {
+        uint32_t my_id = lane < static_cast<int>(m) ? nb[lane] : 0u;
+        for (int s = static_cast<int>(ns) - 1; s >= 0; --s) {
+          const uint32_t last = a.hub.slot_last[static_cast<uint64_t>(s0 + s) * 32 + lane];
+          if (last != kInv) {
+            my_id = nb[last];
+            break;
+          }
+        }
+        if (lane < static_cast<int>(m)) {
+          a.S[row0 + lane] = my_id;
+          mark_first(a.first, my_id, a.tag, static_cast<uint32_t>(row0 + lane));
+        }
+        if (lane == 0) a.cnt[k] = m;
+      }
+      __syncthreads();
+      continue;
+    }
+    if (threadIdx.x == 0) {
+      s_lrun = -1.0;
+      int of = 0;
+      for (uint32_t s = 0; s < ns; ++s) of |= a.hub.rec_cnt[s0 + s] > kRecCap;
+      s_overflow = of;
+    }
+    __syncthreads();
+    if (s_overflow) {  // a segment's records overflowed: exact whole-row replay
+      if (warp == 0) row_by_warp(a, nb, deg, key, k, lane);
+      __syncthreads();
+      continue;
+    }
+    // global fill = records 0..m-1 of segment 0 (positions 0..m-1)
+    WState st;
+    if (warp == 0) {
+      const uint64_t rb = static_cast<uint64_t>(s0) * kRecCap;
+      st.my_key = lane < static_cast<int>(m) ? a.hub.rec_key[rb + lane] : INFINITY;
+      st.my_id = lane < static_cast<int>(m) ? a.hub.rec_id[rb + lane] : 0u;
+      st.thr = st.my_key;
+      st.mp = lane;
+      warp_argmin(st.thr, st.mp);
+    }
+    for (uint32_t w0 = 0; w0 < ns; w0 += kMergeWarps) {
+      // filter: records of segment s with key <= L_s = max_{s'<s} tau_s' are dropped
+      const uint32_t s = w0 + warp;
+      uint32_t n_keep = 0;
+      if (s < ns) {
+        double L = s_lrun;
+        for (uint32_t t = w0; t < s; ++t) L = fmax(L, a.hub.tau[s0 + t]);
+        const uint64_t rb = static_cast<uint64_t>(s0 + s) * kRecCap;
+        const uint32_t rc = a.hub.rec_cnt[s0 + s];
+        for (uint32_t i0 = (s == 0 ? m : 0); i0 < rc; i0 += 32) {
+          const uint32_t i = i0 + lane;
+          double kv = -1.0;
+          uint32_t iv = 0;
+          if (i < rc) {
+            kv = a.hub.rec_key[rb + i];
+            iv = a.hub.rec_id[rb + i];
+          }
+          const bool keep = i < rc && kv > L;
+          const unsigned bm = __ballot_sync(kFull, keep);
+          if (keep) {
+            const uint32_t o = n_keep + __popc(bm & ((1u << lane) - 1u));
+            s_id[warp][o] = iv;
+            s_key[warp][o] = kv;
+          }
+          n_keep += __popc(bm);
+        }
+      }
+      if (lane == 0) s_n[warp] = n_keep;
+      __syncthreads();
+      if (warp == 0) {
+        for (int wr = 0; wr < kMergeWarps && w0 + wr < ns; ++wr) {
+          const uint32_t n = s_n[wr];
+          for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            const double kk = i < n ? s_key[wr][i] : -1.0;
+            const uint32_t v = i < n ? s_id[wr][i] : 0u;
+            unsigned mask = __ballot_sync(kFull, kk > st.thr);
+            while (mask) {
+              const int src = __ffs(mask) - 1;
+              const double kv = __shfl_sync(kFull, kk, src);
+              const uint32_t iv = __shfl_sync(kFull, v, src);
+              if (lane == st.mp) {
+                st.my_key = kv;
+                st.my_id = iv;
+              }
+              st.thr = st.my_key;
+              st.mp = lane;
+              warp_argmin(st.thr, st.mp);
+              mask &= __ballot_sync(kFull, kk > st.thr) & ~((2u << src) - 1u);
+            }
+          }
+        }
+        if (lane == 0) {
+          double L = s_lrun;
+          for (uint32_t t = w0; t < min(ns, w0 + kMergeWarps); ++t) L = fmax(L, a.hub.tau[s0 + t]);
+          s_lrun = L;
+        }
+      }
+      __syncthreads();
+    }
+    if (warp == 0) {
+      if (lane < static_cast<int>(m)) {
+        a.S[row0 + lane] = st.my_id;
+        mark_first(a.first, st.my_id, a.tag, static_cast<uint32_t>(row0 + lane));
       }
       if (lane == 0) a.cnt[k] = m;
     }
+    __syncthreads();
   }
 }
 
@@ -557,8 +862,8 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
     fa.blk = s.d_blk;
     fa.uprev = nullptr;
     fa.unique = s.d_unique;
-    fa.next_front = s.layer[0].front;
-    fa.next_front_idx = s.layer[0].front_idx;
+    fa.next_front = s.L ? s.layer[0].front : nullptr;
+    fa.next_front_idx = s.L ? s.layer[0].front_idx : nullptr;
     fa.inv = nullptr;
     fa.out_nfront = &ctr->nfront[0];
     fa.out_u = &ctr->ucount[0];
@@ -593,7 +898,10 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
     sa.S = la.S;
     sa.first = s.d_first;
     sa.work = &ctr->work[l];
-    sa.scratch = nullptr;
+    sa.scratch = la.scratch;
+    sa.hub = s.hub;
+    sa.hub_count = &ctr->hubs[l];
+    sa.seg_count = &ctr->segs[l];
     sa.seed = rng_seed;
     sa.gamma = gamma;
     sa.inv_gamma = 1.0 / gamma;
@@ -602,9 +910,14 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
     sa.tag = tag;
     sa.kind = kind;
     sa.wmode = wmode;
-    sa.scratch = la.scratch;
-    k_sample_layer<<<sample_blocks, 256, 0, st>>>(sa);
-    A3G_LAUNCH_CHECK("k_sample_layer");
+    k_sample_rows<<<sample_blocks, 256, 0, st>>>(sa);
+    A3G_LAUNCH_CHECK("k_sample_rows");
+    if (la.f <= 32) {
+      k_hub_segments<<<s.sm_count * 8, 256, 0, st>>>(sa);
+      A3G_LAUNCH_CHECK("k_hub_segments");
+      k_hub_merge<<<s.sm_count * 2, kMergeWarps * 32, 0, st>>>(sa);
+      A3G_LAUNCH_CHECK("k_hub_merge");
+    }
     FinArgs fa{};
     fa.S = la.S;
     fa.cnt = la.cnt;

@@ -20,7 +20,25 @@ struct LayerArena {
   double* scratch = nullptr;      // reservoir keys for f > 32 rows [cap_rows*f]
 };
 
+// Hub splitting (rows with deg > kSeg): per-segment local records.
+constexpr uint32_t kSeg = 2048;    // neighbours per segment
+constexpr uint32_t kRecCap = 256;  // record capacity per segment (expected ~m(1+ln(kSeg/m)) <= 90)
+
+struct HubArena {
+  uint32_t hub_cap = 0, seg_cap = 0;
+  uint32_t* row = nullptr;       // [hub_cap] frontier row of hub h
+  uint32_t* seg0 = nullptr;      // [hub_cap] first segment
+  uint32_t* nseg = nullptr;      // [hub_cap] #segments (0: handled in-row)
+  uint32_t* seg_hub = nullptr;   // [seg_cap] owning hub
+  uint32_t* rec_cnt = nullptr;   // [seg_cap]
+  double* tau = nullptr;         // [seg_cap] m-th largest key of the segment (-1: short)
+  uint32_t* rec_id = nullptr;    // [seg_cap * kRecCap]
+  double* rec_key = nullptr;     // [seg_cap * kRecCap]
+  uint32_t* slot_last = nullptr; // [seg_cap * 32] uniform kind: last position per slot
+};
+
 struct SamplerState {
+  HubArena hub;
   a3g_graph* g = nullptr;
   a3g_cache* c = nullptr;
   uint32_t max_seeds = 0;

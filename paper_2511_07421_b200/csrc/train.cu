@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kAggThreads) k_agg1(AggArgs a) {
   constexpr int EPC = Ch::EPC;
   extern __shared__ float smem[];
   float* s_w1 = smem;                                   // F x H
-  float* s_buf = smem + static_cast<size_t>(a.F) * a.H;  // kAggWarps x pitch
+  float* s_buf = smem + (static_cast<size_t>(a.F) * a.H + 7) / 8 * 8;  // kAggWarps x pitch, 32B aligned
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t i = threadIdx.x; i < a.F * a.H; i += kAggThreads) s_w1[i] = a.w1[i];
   __syncthreads();

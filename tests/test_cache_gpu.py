@@ -35,7 +35,7 @@ def test_hotness_exact_set():
     c = CA.build_static_cache(g, CA.CacheConfig(6400, 1))
     assert c.total_cached() == 100
     deg = np.diff(g.row_offsets)
-    order = sorted(range(1000), key=lambda v: (-deg[v], v))
+    order = sorted(range(1000), key=lambda v: (-int(deg[v]), v))
     assert all(c.is_cached(v) for v in order[:100])
 
 

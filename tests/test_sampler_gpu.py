@@ -155,7 +155,7 @@ def test_bias_raises_cached_fraction_and_dedup():
     """test_sampler.cpp:205-239 and :258-288."""
     g = G.generate_power_law(1000, 2, 2.5, 4, 17)
     deg = np.diff(g.row_offsets)
-    order = sorted(range(1000), key=lambda v: (-deg[v], v))
+    order = sorted(range(1000), key=lambda v: (-int(deg[v]), v))
     c = cache_of(1000, order[:100])
 
     def stats(gamma):

@@ -123,9 +123,10 @@ void sampler_alloc(SamplerState& s, a3g_graph* g, a3g_cache* c, uint32_t max_see
   hb.nseg = dalloc<uint32_t>(hb.hub_cap);
   hb.seg_hub = dalloc<uint32_t>(hb.seg_cap);
   hb.rec_cnt = dalloc<uint32_t>(hb.seg_cap);
-  hb.tau = dalloc<double>(hb.seg_cap);
+  hb.tau = dalloc<uint64_t>(hb.seg_cap);
+  hb.tau_ok = dalloc<uint32_t>(hb.seg_cap);
   hb.rec_id = dalloc<uint32_t>(static_cast<size_t>(hb.seg_cap) * kRecCap);
-  hb.rec_key = dalloc<double>(static_cast<size_t>(hb.seg_cap) * kRecCap);
+  hb.rec_key = dalloc<uint64_t>(static_cast<size_t>(hb.seg_cap) * kRecCap);
   hb.slot_last = dalloc<uint32_t>(static_cast<size_t>(hb.seg_cap) * 32);
   s.d_ctr = dalloc<BatchCounters>(1);
   A3G_CUDA(cudaMallocHost(&s.h_ctr, sizeof(BatchCounters)));
@@ -156,6 +157,7 @@ void sampler_free(SamplerState& s) {
   dfree(s.hub.seg_hub);
   dfree(s.hub.rec_cnt);
   dfree(s.hub.tau);
+  dfree(s.hub.tau_ok);
   dfree(s.hub.rec_id);
   dfree(s.hub.rec_key);
   dfree(s.hub.slot_last);

@@ -9,53 +9,35 @@
 //
 // Per layer:
 //   k_sample_rows   warp per frontier row (dynamic chunks of rows). deg <= m:
-//                   copy; m < deg <= kSeg: in-warp exact replay (slot = lane,
-//                   ballot of keys > current min, 4-chunk prefetch); deg > kSeg
-//                   ("hubs", up to n-1 neighbours): registered for splitting.
+//                   copy; m < deg <= kSeg: in-warp exact replay
+//                   (reservoir.cuh); deg > kSeg ("hubs", up to n-1
+//                   neighbours): registered for splitting.
 //   k_hub_segments  warp per kSeg-long segment of a hub row: local replay from
 //                   an empty reservoir, emitting every local insertion
 //                   ("record") and the segment's exact m-th largest key tau_s.
 //                   Every global insertion is a local record of its segment.
-//   k_hub_merge     block per hub: records of segment s with key <= max_{s'<s}
-//                   tau_{s'} can never beat the global minimum and are dropped
-//                   in parallel; warp 0 replays the survivors in order, which
-//                   reproduces the sequential slot history exactly.
+//   k_hub_merge     block per hub: 8 filter warps drop the records of segment
+//                   s whose key cannot beat max_{s'<s} tau_{s'} (a lower bound
+//                   of the running minimum) while a replay warp applies the
+//                   survivors of the previous window in order -- the
+//                   sequential slot history, reproduced exactly.
 //   k_fin_count / k_fin_emit: first-seen dedup + relabel (tagged atomicMax of
 //                   the first position, tile partials, ballot scans).
 // Counts stay on the device: no host sync inside a batch.
 #include <cmath>
 
+#include "reservoir.cuh"
 #include "sampler.cuh"
 
 namespace a3g {
 namespace {
 
-constexpr unsigned kFull = 0xffffffffu;
+using rsv::kFull;
 constexpr int kRowChunk = 4;  // rows claimed per atomic by a warp
-constexpr int kPrefetch = 4;  // 32-key chunks loaded ahead per replay step
-
-__device__ __forceinline__ void warp_argmin(double& k, int& idx) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const double ok = __shfl_xor_sync(kFull, k, off);
-    const int oi = __shfl_xor_sync(kFull, idx, off);
-    if (ok < k || (ok == k && oi < idx)) {
-      k = ok;
-      idx = oi;
-    }
-  }
-}
 
 __device__ __forceinline__ void mark_first(uint64_t* first, uint32_t v, uint32_t tag, uint32_t pos) {
   atomicMax(reinterpret_cast<unsigned long long*>(first + v),
             (static_cast<unsigned long long>(tag) << 32) | static_cast<unsigned long long>(~pos));
-}
-
-// Lower bound in u-space below which a gamma-weighted key pow(u, 1/gamma)
-// cannot exceed thr (conservative by a 1e-6 relative margin).
-__device__ __forceinline__ double gamma_lo(double thr, double gamma) {
-  if (gamma > 1e8) return 0.0;
-  return pow(thr, gamma) * (1.0 - 1e-6);
 }
 
 struct SampleArgs {
@@ -74,155 +56,33 @@ struct SampleArgs {
   uint32_t* seg_count;
   uint64_t seed;
   double gamma, inv_gamma;
+  uint64_t tie;
   uint32_t f, layer, tag;
   int kind;   // A3G_SAMPLER_*
   int wmode;  // 0: all weights 1; 1: all gamma; 2: bitmap
 };
 
+// Key policy of a launch (template dispatch on wmode).
+template <int WM>
+struct PolOf;
+template <>
+struct PolOf<0> {
+  using P = rsv::PolUnit;
+  __device__ static P make(const SampleArgs&) { return P{}; }
+};
+template <>
+struct PolOf<1> {
+  using P = rsv::PolGammaAll;
+  __device__ static P make(const SampleArgs& a) { return P{a.inv_gamma, a.tie}; }
+};
+template <>
+struct PolOf<2> {
+  using P = rsv::PolMixed<rsv::BitmapW>;
+  __device__ static P make(const SampleArgs& a) { return P{rsv::BitmapW{a.bits, a.inv_gamma}, true, a.gamma, 0.0}; }
+};
+
 __device__ __forceinline__ bool is_gamma(const SampleArgs& a, uint32_t v) {
   return a.wmode == 1 || (a.wmode == 2 && ((__ldg(a.bits + (v >> 5)) >> (v & 31)) & 1u));
-}
-
-// Weight of neighbour j (node v): assign_weights (sampler.cpp:60-68).
-struct BitmapWeight {
-  const SampleArgs* a;
-  __device__ __forceinline__ bool unit(uint32_t v, uint64_t) const { return !is_gamma(*a, v); }
-  __device__ __forceinline__ double inv_w(uint32_t, uint64_t) const { return a->inv_gamma; }
-};
-struct ListWeight {  // explicit weights (test hook a3g_weighted_reservoir)
-  const double* w;
-  __device__ __forceinline__ bool unit(uint32_t, uint64_t j) const { return w[j] == 1.0; }
-  __device__ __forceinline__ double inv_w(uint32_t, uint64_t j) const { return 1.0 / w[j]; }
-};
-
-// Reservoir state of one warp: slot = lane (m <= 32), lanes >= m hold +inf.
-struct WState {
-  double my_key;
-  uint32_t my_id;
-  double thr;  // current minimum key (keys[min_pos])
-  int mp;      // min_pos: first slot holding the minimum (std::min_element)
-};
-
-struct NoEmit {
-  __device__ __forceinline__ void operator()(uint32_t, double, int) const {}
-};
-
-// Fill slots [0, nf) from positions j0 + lane (sampler.cpp:30-33); every fill
-// is an insertion. Draw number of position j is c0 + j + 1.
-template <typename WF, typename Emit>
-__device__ __forceinline__ void fill_slots(const uint32_t* nb, uint64_t j0, uint32_t nf, uint64_t key,
-                                           uint64_t c0, int lane, const WF& wf, WState& s, const Emit& emit) {
-  s.my_key = INFINITY;
-  s.my_id = 0;
-  if (lane < static_cast<int>(nf)) {
-    const uint64_t j = j0 + lane;
-    const uint32_t v = __ldg(nb + j);
-    const double u = unit_of(draw(key, c0 + j + 1));
-    s.my_key = wf.unit(v, j) ? u : pow(u, wf.inv_w(v, j));
-    s.my_id = v;
-    emit(v, s.my_key, lane);
-  }
-  s.thr = s.my_key;
-  s.mp = lane;
-  warp_argmin(s.thr, s.mp);
-}
-
-// Replay positions [jb, je) against a full reservoir (sampler.cpp:34-39):
-// a key replaces slot min_pos iff strictly greater than keys[min_pos]; then
-// min_pos = first minimum. Chunks of 32 keys, kPrefetch chunks in flight.
-// With a single non-unit weight (use_filter) a gamma-key is only evaluated
-// (pow) when u >= thr^gamma*(1-1e-6): below that, pow(u,1/gamma) < thr for any
-// <= 2-ulp pow, so no decision can change.
-template <typename WF, typename Emit>
-__device__ __forceinline__ void replay_range(const uint32_t* nb, uint64_t jb, uint64_t je, uint64_t key,
-                                             uint64_t c0, int lane, const WF& wf, bool use_filter,
-                                             double gamma, WState& s, const Emit& emit) {
-  double lo = use_filter ? gamma_lo(s.thr, gamma) : 0.0;
-  for (uint64_t b = jb; b < je; b += 32 * kPrefetch) {
-    uint32_t v[kPrefetch];
-    double kk[kPrefetch];
-#pragma unroll
-    for (int q = 0; q < kPrefetch; ++q) {
-      const uint64_t j = b + q * 32 + lane;
-      v[q] = j < je ? __ldg(nb + j) : 0u;
-    }
-#pragma unroll
-    for (int q = 0; q < kPrefetch; ++q) {
-      const uint64_t j = b + q * 32 + lane;
-      kk[q] = -1.0;
-      if (j < je) {
-        const double u = unit_of(draw(key, c0 + j + 1));
-        if (wf.unit(v[q], j)) {
-          kk[q] = u;
-        } else if (u >= lo) {
-          kk[q] = pow(u, wf.inv_w(v[q], j));
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < kPrefetch; ++q) {
-      unsigned mask = __ballot_sync(kFull, kk[q] > s.thr);
-      if (mask) {
-        while (mask) {
-          const int src = __ffs(mask) - 1;
-          const double kv = __shfl_sync(kFull, kk[q], src);
-          const uint32_t iv = __shfl_sync(kFull, v[q], src);
-          if (lane == s.mp) {
-            s.my_key = kv;
-            s.my_id = iv;
-          }
-          emit(iv, kv, src);
-          s.thr = s.my_key;
-          s.mp = lane;
-          warp_argmin(s.thr, s.mp);
-          mask &= __ballot_sync(kFull, kk[q] > s.thr) & ~((2u << src) - 1u);
-        }
-        if (use_filter) lo = gamma_lo(s.thr, gamma);
-      }
-    }
-  }
-}
-
-// Weighted reservoir of one whole row by one warp, m <= 32 < deg.
-template <typename WF>
-__device__ __forceinline__ uint32_t weighted_row_warp(const uint32_t* nb, uint64_t deg, uint32_t m,
-                                                      uint64_t key, int lane, const WF& wf,
-                                                      bool use_filter, double gamma, uint64_t c0 = 0) {
-  WState s;
-  fill_slots(nb, 0, m, key, c0, lane, wf, s, NoEmit{});
-  replay_range(nb, m, deg, key, c0, lane, wf, use_filter, gamma, s, NoEmit{});
-  return s.my_id;
-}
-
-// Algorithm R (sampler.cpp:44-58) by one warp over positions [jb, je), jb >=
-// m: slot r of position j is replaced iff r = next_below(j+1) < m (draw number
-// c0 + j - m + 1); candidates applied in position order.
-__device__ __forceinline__ void uniform_range(const uint32_t* nb, uint64_t jb, uint64_t je, uint32_t m,
-                                              uint64_t key, int lane, uint64_t c0, uint32_t& my_id) {
-  for (uint64_t b = jb; b < je; b += 32) {
-    const uint64_t j = b + lane;
-    const bool valid = j < je;
-    uint32_t r = kInv, v = 0;
-    if (valid) {
-      r = static_cast<uint32_t>(__umul64hi(draw(key, c0 + j - m + 1), j + 1));
-      if (r < m) v = __ldg(nb + j);
-    }
-    unsigned mask = __ballot_sync(kFull, valid && r < m);
-    while (mask) {
-      const int src = __ffs(mask) - 1;
-      const uint32_t slot = __shfl_sync(kFull, r, src);
-      const uint32_t iv = __shfl_sync(kFull, v, src);
-      if (lane == static_cast<int>(slot)) my_id = iv;
-      mask &= mask - 1;
-    }
-  }
-}
-
-__device__ __forceinline__ uint32_t uniform_row_warp(const uint32_t* nb, uint64_t deg, uint32_t m,
-                                                     uint64_t key, int lane, uint64_t c0 = 0) {
-  uint32_t my_id = lane < static_cast<int>(m) ? __ldg(nb + lane) : 0u;
-  uniform_range(nb, m, deg, m, key, lane, c0, my_id);
-  return my_id;
 }
 
 // Thread-serial exact reservoir for rows with f > 32 (rare; e.g. exhaustive
@@ -262,15 +122,16 @@ __device__ void serial_row(const SampleArgs& a, const uint32_t* nb, uint64_t deg
 }
 
 // Whole row by one warp (m <= 32 < deg); writes slots + first-position marks.
+template <int WM>
 __device__ __forceinline__ void row_by_warp(const SampleArgs& a, const uint32_t* nb, uint64_t deg, uint64_t key,
                                             uint32_t k, int lane) {
   const uint32_t m = a.f;
   uint32_t my_id;
   if (a.kind == A3G_SAMPLER_UNIFORM) {
-    my_id = uniform_row_warp(nb, deg, m, key, lane);
+    my_id = rsv::uniform_row_warp(nb, deg, m, key, lane);
   } else {
-    const BitmapWeight wf{&a};
-    my_id = weighted_row_warp(nb, deg, m, key, lane, wf, a.wmode != 0, a.gamma);
+    auto pol = PolOf<WM>::make(a);
+    my_id = rsv::weighted_row_warp(nb, deg, m, key, lane, pol);
   }
   const uint64_t row0 = static_cast<uint64_t>(k) * m;
   if (lane < static_cast<int>(m)) {
@@ -280,6 +141,7 @@ __device__ __forceinline__ void row_by_warp(const SampleArgs& a, const uint32_t*
   if (lane == 0) a.cnt[k] = m;
 }
 
+template <int WM>
 __global__ void __launch_bounds__(256) k_sample_rows(SampleArgs a) {
   const int lane = threadIdx.x & 31;
   const uint32_t nrows = *a.nrows;
@@ -334,41 +196,47 @@ __global__ void __launch_bounds__(256) k_sample_rows(SampleArgs a) {
           continue;
         }
       }
-      row_by_warp(a, nb, deg, key, k, lane);
+      row_by_warp<WM>(a, nb, deg, key, k, lane);
     }
   }
 }
 
-// Local replay of one hub segment [sb, se) from an empty reservoir; records =
-// every local insertion (id, key) in order; tau = segment's m-th largest key.
+// Records of a segment's local replay: every local insertion (id, key bits).
+template <typename K>
 struct SegEmit {
   uint32_t* rid;
-  double* rkey;
-  uint32_t* cnt;  // warp-uniform counter (register, by reference)
+  uint64_t* rkey;
+  uint32_t* cnt;  // warp-uniform counter
   uint32_t cap;
   int lane;
-  __device__ __forceinline__ void operator()(uint32_t id, double key, int src) const {
+  __device__ __forceinline__ void operator()(uint32_t id, K key, int src) const {
     const uint32_t c = *cnt;
     if (lane == src && c < cap) {
       rid[c] = id;
-      rkey[c] = key;
+      rkey[c] = *reinterpret_cast<const uint64_t*>(&key);
     }
     *cnt = c + 1;
   }
 };
-struct FillEmit {  // fills: lane i writes record i (records 0..nf-1)
+template <typename K>
+struct FillEmit {  // fills: lane i writes record i
   uint32_t* rid;
-  double* rkey;
-  uint32_t cap;
-  __device__ __forceinline__ void operator()(uint32_t id, double key, int lane) const {
-    if (static_cast<uint32_t>(lane) < cap) {
-      rid[lane] = id;
-      rkey[lane] = key;
-    }
+  uint64_t* rkey;
+  __device__ __forceinline__ void operator()(uint32_t id, K key, int lane) const {
+    rid[lane] = id;
+    rkey[lane] = *reinterpret_cast<const uint64_t*>(&key);
   }
 };
 
+template <typename K>
+__device__ __forceinline__ K key_from_bits(uint64_t b) {
+  return *reinterpret_cast<const K*>(&b);
+}
+
+template <int WM>
 __global__ void __launch_bounds__(256) k_hub_segments(SampleArgs a) {
+  using P = typename PolOf<WM>::P;
+  using K = typename P::K;
   const int lane = threadIdx.x & 31;
   const uint32_t nhub = min(*a.hub_count, a.hub.hub_cap);
   const uint32_t nseg_total = min(*a.seg_count, a.hub.seg_cap);
@@ -405,41 +273,61 @@ __global__ void __launch_bounds__(256) k_hub_segments(SampleArgs a) {
       a.hub.slot_last[static_cast<uint64_t>(s) * 32 + lane] = last;
       continue;
     }
-    const BitmapWeight wf{&a};
+    P pol = PolOf<WM>::make(a);
     uint32_t* rid = a.hub.rec_id + static_cast<uint64_t>(s) * kRecCap;
-    double* rkey = a.hub.rec_key + static_cast<uint64_t>(s) * kRecCap;
+    uint64_t* rkey = a.hub.rec_key + static_cast<uint64_t>(s) * kRecCap;
     const uint32_t nf = static_cast<uint32_t>(se - sb < m ? se - sb : m);
-    WState st;
-    fill_slots(nb, sb, nf, key, 0, lane, wf, st, FillEmit{rid, rkey, kRecCap});
+    rsv::WState<K> st;
+    rsv::fill_slots(nb, sb, nf, key, 0, lane, pol, st, FillEmit<K>{rid, rkey});
     uint32_t cnt = nf;
-    double tau = -1.0;
+    bool ok = false;
     if (se - sb >= m) {
-      SegEmit em{rid, rkey, &cnt, kRecCap, lane};
-      replay_range(nb, sb + m, se, key, 0, lane, wf, a.wmode != 0, a.gamma, st, em);
-      tau = st.thr;
+      SegEmit<K> em{rid, rkey, &cnt, kRecCap, lane};
+      rsv::replay_range(nb, sb + m, se, key, 0, lane, pol, st, em);
+      ok = true;
     }
     if (lane == 0) {
       a.hub.rec_cnt[s] = cnt;
-      a.hub.tau[s] = tau;
+      a.hub.tau[s] = *reinterpret_cast<const uint64_t*>(&st.thr);
+      a.hub.tau_ok[s] = ok ? 1u : 0u;
     }
   }
 }
 
-constexpr int kMergeWarps = 8;
+constexpr int kMergeFilterWarps = 8;
+constexpr int kMergeThreads = (kMergeFilterWarps + 1) * 32;
+constexpr size_t kMergeSmem = 2ull * kMergeFilterWarps * kRecCap * (8 + 4);
 
-__global__ void __launch_bounds__(kMergeWarps * 32) k_hub_merge(SampleArgs a) {
-  __shared__ uint32_t s_id[kMergeWarps][kRecCap];
-  __shared__ double s_key[kMergeWarps][kRecCap];
-  __shared__ uint32_t s_n[kMergeWarps];
-  __shared__ double s_lrun;
-  __shared__ int s_overflow;
+// Block per hub: warp 0 replays window w-1 while warps 1..8 filter window w.
+template <int WM>
+__global__ void __launch_bounds__(kMergeThreads) k_hub_merge(SampleArgs a) {
+  using P = typename PolOf<WM>::P;
+  using K = typename P::K;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  K* s_key = reinterpret_cast<K*>(smem_raw);  // [2][8][kRecCap]
+  uint32_t* s_id = reinterpret_cast<uint32_t*>(smem_raw + 2ull * kMergeFilterWarps * kRecCap * 8);
+  __shared__ uint32_t s_n[2][kMergeFilterWarps];
+  __shared__ K s_lrun[2];
+  __shared__ int s_lok[2];
+  __shared__ uint32_t s_hub[4];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t nhub = min(*a.hub_count, a.hub.hub_cap);
   const uint32_t m = a.f;
   for (uint32_t h = blockIdx.x; h < nhub; h += gridDim.x) {
-    const uint32_t ns = a.hub.nseg[h];
-    if (ns == 0) continue;  // processed by k_sample_rows
-    const uint32_t s0 = a.hub.seg0[h], k = a.hub.row[h];
+    if (threadIdx.x == 0) {
+      s_hub[0] = a.hub.nseg[h];
+      s_hub[1] = a.hub.seg0[h];
+      s_hub[2] = a.hub.row[h];
+      s_lok[0] = 0;
+      s_lok[1] = 0;
+    }
+    __syncthreads();
+    const uint32_t ns = s_hub[0];
+    if (ns == 0) {  // processed by k_sample_rows
+      __syncthreads();
+      continue;
+    }
+    const uint32_t s0 = s_hub[1], k = s_hub[2];
     const uint32_t dst = a.front[k];
     const uint64_t beg = a.ro[dst], deg = a.ro[dst + 1] - beg;
     const uint32_t* nb = a.col + beg;
@@ -464,84 +352,132 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_hub_merge(SampleArgs a) {
       __syncthreads();
       continue;
     }
-    if (threadIdx.x == 0) {
-      s_lrun = -1.0;
-      int of = 0;
-      for (uint32_t s = 0; s < ns; ++s) of |= a.hub.rec_cnt[s0 + s] > kRecCap;
-      s_overflow = of;
-    }
-    __syncthreads();
-    if (s_overflow) {  // a segment's records overflowed: exact whole-row replay
-      if (warp == 0) row_by_warp(a, nb, deg, key, k, lane);
+    int of = 0;
+    for (uint32_t s = threadIdx.x; s < ns; s += kMergeThreads) of |= a.hub.rec_cnt[s0 + s] > kRecCap;
+    if (__syncthreads_or(of)) {  // a segment overflowed its records: exact whole-row replay
+      if (warp == 0) row_by_warp<WM>(a, nb, deg, key, k, lane);
       __syncthreads();
       continue;
     }
-    // global fill = records 0..m-1 of segment 0 (positions 0..m-1)
-    WState st;
-    if (warp == 0) {
+    P pol = PolOf<WM>::make(a);
+    rsv::WState<K> st;
+    if (warp == 0) {  // global fill = records 0..m-1 of segment 0 (positions 0..m-1)
       const uint64_t rb = static_cast<uint64_t>(s0) * kRecCap;
-      st.my_key = lane < static_cast<int>(m) ? a.hub.rec_key[rb + lane] : INFINITY;
+      st.my_key = lane < static_cast<int>(m) ? key_from_bits<K>(a.hub.rec_key[rb + lane]) : pol.inf();
       st.my_id = lane < static_cast<int>(m) ? a.hub.rec_id[rb + lane] : 0u;
-      st.thr = st.my_key;
-      st.mp = lane;
-      warp_argmin(st.thr, st.mp);
+      pol.argmin(st.thr, st.mp, st.my_key, lane);
     }
-    for (uint32_t w0 = 0; w0 < ns; w0 += kMergeWarps) {
-      // filter: records of segment s with key <= L_s = max_{s'<s} tau_s' are dropped
-      const uint32_t s = w0 + warp;
-      uint32_t n_keep = 0;
-      if (s < ns) {
-        double L = s_lrun;
-        for (uint32_t t = w0; t < s; ++t) L = fmax(L, a.hub.tau[s0 + t]);
-        const uint64_t rb = static_cast<uint64_t>(s0 + s) * kRecCap;
-        const uint32_t rc = a.hub.rec_cnt[s0 + s];
-        for (uint32_t i0 = (s == 0 ? m : 0); i0 < rc; i0 += 32) {
-          const uint32_t i = i0 + lane;
-          double kv = -1.0;
-          uint32_t iv = 0;
-          if (i < rc) {
-            kv = a.hub.rec_key[rb + i];
-            iv = a.hub.rec_id[rb + i];
+    const uint32_t nwin = (ns + kMergeFilterWarps - 1) / kMergeFilterWarps;
+    for (uint32_t it = 0; it <= nwin; ++it) {
+      if (warp > 0 && it < nwin) {
+        // ---- filter window `it` into buffer it%2
+        const uint32_t fw = warp - 1, buf = it & 1, w0 = it * kMergeFilterWarps;
+        const uint32_t s = w0 + fw;
+        // L = max tau over segments < s (prefix from earlier windows + this window)
+        K L = s_lrun[buf];
+        int lok = s_lok[buf];
+        {
+          const uint32_t t = w0 + lane;
+          K tv{};
+          int tok = 0;
+          if (lane < static_cast<int>(fw) && t < ns) {
+            tok = a.hub.tau_ok[s0 + t];
+            tv = key_from_bits<K>(a.hub.tau[s0 + t]);
           }
-          const bool keep = i < rc && kv > L;
-          const unsigned bm = __ballot_sync(kFull, keep);
-          if (keep) {
-            const uint32_t o = n_keep + __popc(bm & ((1u << lane) - 1u));
-            s_id[warp][o] = iv;
-            s_key[warp][o] = kv;
-          }
-          n_keep += __popc(bm);
-        }
-      }
-      if (lane == 0) s_n[warp] = n_keep;
-      __syncthreads();
-      if (warp == 0) {
-        for (int wr = 0; wr < kMergeWarps && w0 + wr < ns; ++wr) {
-          const uint32_t n = s_n[wr];
-          for (uint32_t i0 = 0; i0 < n; i0 += 32) {
-            const uint32_t i = i0 + lane;
-            const double kk = i < n ? s_key[wr][i] : -1.0;
-            const uint32_t v = i < n ? s_id[wr][i] : 0u;
-            unsigned mask = __ballot_sync(kFull, kk > st.thr);
-            while (mask) {
-              const int src = __ffs(mask) - 1;
-              const double kv = __shfl_sync(kFull, kk, src);
-              const uint32_t iv = __shfl_sync(kFull, v, src);
-              if (lane == st.mp) {
-                st.my_key = kv;
-                st.my_id = iv;
-              }
-              st.thr = st.my_key;
-              st.mp = lane;
-              warp_argmin(st.thr, st.mp);
-              mask &= __ballot_sync(kFull, kk > st.thr) & ~((2u << src) - 1u);
+          for (int off = 16; off > 0; off >>= 1) {
+            const K ov = __shfl_xor_sync(kFull, tv, off);
+            const int oo = __shfl_xor_sync(kFull, tok, off);
+            if (oo && (!tok || ov > tv)) {
+              tv = ov;
+              tok = 1;
             }
           }
+          if (tok && (!lok || tv > L)) {
+            L = tv;
+            lok = 1;
+          }
         }
-        if (lane == 0) {
-          double L = s_lrun;
-          for (uint32_t t = w0; t < min(ns, w0 + kMergeWarps); ++t) L = fmax(L, a.hub.tau[s0 + t]);
-          s_lrun = L;
+        uint32_t n_keep = 0;
+        if (s < ns) {
+          const uint64_t rb = static_cast<uint64_t>(s0 + s) * kRecCap;
+          const uint32_t rc = a.hub.rec_cnt[s0 + s];
+          K* kb = s_key + (buf * kMergeFilterWarps + fw) * kRecCap;
+          uint32_t* ib = s_id + (buf * kMergeFilterWarps + fw) * kRecCap;
+          for (uint32_t i0 = (s == 0 ? m : 0); i0 < rc; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            K kv{};
+            uint32_t iv = 0;
+            if (i < rc) {
+              kv = key_from_bits<K>(a.hub.rec_key[rb + i]);
+              iv = a.hub.rec_id[rb + i];
+            }
+            const bool keep = i < rc && (!lok || pol.keep(kv, L));
+            const unsigned bm = __ballot_sync(kFull, keep);
+            if (keep) {
+              const uint32_t o = n_keep + __popc(bm & ((1u << lane) - 1u));
+              kb[o] = kv;
+              ib[o] = iv;
+            }
+            n_keep += __popc(bm);
+          }
+        }
+        if (lane == 0) s_n[buf][fw] = n_keep;
+        if (fw == 0) {  // running bound for the next window
+          const uint32_t t = w0 + lane;
+          K tv{};
+          int tok = 0;
+          if (lane < kMergeFilterWarps && t < ns) {
+            tok = a.hub.tau_ok[s0 + t];
+            tv = key_from_bits<K>(a.hub.tau[s0 + t]);
+          }
+          for (int off = 16; off > 0; off >>= 1) {
+            const K ov = __shfl_xor_sync(kFull, tv, off);
+            const int oo = __shfl_xor_sync(kFull, tok, off);
+            if (oo && (!tok || ov > tv)) {
+              tv = ov;
+              tok = 1;
+            }
+          }
+          K nl = s_lrun[buf];
+          int nok = s_lok[buf];
+          if (tok && (!nok || tv > nl)) {
+            nl = tv;
+            nok = 1;
+          }
+          if (lane == 0) {
+            s_lrun[buf ^ 1] = nl;
+            s_lok[buf ^ 1] = nok;
+          }
+        }
+      }
+      if (warp == 0 && it > 0) {
+        // ---- replay window it-1 from buffer (it-1)%2, in segment order
+        const uint32_t buf = (it - 1) & 1, w0 = (it - 1) * kMergeFilterWarps;
+        for (uint32_t fw = 0; fw < kMergeFilterWarps && w0 + fw < ns; ++fw) {
+          const uint32_t n = s_n[buf][fw];
+          const K* kb = s_key + (buf * kMergeFilterWarps + fw) * kRecCap;
+          const uint32_t* ib = s_id + (buf * kMergeFilterWarps + fw) * kRecCap;
+          for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            const bool valid = i < n;
+            const K kk = valid ? kb[i] : K{};
+            const uint32_t v = valid ? ib[i] : 0u;
+            unsigned mask = __ballot_sync(kFull, valid && pol.cheap_gt(kk, st.thr));
+            while (mask) {
+              const int src = __ffs(mask) - 1;
+              const K kv = __shfl_sync(kFull, kk, src);
+              const uint32_t iv = __shfl_sync(kFull, v, src);
+              if (pol.gt(kv, st.thr)) {
+                if (lane == st.mp) {
+                  st.my_key = kv;
+                  st.my_id = iv;
+                }
+                pol.argmin(st.thr, st.mp, st.my_key, lane);
+                mask &= __ballot_sync(kFull, valid && pol.cheap_gt(kk, st.thr));
+              }
+              mask &= ~((2u << src) - 1u);
+            }
+          }
         }
       }
       __syncthreads();
@@ -569,10 +505,10 @@ __global__ void k_reservoir_list(const uint32_t* nb, const double* w, uint64_t d
   if (m <= 32) {
     uint32_t id;
     if (kind == A3G_SAMPLER_UNIFORM) {
-      id = uniform_row_warp(nb, deg, m, key, lane, c0);
+      id = rsv::uniform_row_warp(nb, deg, m, key, lane, c0);
     } else {
-      const ListWeight wf{w};
-      id = weighted_row_warp(nb, deg, m, key, lane, wf, false, 1.0, c0);
+      rsv::PolMixed<rsv::ListW> pol{rsv::ListW{w}, false, 1.0, 0.0};
+      id = rsv::weighted_row_warp(nb, deg, m, key, lane, pol, c0);
     }
     if (lane < static_cast<int>(m)) out[lane] = id;
     return;
@@ -836,6 +772,24 @@ __global__ void k_gather_unique(const T* feat, uint32_t pitch, uint32_t F, const
   }
 }
 
+template <int WM>
+void launch_layer_kernels(const SampleArgs& sa, int sm_count, cudaStream_t st) {
+  k_sample_rows<WM><<<sm_count * 4, 256, 0, st>>>(sa);
+  A3G_LAUNCH_CHECK("k_sample_rows");
+  if (sa.f <= 32) {
+    k_hub_segments<WM><<<sm_count * 8, 256, 0, st>>>(sa);
+    A3G_LAUNCH_CHECK("k_hub_segments");
+    static bool attr_set = false;
+    if (!attr_set) {
+      A3G_CUDA(cudaFuncSetAttribute(k_hub_merge<WM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kMergeSmem)));
+      attr_set = true;
+    }
+    k_hub_merge<WM><<<sm_count * 2, kMergeThreads, kMergeSmem, st>>>(sa);
+    A3G_LAUNCH_CHECK("k_hub_merge");
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------ host side ----
@@ -884,7 +838,6 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
     else if (!c->none_cached)
       wmode = 2;
   }
-  const int sample_blocks = s.sm_count * 4;
   for (uint32_t l = 0; l < s.L; ++l) {
     LayerArena& la = s.layer[l];
     const uint32_t tag = ++s.tag;
@@ -905,19 +858,18 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
     sa.seed = rng_seed;
     sa.gamma = gamma;
     sa.inv_gamma = 1.0 / gamma;
+    sa.tie = 64ull * (static_cast<uint64_t>(std::ceil(std::min(gamma, 1e12))) + 1);
     sa.f = la.f;
     sa.layer = l;
     sa.tag = tag;
     sa.kind = kind;
     sa.wmode = wmode;
-    k_sample_rows<<<sample_blocks, 256, 0, st>>>(sa);
-    A3G_LAUNCH_CHECK("k_sample_rows");
-    if (la.f <= 32) {
-      k_hub_segments<<<s.sm_count * 8, 256, 0, st>>>(sa);
-      A3G_LAUNCH_CHECK("k_hub_segments");
-      k_hub_merge<<<s.sm_count * 2, kMergeWarps * 32, 0, st>>>(sa);
-      A3G_LAUNCH_CHECK("k_hub_merge");
-    }
+    if (wmode == 1)
+      launch_layer_kernels<1>(sa, s.sm_count, st);
+    else if (wmode == 2)
+      launch_layer_kernels<2>(sa, s.sm_count, st);
+    else
+      launch_layer_kernels<0>(sa, s.sm_count, st);
     FinArgs fa{};
     fa.S = la.S;
     fa.cnt = la.cnt;

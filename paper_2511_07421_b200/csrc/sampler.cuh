@@ -31,9 +31,10 @@ struct HubArena {
   uint32_t* nseg = nullptr;      // [hub_cap] #segments (0: handled in-row)
   uint32_t* seg_hub = nullptr;   // [seg_cap] owning hub
   uint32_t* rec_cnt = nullptr;   // [seg_cap]
-  double* tau = nullptr;         // [seg_cap] m-th largest key of the segment (-1: short)
+  uint64_t* tau = nullptr;       // [seg_cap] m-th largest key of the segment (policy key bits)
+  uint32_t* tau_ok = nullptr;    // [seg_cap] 0: segment shorter than m (no bound)
   uint32_t* rec_id = nullptr;    // [seg_cap * kRecCap]
-  double* rec_key = nullptr;     // [seg_cap * kRecCap]
+  uint64_t* rec_key = nullptr;   // [seg_cap * kRecCap] policy key bits
   uint32_t* slot_last = nullptr; // [seg_cap * 32] uniform kind: last position per slot
 };
 

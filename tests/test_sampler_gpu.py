@@ -68,6 +68,19 @@ def test_c1_three_hops_and_wide_fanout(c1, orc):
         assert_same_batch(a, b, f"uniform fan {fan}")
 
 
+@pytest.mark.parametrize("gamma", [2.0, 8.0, 1000.0])
+def test_c1_full_cache_integer_keys(c1, orc, gamma):
+    """Every neighbour cached: the sampler compares u-space integer keys
+    (PolGammaAll) with exact pow only on near-ties; must equal the oracle."""
+    g = c1
+    cache = CA.build_static_cache(g, CA.CacheConfig(g.num_nodes * g.feat_dim * 4, 1))
+    seeds = np.arange(3, 100_000, 53, dtype=np.uint32)
+    for fan in ([15, 10, 5], [25, 3]):
+        a = run(g, seeds, fan, gamma, 0, 4242, cache)
+        b = orc.sample_khop(g, seeds, fan, gamma, 0, 4242, cache.device_map)
+        assert_same_batch(a, b, f"full cache gamma {gamma} fan {fan}")
+
+
 @pytest.mark.slow
 def test_c2_reddit_shaped_slice(orc):
     """Config 2 shape: 233K nodes, m=165 (mean deg ~484, hubs up to n-1),

@@ -66,6 +66,8 @@ struct BatchCounters {
   uint32_t work[kMaxLayers];        // dynamic row counters of the sampling kernels
   uint32_t hubs[kMaxLayers];        // hub rows registered per layer
   uint32_t segs[kMaxLayers];        // hub segments reserved per layer
+  uint32_t items[kMaxLayers];       // stream items appended per layer
+  uint32_t iwork[kMaxLayers];       // stream items claimed per layer
   uint32_t n_seeds;                 // seeds given (incl. duplicates)
   uint32_t hits, misses;            // retrieve_features accounting
   uint32_t pad;

@@ -128,6 +128,8 @@ void sampler_alloc(SamplerState& s, a3g_graph* g, a3g_cache* c, uint32_t max_see
   hb.rec_id = dalloc<uint32_t>(static_cast<size_t>(hb.seg_cap) * kRecCap);
   hb.rec_key = dalloc<uint64_t>(static_cast<size_t>(hb.seg_cap) * kRecCap);
   hb.slot_last = dalloc<uint32_t>(static_cast<size_t>(hb.seg_cap) * 32);
+  hb.item_cap = hb.hub_cap + hb.seg_cap;
+  hb.items = dalloc<uint4>(hb.item_cap);
   s.d_ctr = dalloc<BatchCounters>(1);
   A3G_CUDA(cudaMallocHost(&s.h_ctr, sizeof(BatchCounters)));
   A3G_CUDA(cudaMallocHost(&s.h_seeds, max_seeds * sizeof(uint32_t)));
@@ -161,6 +163,7 @@ void sampler_free(SamplerState& s) {
   dfree(s.hub.rec_id);
   dfree(s.hub.rec_key);
   dfree(s.hub.slot_last);
+  dfree(s.hub.items);
   dfree(s.d_ctr);
   if (s.h_ctr) cudaFreeHost(s.h_ctr);
   if (s.h_seeds) cudaFreeHost(s.h_seeds);
@@ -281,7 +284,8 @@ a3g_status a3g_graph_create(int device, uint64_t n, uint64_t m, uint32_t F, cons
     g->feat_dtype = feat_dtype;
     g->h_ro.assign(ro, ro + n + 1);
     g->d_ro = dalloc<uint64_t>(n + 1);
-    g->d_col = dalloc<uint32_t>(m);
+    g->d_col = dalloc<uint32_t>(m + 8);  // +8: 16-byte rounded TMA pieces may read past the end
+    A3G_CUDA(cudaMemset(g->d_col + m, 0, 8 * 4));
     A3G_CUDA(cudaMemcpy(g->d_ro, ro, (n + 1) * 8, cudaMemcpyHostToDevice));
     if (m) A3G_CUDA(cudaMemcpy(g->d_col, col, m * 4, cudaMemcpyHostToDevice));
     g->d_labels = dalloc<uint32_t>(n);

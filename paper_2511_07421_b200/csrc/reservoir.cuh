@@ -43,16 +43,15 @@ __device__ __forceinline__ void argmin_f64(double& k, int& idx) {
     }
   }
 }
-__device__ __forceinline__ void argmin_u64(uint64_t& k, int& idx) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const uint64_t ok = __shfl_xor_sync(kFull, k, off);
-    const int oi = __shfl_xor_sync(kFull, idx, off);
-    if (ok < k || (ok == k && oi < idx)) {
-      k = ok;
-      idx = oi;
-    }
-  }
+// Warp argmin of 64-bit order keys, ties -> lowest lane (std::min_element):
+// two redux.sync.min.u32 (high then low word) + one ballot -- a short
+// dependency chain instead of five rounds of 64-bit shuffles.
+__device__ __forceinline__ void argmin_bits(uint64_t b, uint64_t& mn, int& mp) {
+  const uint32_t hi = static_cast<uint32_t>(b >> 32), lo = static_cast<uint32_t>(b);
+  const uint32_t mh = __reduce_min_sync(kFull, hi);
+  const uint32_t ml = __reduce_min_sync(kFull, hi == mh ? lo : 0xffffffffu);
+  mn = (static_cast<uint64_t>(mh) << 32) | ml;
+  mp = __ffs(__ballot_sync(kFull, b == mn)) - 1;
 }
 
 __device__ __forceinline__ double gamma_lo(double thr, double gamma) {
@@ -71,11 +70,7 @@ struct PolUnit {
   __device__ __forceinline__ bool gt(K a, K b) const { return a > b; }
   __device__ __forceinline__ bool cheap_gt(K a, K b) const { return a > b; }
   __device__ __forceinline__ void on_thr(K) {}
-  __device__ __forceinline__ void argmin(K& thr, int& mp, K my, int lane) const {
-    thr = my;
-    mp = lane;
-    argmin_u64(thr, mp);
-  }
+  __device__ __forceinline__ void argmin(K& thr, int& mp, K my, int) const { argmin_bits(my, thr, mp); }
   // record filter of the hub merge: may a record with key k beat a minimum >= L?
   __device__ __forceinline__ bool keep(K k, K L) const { return k > L; }
 };
@@ -96,9 +91,7 @@ struct PolGammaAll {
   __device__ __forceinline__ bool cheap_gt(K a, K b) const { return a > b; }
   __device__ __forceinline__ void on_thr(K) {}
   __device__ __forceinline__ void argmin(K& thr, int& mp, K my, int lane) const {
-    thr = my;
-    mp = lane;
-    argmin_u64(thr, mp);
+    argmin_bits(my, thr, mp);
     // another slot within `tie` of the minimum may hold an equal k: decide
     // with the exact keys (std::min_element semantics)
     if (__ballot_sync(kFull, my != ~0ull && my != thr && my - thr <= tie)) {
@@ -155,10 +148,11 @@ struct PolMixed {
   __device__ __forceinline__ void on_thr(K thr) {
     if (use_filter) lo = gamma_lo(thr, gamma);
   }
-  __device__ __forceinline__ void argmin(K& thr, int& mp, K my, int lane) const {
-    thr = my;
-    mp = lane;
-    argmin_f64(thr, mp);
+  __device__ __forceinline__ void argmin(K& thr, int& mp, K my, int) const {
+    // keys are >= 0 (or +inf): their IEEE bit patterns order like the values
+    uint64_t mn;
+    argmin_bits(static_cast<uint64_t>(__double_as_longlong(my)), mn, mp);
+    thr = __longlong_as_double(static_cast<long long>(mn));
   }
   __device__ __forceinline__ bool keep(K k, K L) const { return k > L; }
 };
@@ -186,7 +180,7 @@ __device__ __forceinline__ void fill_slots(const uint32_t* nb, uint64_t j0, uint
   s.my_id = 0;
   if (lane < static_cast<int>(nf)) {
     const uint64_t j = j0 + lane;
-    const uint32_t v = __ldg(nb + j);
+    const uint32_t v = nb[j];
     s.my_key = pol.fill_key(mix64(key + (c0 + j + 1) * kPhi), v, j);
     s.my_id = v;
     emit(v, s.my_key, lane);
@@ -210,7 +204,7 @@ __device__ __forceinline__ void replay_range(const uint32_t* nb, uint64_t jb, ui
 #pragma unroll
     for (int q = 0; q < kPrefetch; ++q) {
       const uint64_t j = b + q * 32 + lane;
-      v[q] = j < je ? __ldg(nb + j) : 0u;
+      v[q] = j < je ? nb[j] : 0u;  // nb: global or a TMA-staged shared-memory piece
     }
 #pragma unroll
     for (int q = 0; q < kPrefetch; ++q) {
@@ -265,7 +259,7 @@ __device__ __forceinline__ void uniform_range(const uint32_t* nb, uint64_t jb, u
     uint32_t r = kInv, v = 0;
     if (valid) {
       r = static_cast<uint32_t>(__umul64hi(draw(key, c0 + j - m + 1), j + 1));
-      if (r < m) v = __ldg(nb + j);
+      if (r < m) v = nb[j];
     }
     unsigned mask = __ballot_sync(kFull, valid && r < m);
     while (mask) {
@@ -280,7 +274,7 @@ __device__ __forceinline__ void uniform_range(const uint32_t* nb, uint64_t jb, u
 
 __device__ __forceinline__ uint32_t uniform_row_warp(const uint32_t* nb, uint64_t deg, uint32_t m, uint64_t key,
                                                      int lane, uint64_t c0 = 0) {
-  uint32_t my_id = lane < static_cast<int>(m) ? __ldg(nb + lane) : 0u;
+  uint32_t my_id = lane < static_cast<int>(m) ? nb[lane] : 0u;
   uniform_range(nb, m, deg, m, key, lane, c0, my_id);
   return my_id;
 }

@@ -26,6 +26,7 @@
 // Counts stay on the device: no host sync inside a batch.
 #include <cmath>
 
+#include "ptx.cuh"
 #include "reservoir.cuh"
 #include "sampler.cuh"
 
@@ -54,6 +55,8 @@ struct SampleArgs {
   HubArena hub;
   uint32_t* hub_count;
   uint32_t* seg_count;
+  uint32_t* item_count;
+  uint32_t* item_work;
   uint64_t seed;
   double gamma, inv_gamma;
   uint64_t tie;
@@ -141,66 +144,6 @@ __device__ __forceinline__ void row_by_warp(const SampleArgs& a, const uint32_t*
   if (lane == 0) a.cnt[k] = m;
 }
 
-template <int WM>
-__global__ void __launch_bounds__(256) k_sample_rows(SampleArgs a) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t nrows = *a.nrows;
-  const uint32_t m = a.f;
-  for (;;) {
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(a.work, kRowChunk);
-    base = __shfl_sync(kFull, base, 0);
-    if (base >= nrows) break;
-    const uint32_t rend = min(base + kRowChunk, nrows);
-    for (uint32_t k = base; k < rend; ++k) {
-      const uint32_t dst = __ldg(a.front + k);
-      const uint64_t beg = __ldg(a.ro + dst), deg = __ldg(a.ro + dst + 1) - beg;
-      const uint32_t* nb = a.col + beg;
-      const uint64_t row0 = static_cast<uint64_t>(k) * m;
-      if (deg <= m) {  // fill phase only: output = neighbour list (sampler.cpp:30-33)
-        for (uint32_t t = lane; t < deg; t += 32) {
-          const uint32_t v = __ldg(nb + t);
-          a.S[row0 + t] = v;
-          mark_first(a.first, v, a.tag, static_cast<uint32_t>(row0 + t));
-        }
-        if (lane == 0) a.cnt[k] = static_cast<uint32_t>(deg);
-        continue;
-      }
-      const uint64_t key = hash2(a.seed, hash2(a.layer, dst));  // sampler.cpp:117
-      if (m > 32) {
-        if (lane == 0) serial_row(a, nb, deg, key, a.S + row0, a.scratch + row0);
-        __syncwarp();
-        for (uint32_t t = lane; t < m; t += 32)
-          mark_first(a.first, a.S[row0 + t], a.tag, static_cast<uint32_t>(row0 + t));
-        if (lane == 0) a.cnt[k] = m;
-        continue;
-      }
-      if (deg > kSeg) {  // hub: register for the segmented path
-        const uint32_t nseg = static_cast<uint32_t>((deg + kSeg - 1) / kSeg);
-        uint32_t h = 0, s0 = 0;
-        if (lane == 0) {
-          h = atomicAdd(a.hub_count, 1u);
-          s0 = atomicAdd(a.seg_count, nseg);
-          const bool ok = h < a.hub.hub_cap && s0 + static_cast<uint64_t>(nseg) <= a.hub.seg_cap;
-          if (h < a.hub.hub_cap) {
-            a.hub.row[h] = k;
-            a.hub.seg0[h] = s0;
-            a.hub.nseg[h] = ok ? nseg : 0u;  // 0 = handled here (capacity exceeded)
-          }
-          if (!ok) h = kInv;
-        }
-        h = __shfl_sync(kFull, h, 0);
-        s0 = __shfl_sync(kFull, s0, 0);
-        if (h != kInv) {
-          for (uint32_t i = lane; i < nseg; i += 32) a.hub.seg_hub[s0 + i] = h;
-          continue;
-        }
-      }
-      row_by_warp<WM>(a, nb, deg, key, k, lane);
-    }
-  }
-}
-
 // Records of a segment's local replay: every local insertion (id, key bits).
 template <typename K>
 struct SegEmit {
@@ -233,66 +176,284 @@ __device__ __forceinline__ K key_from_bits(uint64_t b) {
   return *reinterpret_cast<const K*>(&b);
 }
 
+// Classification of a layer's frontier rows, warp per 32 rows (lane = row):
+//   deg == 0           no edges, no draws (sampler.cpp:116)
+//   deg <= m           fill only: output = neighbour list (sampler.cpp:30-33)
+//   m > 32 < deg       thread-serial exact replay (rare wide fanouts)
+//   m < deg <= kSeg    one stream item (whole row)
+//   deg > kSeg         hub: ceil(deg/kSeg) segment items + a merge entry
+// Items are appended with one warp-aggregated atomic.
 template <int WM>
-__global__ void __launch_bounds__(256) k_hub_segments(SampleArgs a) {
-  using P = typename PolOf<WM>::P;
-  using K = typename P::K;
+__global__ void __launch_bounds__(256) k_classify(SampleArgs a) {
   const int lane = threadIdx.x & 31;
-  const uint32_t nhub = min(*a.hub_count, a.hub.hub_cap);
-  const uint32_t nseg_total = min(*a.seg_count, a.hub.seg_cap);
+  const uint32_t nrows = *a.nrows;
+  const uint32_t m = a.f;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t m = a.f;
-  for (uint32_t s = gw; s < nseg_total; s += nw) {
-    const uint32_t h = a.hub.seg_hub[s];
-    if (h >= nhub) continue;  // stale entry
-    const uint32_t s0 = a.hub.seg0[h], ns = a.hub.nseg[h];
-    if (s < s0 || s >= s0 + ns) continue;
-    const uint32_t k = a.hub.row[h];
-    const uint32_t dst = a.front[k];
-    const uint64_t beg = a.ro[dst], deg = a.ro[dst + 1] - beg;
-    const uint32_t* nb = a.col + beg;
-    const uint64_t key = hash2(a.seed, hash2(a.layer, dst));
-    const uint64_t sb = static_cast<uint64_t>(s - s0) * kSeg, se = min(deg, sb + kSeg);
-    if (a.kind == A3G_SAMPLER_UNIFORM) {
-      // last position per slot within the segment (positions >= m)
-      uint32_t last = kInv;  // lane = slot
-      const uint64_t jb = sb > m ? sb : static_cast<uint64_t>(m);
-      for (uint64_t b = jb; b < se; b += 32) {
-        const uint64_t j = b + lane;
-        uint32_t r = kInv;
-        if (j < se) r = static_cast<uint32_t>(__umul64hi(draw(key, j - m + 1), j + 1));
-        unsigned mask = __ballot_sync(kFull, j < se && r < m);
-        while (mask) {
-          const int src = __ffs(mask) - 1;
-          const uint32_t slot = __shfl_sync(kFull, r, src);
-          if (lane == static_cast<int>(slot)) last = static_cast<uint32_t>(b + src);
-          mask &= mask - 1;
-        }
+  for (uint32_t r0 = gw * 32; r0 < nrows; r0 += nw * 32) {
+    const uint32_t k = r0 + lane;
+    const bool valid = k < nrows;
+    uint32_t dst = 0;
+    uint64_t beg = 0, deg = 0;
+    if (valid) {
+      dst = __ldg(a.front + k);
+      beg = __ldg(a.ro + dst);
+      deg = __ldg(a.ro + dst + 1) - beg;
+    }
+    const uint64_t row0 = static_cast<uint64_t>(k) * m;
+    // ---- fill-only rows, copied cooperatively
+    unsigned cm = __ballot_sync(kFull, valid && deg <= m);
+    while (cm) {
+      const int src = __ffs(cm) - 1;
+      cm &= cm - 1;
+      const uint64_t sb = __shfl_sync(kFull, beg, src);
+      const uint32_t sd = static_cast<uint32_t>(__shfl_sync(kFull, deg, src));
+      const uint64_t sr0 = static_cast<uint64_t>(r0 + src) * m;
+      for (uint32_t t = lane; t < sd; t += 32) {
+        const uint32_t v = __ldg(a.col + sb + t);
+        a.S[sr0 + t] = v;
+        mark_first(a.first, v, a.tag, static_cast<uint32_t>(sr0 + t));
       }
-      a.hub.slot_last[static_cast<uint64_t>(s) * 32 + lane] = last;
-      continue;
     }
-    P pol = PolOf<WM>::make(a);
-    uint32_t* rid = a.hub.rec_id + static_cast<uint64_t>(s) * kRecCap;
-    uint64_t* rkey = a.hub.rec_key + static_cast<uint64_t>(s) * kRecCap;
-    const uint32_t nf = static_cast<uint32_t>(se - sb < m ? se - sb : m);
-    rsv::WState<K> st;
-    rsv::fill_slots(nb, sb, nf, key, 0, lane, pol, st, FillEmit<K>{rid, rkey});
-    uint32_t cnt = nf;
-    bool ok = false;
-    if (se - sb >= m) {
-      SegEmit<K> em{rid, rkey, &cnt, kRecCap, lane};
-      rsv::replay_range(nb, sb + m, se, key, 0, lane, pol, st, em);
-      ok = true;
+    if (valid && deg <= m) a.cnt[k] = static_cast<uint32_t>(deg);
+    uint32_t n_items = 0, h = kInv, s0 = 0, nseg = 0;
+    if (valid && deg > m) {
+      if (m > 32) {  // wide fanout: exact serial replay by this thread
+        serial_row(a, a.col + beg, deg, hash2(a.seed, hash2(a.layer, dst)), a.S + row0, a.scratch + row0);
+        for (uint32_t t = 0; t < m; ++t) mark_first(a.first, a.S[row0 + t], a.tag, static_cast<uint32_t>(row0 + t));
+        a.cnt[k] = m;
+      } else if (deg > kSeg) {
+        nseg = static_cast<uint32_t>((deg + kSeg - 1) / kSeg);
+        h = atomicAdd(a.hub_count, 1u);
+        s0 = atomicAdd(a.seg_count, nseg);
+        const bool ok = h < a.hub.hub_cap && s0 + static_cast<uint64_t>(nseg) <= a.hub.seg_cap;
+        if (h < a.hub.hub_cap) {
+          a.hub.row[h] = k;
+          a.hub.seg0[h] = s0;
+          a.hub.nseg[h] = ok ? nseg : 0u;  // 0: streamed as one whole-row item instead
+        }
+        if (ok) {
+          for (uint32_t i = 0; i < nseg; ++i) a.hub.seg_hub[s0 + i] = h;
+          n_items = nseg;
+        } else {
+          h = kInv;
+          n_items = 1;
+        }
+      } else {
+        n_items = 1;
+      }
     }
-    if (lane == 0) {
-      a.hub.rec_cnt[s] = cnt;
-      a.hub.tau[s] = *reinterpret_cast<const uint64_t*>(&st.thr);
-      a.hub.tau_ok[s] = ok ? 1u : 0u;
+    // ---- warp-aggregated append of the items
+    uint32_t incl = n_items;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, off);
+      if (lane >= off) incl += y;
+    }
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    uint32_t base = 0;
+    if (lane == 0 && total) base = atomicAdd(a.item_count, total);
+    base = __shfl_sync(kFull, base, 0);
+    uint32_t o = base + incl - n_items;
+    if (h != kInv) {
+      for (uint32_t i = 0; i < nseg; ++i, ++o) {
+        const uint32_t sb = i * kSeg;
+        const uint32_t se = static_cast<uint32_t>(deg < sb + static_cast<uint64_t>(kSeg) ? deg : sb + kSeg);
+        if (o < a.hub.item_cap) a.hub.items[o] = make_uint4(k, sb, se, s0 + i);
+      }
+    } else if (n_items == 1) {
+      if (o < a.hub.item_cap) a.hub.items[o] = make_uint4(k, 0, static_cast<uint32_t>(deg), kInv);
     }
   }
 }
+
+// ---------------------------------------------------------------- stream ---
+// Warp-level streaming of items through a shared-memory ring fed by TMA 1-D
+// bulk copies (cp.async.bulk + mbarrier): piece q+kStages is in flight while
+// piece q is replayed, so every warp keeps kStages-1 pieces of neighbour ids
+// in flight instead of stalling on each 32-key chunk.
+constexpr uint32_t kPiece = 512;                 // neighbour ids per piece
+constexpr uint32_t kStages = 4;                  // ring depth per warp
+constexpr uint32_t kPieceBuf = kPiece + 8;       // + 16-byte alignment slack
+constexpr uint32_t kItemsPerClaim = 8;
+constexpr int kStreamWarps = 8;
+constexpr size_t kStreamSmem = static_cast<size_t>(kStreamWarps) * kStages * (kPieceBuf * 4 + 8);
+
+struct PieceMeta {
+  uint32_t it;     // item slot within the claim (lane holding its meta)
+  uint32_t p0, p1; // row positions of the piece
+};
+
+// Piece q of a claim: the item holding it (lanes hold per-item np / exclusive
+// piece prefix / [ia, ib)) and its row positions. Warp-uniform.
+__device__ __forceinline__ PieceMeta piece_meta(uint32_t q, uint32_t np, uint32_t pref_ex, uint32_t ia,
+                                                uint32_t ib) {
+  const unsigned bm = __ballot_sync(kFull, np > 0 && pref_ex <= q);
+  PieceMeta pm;
+  pm.it = 31 - __clz(bm);
+  const uint32_t a0 = __shfl_sync(kFull, ia, pm.it), a1 = __shfl_sync(kFull, ib, pm.it);
+  const uint32_t px = __shfl_sync(kFull, pref_ex, pm.it);
+  pm.p0 = a0 + (q - px) * kPiece;
+  pm.p1 = min(a1, pm.p0 + kPiece);
+  return pm;
+}
+
+// Lane 0 arms stage `st` and issues the TMA bulk copy of piece pm (16-byte
+// aligned window of col[beg + p0, beg + p1)).
+__device__ __forceinline__ void issue_piece(const PieceMeta& pm, uint64_t b0, const uint32_t* col, uint32_t* ring,
+                                            uint64_t* bar, uint32_t st, int lane) {
+  if (lane == 0) {
+    const uint64_t g0 = (b0 + pm.p0) & ~3ull, g1 = (b0 + pm.p1 + 3) & ~3ull;
+    const uint32_t bytes = static_cast<uint32_t>(g1 - g0) * 4;
+    ptx::mbar_arrive_expect_tx(bar + st, bytes);
+    ptx::bulk_g2s(ring + st * kPieceBuf, col + g0, bytes, bar + st);
+  }
+}
+
+template <int WM>
+__global__ void __launch_bounds__(kStreamWarps * 32) k_stream(SampleArgs a) {
+  using P = typename PolOf<WM>::P;
+  using K = typename P::K;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* ring = reinterpret_cast<uint32_t*>(smem_raw) + static_cast<size_t>(warp) * kStages * kPieceBuf;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + static_cast<size_t>(kStreamWarps) * kStages * kPieceBuf * 4) +
+                  warp * kStages;
+  if (lane == 0) {
+    for (uint32_t s = 0; s < kStages; ++s) ptx::mbar_init(bar + s, 1);
+    ptx::fence_mbar_init();
+  }
+  __syncwarp();
+  const uint32_t nitems = min(*a.item_count, a.hub.item_cap);
+  const uint32_t m = a.f;
+  // claim size: spread small layers over all warps, amortise the atomic on big ones
+  const uint32_t nwarps_total = gridDim.x * kStreamWarps;
+  const uint32_t claim = max(1u, min(kItemsPerClaim, nitems / (4 * nwarps_total)));
+  uint32_t Q = 0;  // pieces consumed by this warp so far (ring position / parity)
+  for (;;) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(a.item_work, claim);
+    base = __shfl_sync(kFull, base, 0);
+    if (base >= nitems) break;
+    // lane i < claim holds item i's meta
+    uint4 itm = make_uint4(0, 0, 0, kInv);
+    uint64_t beg = 0, key = 0;
+    uint32_t np = 0;
+    if (lane < static_cast<int>(claim) && base + lane < nitems) {
+      itm = a.hub.items[base + lane];
+      const uint32_t dst = __ldg(a.front + itm.x);
+      beg = __ldg(a.ro + dst);
+      key = hash2(a.seed, hash2(a.layer, dst));
+      np = (itm.z - itm.y + kPiece - 1) / kPiece;
+    }
+    uint32_t pref = np;  // inclusive scan of pieces
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, pref, off);
+      if (lane >= off) pref += y;
+    }
+    const uint32_t NP = __shfl_sync(kFull, pref, 31);
+    const uint32_t pref_ex = pref - np;
+    for (uint32_t q = 0; q < min(NP, kStages); ++q) {
+      const PieceMeta pm = piece_meta(q, np, pref_ex, itm.y, itm.z);
+      issue_piece(pm, __shfl_sync(kFull, beg, pm.it), a.col, ring, bar, (Q + q) % kStages, lane);
+    }
+    rsv::WState<K> wst;
+    P pol = PolOf<WM>::make(a);
+    uint32_t rcnt = 0, ulast = kInv, uid = 0;
+    for (uint32_t q = 0; q < NP; ++q) {
+      const PieceMeta pm = piece_meta(q, np, pref_ex, itm.y, itm.z);
+      const uint4 im = make_uint4(__shfl_sync(kFull, itm.x, pm.it), __shfl_sync(kFull, itm.y, pm.it),
+                                  __shfl_sync(kFull, itm.z, pm.it), __shfl_sync(kFull, itm.w, pm.it));
+      const uint64_t b0 = __shfl_sync(kFull, beg, pm.it);
+      const uint64_t ky = __shfl_sync(kFull, key, pm.it);
+      const uint32_t st = (Q + q) % kStages;
+      ptx::mbar_wait(bar + st, ((Q + q) / kStages) & 1u);
+      // nb[j] == col[beg + j] for j in [p0, p1)
+      const uint32_t* nb = ring + st * kPieceBuf - static_cast<int64_t>(((b0 + pm.p0) & ~3ull) - b0);
+      const bool seg = im.w != kInv;
+      const bool first_piece = pm.p0 == im.y, last_piece = pm.p1 == im.z;
+      uint32_t* rid = nullptr;
+      uint64_t* rkey = nullptr;
+      if (seg) {
+        rid = a.hub.rec_id + static_cast<uint64_t>(im.w) * kRecCap;
+        rkey = a.hub.rec_key + static_cast<uint64_t>(im.w) * kRecCap;
+      }
+      if (a.kind == A3G_SAMPLER_UNIFORM) {
+        if (!seg) {
+          if (first_piece) uid = lane < static_cast<int>(m) ? nb[lane] : 0u;
+          const uint64_t jb = pm.p0 > m ? pm.p0 : static_cast<uint64_t>(m);
+          if (jb < pm.p1) rsv::uniform_range(nb, jb, pm.p1, m, ky, lane, 0, uid);
+        } else {
+          if (first_piece) ulast = kInv;
+          const uint64_t jb = pm.p0 > m ? pm.p0 : static_cast<uint64_t>(m);
+          for (uint64_t b = jb; b < pm.p1; b += 32) {
+            const uint64_t j = b + lane;
+            uint32_t r = kInv;
+            if (j < pm.p1) r = static_cast<uint32_t>(__umul64hi(draw(ky, j - m + 1), j + 1));
+            unsigned mask = __ballot_sync(kFull, j < pm.p1 && r < m);
+            while (mask) {
+              const int src = __ffs(mask) - 1;
+              const uint32_t slot = __shfl_sync(kFull, r, src);
+              if (lane == static_cast<int>(slot)) ulast = static_cast<uint32_t>(b + src);
+              mask &= mask - 1;
+            }
+          }
+        }
+      } else if (seg) {
+        uint64_t jb = pm.p0;
+        if (first_piece) {
+          const uint32_t nf = min(m, im.z - im.y);
+          rsv::fill_slots(nb, im.y, nf, ky, 0, lane, pol, wst, FillEmit<K>{rid, rkey});
+          rcnt = nf;
+          jb = im.y + nf;
+        }
+        if (im.z - im.y >= m && jb < pm.p1) {
+          SegEmit<K> em{rid, rkey, &rcnt, kRecCap, lane};
+          rsv::replay_range(nb, jb, pm.p1, ky, 0, lane, pol, wst, em);
+        }
+      } else {
+        uint64_t jb = pm.p0;
+        if (first_piece) {
+          rsv::fill_slots(nb, 0, m, ky, 0, lane, pol, wst, rsv::NoEmit{});
+          jb = m;
+        }
+        if (jb < pm.p1) rsv::replay_range(nb, jb, pm.p1, ky, 0, lane, pol, wst, rsv::NoEmit{});
+      }
+      if (last_piece) {
+        if (seg) {
+          if (a.kind == A3G_SAMPLER_UNIFORM) {
+            a.hub.slot_last[static_cast<uint64_t>(im.w) * 32 + lane] = ulast;
+          } else if (lane == 0) {
+            a.hub.rec_cnt[im.w] = rcnt;
+            a.hub.tau[im.w] = *reinterpret_cast<const uint64_t*>(&wst.thr);
+            a.hub.tau_ok[im.w] = (im.z - im.y >= m) ? 1u : 0u;
+          }
+        } else {
+          const uint64_t row0 = static_cast<uint64_t>(im.x) * m;
+          const uint32_t id = a.kind == A3G_SAMPLER_UNIFORM ? uid : wst.my_id;
+          if (lane < static_cast<int>(m)) {
+            a.S[row0 + lane] = id;
+            mark_first(a.first, id, a.tag, static_cast<uint32_t>(row0 + lane));
+          }
+          if (lane == 0) a.cnt[im.x] = m;
+        }
+      }
+      __syncwarp();
+      if (q + kStages < NP) {
+        if (lane == 0) ptx::fence_proxy_async_smem();
+        const PieceMeta pn = piece_meta(q + kStages, np, pref_ex, itm.y, itm.z);
+        issue_piece(pn, __shfl_sync(kFull, beg, pn.it), a.col, ring, bar, st, lane);
+      }
+    }
+    Q += NP;
+  }
+}
+
+// Warp per hub with few segments (<= kMergeFilterWarps): replay the records in
+// segment order, dropping those that cannot beat max_{s'<s} tau_{s'}.
+template <int WM>
+__global__ void __launch_bounds__(256) k_hub_merge_warp(SampleArgs a);
 
 constexpr int kMergeFilterWarps = 8;
 constexpr int kMergeThreads = (kMergeFilterWarps + 1) * 32;
@@ -323,7 +484,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_hub_merge(SampleArgs a) {
     }
     __syncthreads();
     const uint32_t ns = s_hub[0];
-    if (ns == 0) {  // processed by k_sample_rows
+    if (ns <= kMergeFilterWarps) {  // 0: streamed whole; small: k_hub_merge_warp
       __syncthreads();
       continue;
     }
@@ -490,6 +651,98 @@ __global__ void __launch_bounds__(kMergeThreads) k_hub_merge(SampleArgs a) {
       if (lane == 0) a.cnt[k] = m;
     }
     __syncthreads();
+  }
+}
+
+template <int WM>
+__global__ void __launch_bounds__(256) k_hub_merge_warp(SampleArgs a) {
+  using P = typename PolOf<WM>::P;
+  using K = typename P::K;
+  const int lane = threadIdx.x & 31;
+  const uint32_t nhub = min(*a.hub_count, a.hub.hub_cap);
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t m = a.f;
+  for (uint32_t h = gw; h < nhub; h += nw) {
+    const uint32_t ns = a.hub.nseg[h];
+    if (ns == 0 || ns > kMergeFilterWarps) continue;
+    const uint32_t s0 = a.hub.seg0[h], k = a.hub.row[h];
+    const uint32_t dst = a.front[k];
+    const uint64_t beg = a.ro[dst], deg = a.ro[dst + 1] - beg;
+    const uint32_t* nb = a.col + beg;
+    const uint64_t key = hash2(a.seed, hash2(a.layer, dst));
+    const uint64_t row0 = static_cast<uint64_t>(k) * m;
+    uint32_t rc_l = 0, tok_l = 0;
+    uint64_t tau_l = 0;
+    if (lane < static_cast<int>(ns)) {
+      rc_l = a.hub.rec_cnt[s0 + lane];
+      tok_l = a.hub.tau_ok[s0 + lane];
+      tau_l = a.hub.tau[s0 + lane];
+    }
+    uint32_t my_id;
+    if (a.kind == A3G_SAMPLER_UNIFORM) {
+      my_id = lane < static_cast<int>(m) ? nb[lane] : 0u;
+      for (int s = static_cast<int>(ns) - 1; s >= 0; --s) {
+        const uint32_t last = a.hub.slot_last[static_cast<uint64_t>(s0 + s) * 32 + lane];
+        if (last != kInv) {
+          my_id = nb[last];
+          break;
+        }
+      }
+    } else if (__ballot_sync(kFull, rc_l > kRecCap)) {  // records overflowed: whole-row replay
+      row_by_warp<WM>(a, nb, deg, key, k, lane);
+      continue;
+    } else {
+      P pol = PolOf<WM>::make(a);
+      rsv::WState<K> st;
+      const uint64_t rb0 = static_cast<uint64_t>(s0) * kRecCap;
+      st.my_key = lane < static_cast<int>(m) ? key_from_bits<K>(a.hub.rec_key[rb0 + lane]) : pol.inf();
+      st.my_id = lane < static_cast<int>(m) ? a.hub.rec_id[rb0 + lane] : 0u;
+      pol.argmin(st.thr, st.mp, st.my_key, lane);
+      K L{};
+      bool lok = false;
+      for (uint32_t s = 0; s < ns; ++s) {
+        const uint32_t rc = __shfl_sync(kFull, rc_l, s);
+        const uint64_t rb = static_cast<uint64_t>(s0 + s) * kRecCap;
+        for (uint32_t i0 = (s == 0 ? m : 0); i0 < rc; i0 += 32) {
+          const uint32_t i = i0 + lane;
+          const bool valid = i < rc;
+          K kk{};
+          uint32_t v = 0;
+          if (valid) {
+            kk = key_from_bits<K>(a.hub.rec_key[rb + i]);
+            v = a.hub.rec_id[rb + i];
+          }
+          const bool keep = valid && (!lok || pol.keep(kk, L));
+          unsigned mask = __ballot_sync(kFull, keep && pol.cheap_gt(kk, st.thr));
+          while (mask) {
+            const int src = __ffs(mask) - 1;
+            const K kv = __shfl_sync(kFull, kk, src);
+            const uint32_t iv = __shfl_sync(kFull, v, src);
+            if (pol.gt(kv, st.thr)) {
+              if (lane == st.mp) {
+                st.my_key = kv;
+                st.my_id = iv;
+              }
+              pol.argmin(st.thr, st.mp, st.my_key, lane);
+              mask &= __ballot_sync(kFull, keep && pol.cheap_gt(kk, st.thr));
+            }
+            mask &= ~((2u << src) - 1u);
+          }
+        }
+        if (__shfl_sync(kFull, tok_l, s)) {
+          const K ts = key_from_bits<K>(__shfl_sync(kFull, tau_l, s));
+          if (!lok || ts > L) L = ts;
+          lok = true;
+        }
+      }
+      my_id = st.my_id;
+    }
+    if (lane < static_cast<int>(m)) {
+      a.S[row0 + lane] = my_id;
+      mark_first(a.first, my_id, a.tag, static_cast<uint32_t>(row0 + lane));
+    }
+    if (lane == 0) a.cnt[k] = m;
   }
 }
 
@@ -774,17 +1027,21 @@ __global__ void k_gather_unique(const T* feat, uint32_t pitch, uint32_t F, const
 
 template <int WM>
 void launch_layer_kernels(const SampleArgs& sa, int sm_count, cudaStream_t st) {
-  k_sample_rows<WM><<<sm_count * 4, 256, 0, st>>>(sa);
-  A3G_LAUNCH_CHECK("k_sample_rows");
+  k_classify<WM><<<sm_count * 2, 256, 0, st>>>(sa);
+  A3G_LAUNCH_CHECK("k_classify");
   if (sa.f <= 32) {
-    k_hub_segments<WM><<<sm_count * 8, 256, 0, st>>>(sa);
-    A3G_LAUNCH_CHECK("k_hub_segments");
     static bool attr_set = false;
     if (!attr_set) {
+      A3G_CUDA(cudaFuncSetAttribute(k_stream<WM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kStreamSmem)));
       A3G_CUDA(cudaFuncSetAttribute(k_hub_merge<WM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kMergeSmem)));
       attr_set = true;
     }
+    k_stream<WM><<<sm_count * 3, kStreamWarps * 32, kStreamSmem, st>>>(sa);
+    A3G_LAUNCH_CHECK("k_stream");
+    k_hub_merge_warp<WM><<<sm_count * 2, 256, 0, st>>>(sa);
+    A3G_LAUNCH_CHECK("k_hub_merge_warp");
     k_hub_merge<WM><<<sm_count * 2, kMergeThreads, kMergeSmem, st>>>(sa);
     A3G_LAUNCH_CHECK("k_hub_merge");
   }
@@ -855,6 +1112,8 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
     sa.hub = s.hub;
     sa.hub_count = &ctr->hubs[l];
     sa.seg_count = &ctr->segs[l];
+    sa.item_count = &ctr->items[l];
+    sa.item_work = &ctr->iwork[l];
     sa.seed = rng_seed;
     sa.gamma = gamma;
     sa.inv_gamma = 1.0 / gamma;

@@ -36,6 +36,8 @@ struct HubArena {
   uint32_t* rec_id = nullptr;    // [seg_cap * kRecCap]
   uint64_t* rec_key = nullptr;   // [seg_cap * kRecCap] policy key bits
   uint32_t* slot_last = nullptr; // [seg_cap * 32] uniform kind: last position per slot
+  uint32_t item_cap = 0;
+  uint4* items = nullptr;        // [item_cap] stream work: (row, begin, end, segment | kInv)
 };
 
 struct SamplerState {

@@ -39,6 +39,18 @@ typedef enum a3g_status {
 
 enum { A3G_SAMPLER_WEIGHTED = 0, A3G_SAMPLER_UNIFORM = 1 }; /* sampler.hpp:18-21 */
 enum { A3G_FEAT_F32 = 0, A3G_FEAT_BF16 = 1 };
+/* Feature placement of the reference's static cache (cache.cpp:12-46). */
+enum { A3G_STORE_HBM = 0, A3G_STORE_CACHE = 1, A3G_STORE_SHARDED = 2 };
+/* Per-step statistics rows of a3g_trainer_step_stats. */
+enum {
+  A3G_STAT_UNIQUE = 0, /* |unique_nodes| */
+  A3G_STAT_EDGES = 1,  /* total sampled edges */
+  A3G_STAT_INNER = 2,  /* inner rows (seeds + layer-0 sources, trainer.cpp:76-89) */
+  A3G_STAT_SEEDS = 3,  /* unique seeds */
+  A3G_STAT_HITS = 4,   /* cache hits over unique_nodes (cache.cpp:48-68) */
+  A3G_STAT_MISSES = 5,
+  A3G_STEP_STATS = 8
+};
 
 typedef struct a3g_host_graph {
   /* graph.hpp:14-36 layout, host memory owned by the library */
@@ -58,6 +70,7 @@ typedef struct a3g_cache a3g_cache;     /* static hotness cache state */
 typedef struct a3g_sampler a3g_sampler; /* k-hop sampler arena (one batch in flight) */
 typedef struct a3g_trainer a3g_trainer; /* model, grads, streams, pipeline */
 typedef struct a3g_comm a3g_comm;       /* NCCL communicator (data-parallel sync) */
+typedef struct a3g_store a3g_store;     /* tiered feature store (HBM / NVLink peers / pinned host) */
 
 const char* a3g_last_error(void);
 const char* a3g_version(void);
@@ -91,6 +104,24 @@ a3g_status a3g_graph_create(int device, uint64_t num_nodes, uint64_t num_edges, 
                             const float* features, int feat_dtype, const uint32_t* labels,
                             a3g_graph** out);
 void a3g_graph_destroy(a3g_graph* g);
+
+/* --------------------------------------------------------------- store --- */
+/* Places the feature rows of `g` by `policy` (A3G_STORE_*) from host f32
+ * features (n x feat_dim, encoded to the graph's feat_dtype) and attaches the
+ * store to the graph: every gather of the path then reads through it.
+ * device_map: the cache placement (i32[n], -1 = miss, cache.hpp:31); ignored
+ * for A3G_STORE_HBM. rank/nranks: this GPU's shard for A3G_STORE_SHARDED. */
+a3g_status a3g_store_create(a3g_graph* g, const float* features, const int32_t* device_map, int policy,
+                            int rank, int nranks, a3g_store** out);
+a3g_status a3g_store_info(const a3g_store* s, uint64_t* local_rows, uint64_t* host_rows,
+                          uint64_t* remote_rows);
+/* Peer shards: same-process device pointers (a3g_store_local_ptr of the peer's
+ * store; peer access is enabled), or cudaIpc handles across processes. */
+a3g_status a3g_store_local_ptr(a3g_store* s, void** dev_ptr);
+a3g_status a3g_store_set_peer(a3g_store* s, int rank, void* dev_ptr);
+a3g_status a3g_store_ipc_handle(a3g_store* s, uint8_t handle[64]);
+a3g_status a3g_store_open_peer(a3g_store* s, int rank, const uint8_t handle[64]);
+void a3g_store_destroy(a3g_store* s); /* detaches; the graph keeps its own rows (if any) */
 
 /* --------------------------------------------------------------- cache --- */
 /* cache.cpp:12-46 build_static_cache: (out-degree desc, id asc), round-robin
@@ -181,6 +212,20 @@ a3g_status a3g_train_step(a3g_trainer* t, const uint32_t* seeds, uint32_t n_seed
 a3g_status a3g_train_steps(a3g_trainer* t, const uint32_t* seeds, uint32_t batch_size,
                            uint32_t num_steps, const uint64_t* rng_seeds, double bias_rate,
                            int kind, int seeds_on_device, double* losses_out);
+
+/* As a3g_train_steps with per-step batch sizes (the last batch of an epoch is
+ * short, trainer.cpp:338-341): batch i = seeds[offsets[i] .. offsets[i+1]). */
+a3g_status a3g_train_steps_v(a3g_trainer* t, const uint32_t* seeds, const uint64_t* offsets,
+                             uint32_t num_steps, const uint64_t* rng_seeds, double bias_rate, int kind,
+                             int seeds_on_device, double* losses_out);
+/* Statistics of the steps of the last a3g_train_steps[_v] call:
+ * out[i * A3G_STEP_STATS + A3G_STAT_*] for i < num_steps. */
+a3g_status a3g_trainer_step_stats(a3g_trainer* t, uint64_t* out, uint32_t num_steps);
+
+/* evaluate_full_graph (trainer.cpp:241-303) on the device with the trainer's
+ * current weights: full-neighbourhood 2-layer mean-GCN over all nodes, argmax
+ * accuracy over test_mask (host u8[n]). ConfigError when no test nodes. */
+a3g_status a3g_evaluate_full_graph(a3g_trainer* t, const uint8_t* test_mask, double* accuracy);
 
 /* Debug/parity copy-out of the last step (host f64 buffers; NULL skips):
  * gradients (F*H, H*C), and ForwardResult arrays (trainer.hpp:49-60). */

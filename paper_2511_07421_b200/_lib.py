@@ -85,6 +85,13 @@ _SIGS = {
     "a3g_graph_create": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint32, u64p, u32p, f32p, C.c_int, u32p,
                                    C.POINTER(vp)]),
     "a3g_graph_destroy": (None, [vp]),
+    "a3g_store_create": (C.c_int, [vp, f32p, i32p, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
+    "a3g_store_info": (C.c_int, [vp, u64p, u64p, u64p]),
+    "a3g_store_local_ptr": (C.c_int, [vp, C.POINTER(vp)]),
+    "a3g_store_set_peer": (C.c_int, [vp, C.c_int, vp]),
+    "a3g_store_ipc_handle": (C.c_int, [vp, u8p]),
+    "a3g_store_open_peer": (C.c_int, [vp, C.c_int, u8p]),
+    "a3g_store_destroy": (None, [vp]),
     "a3g_cache_build": (C.c_int, [vp, C.c_uint64, C.c_uint32, i32p, C.POINTER(vp)]),
     "a3g_cache_from_map": (C.c_int, [vp, i32p, C.c_uint32, C.POINTER(vp)]),
     "a3g_cache_total_cached": (C.c_uint64, [vp]),
@@ -108,6 +115,9 @@ _SIGS = {
     "a3g_train_step": (C.c_int, [vp, u32p, C.c_uint32, C.c_int, C.c_double, C.c_int, C.c_uint64, C.c_double,
                                  f64p]),
     "a3g_train_steps": (C.c_int, [vp, u32p, C.c_uint32, C.c_uint32, u64p, C.c_double, C.c_int, C.c_int, f64p]),
+    "a3g_train_steps_v": (C.c_int, [vp, u32p, u64p, C.c_uint32, u64p, C.c_double, C.c_int, C.c_int, f64p]),
+    "a3g_trainer_step_stats": (C.c_int, [vp, u64p, C.c_uint32]),
+    "a3g_evaluate_full_graph": (C.c_int, [vp, u8p, f64p]),
     "a3g_trainer_last_grads": (C.c_int, [vp, f64p, f64p]),
     "a3g_trainer_last_forward": (C.c_int, [vp, u64p, f64p, f64p, f64p, f64p]),
     "a3g_trainer_sampler": (vp, [vp, C.c_int]),

@@ -24,6 +24,27 @@ inline void cuda_check(cudaError_t e, const char* what) {
           std::string(what) + ": " + cudaGetErrorString(e));
   }
 }
+// Thread-local message behind a3g_last_error() (api.cu).
+void set_error(const std::string& msg);
+
+// Runs fn, mapping exceptions onto a3g_status (the C-ABI never throws).
+template <typename Fn>
+a3g_status guard(Fn&& fn) {
+  try {
+    fn();
+    return A3G_OK;
+  } catch (const Error& e) {
+    set_error(e.what());
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    set_error("host allocation failed");
+    return A3G_ERR_OOM;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return A3G_ERR_CUDA;
+  }
+}
+
 #define A3G_CUDA(x) ::a3g::cuda_check((x), #x)
 #define A3G_LAUNCH_CHECK(name) ::a3g::cuda_check(cudaGetLastError(), name)
 
@@ -73,7 +94,35 @@ struct BatchCounters {
   uint32_t pad;
 };
 
+// ------------------------------------------------------------ feature store -
+// Where feature row v lives. loc[v] = (tier << 28) | slot:
+// tier r < 15 = HBM shard of device r (local, or an NVLink peer pointer),
+// tier 15 = mapped pinned host memory (zero-copy over PCIe). loc == nullptr:
+// identity layout, row v at base[0] + v * row_bytes.
+constexpr uint32_t kLocShift = 28;
+constexpr uint32_t kLocSlotMask = (1u << kLocShift) - 1u;
+constexpr uint32_t kTierHost = 15;
+constexpr int kMaxTiers = 16;
+
+struct StoreView {
+  const uint8_t* base[kMaxTiers];
+  const uint32_t* loc;
+  uint32_t row_bytes;
+};
+
+#ifdef __CUDACC__
+// Kernels take StoreView inside a __grid_constant__ parameter so base[tier]
+// is an indexed constant-bank load, not a local-memory copy.
+__device__ __forceinline__ const uint8_t* row_ptr(const StoreView& s, uint32_t v) {
+  if (!s.loc) return s.base[0] + static_cast<uint64_t>(v) * s.row_bytes;
+  const uint32_t l = __ldg(s.loc + v);
+  return s.base[l >> kLocShift] + static_cast<uint64_t>(l & kLocSlotMask) * s.row_bytes;
+}
+#endif
+
 }  // namespace a3g
+
+struct a3g_store;
 
 // ---------------------------------------------------------- handles --------
 struct a3g_graph {
@@ -89,6 +138,8 @@ struct a3g_graph {
   std::vector<uint64_t> h_ro;       // host copy (validation, degrees)
   std::vector<uint32_t> h_labels;   // host copy
   bool has_features = false;
+  a3g::StoreView view{};            // how kernels reach feature rows (default: d_feat, identity)
+  a3g_store* store = nullptr;       // attached tiered store (a3g_store_create), else null
 };
 
 struct a3g_cache {

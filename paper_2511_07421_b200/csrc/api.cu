@@ -25,26 +25,12 @@ void comm_destroy(a3g_comm* c);
 
 using namespace a3g;
 
-namespace {
-thread_local std::string g_err;
-
-template <typename Fn>
-a3g_status guard(Fn&& fn) {
-  try {
-    fn();
-    return A3G_OK;
-  } catch (const Error& e) {
-    g_err = e.what();
-    return e.status;
-  } catch (const std::bad_alloc&) {
-    g_err = "host allocation failed";
-    return A3G_ERR_OOM;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return A3G_ERR_CUDA;
-  }
+namespace a3g {
+void set_error(const std::string& msg);
 }
 
+namespace {
+thread_local std::string g_err;
 template <typename T>
 T* dalloc(size_t count) {
   void* p = nullptr;
@@ -228,6 +214,8 @@ void init_weights(uint32_t F, uint32_t H, uint32_t C, uint64_t seed, std::vector
 
 }  // namespace
 
+void a3g::set_error(const std::string& msg) { g_err = msg; }
+
 // ====================================================================== ABI
 extern "C" {
 
@@ -297,11 +285,13 @@ a3g_status a3g_graph_create(int device, uint64_t n, uint64_t m, uint32_t F, cons
     }
     const size_t esz = feat_dtype == A3G_FEAT_BF16 ? 2 : 4;
     const size_t row_bytes = static_cast<size_t>(g->pitch) * esz;
-    void* d = nullptr;
-    A3G_CUDA(cudaMalloc(&d, std::max<size_t>(1, n * row_bytes)));
-    g->d_feat = d;
-    A3G_CUDA(cudaMemset(d, 0, n * row_bytes));
+    g->view.loc = nullptr;
+    g->view.row_bytes = static_cast<uint32_t>(row_bytes);
     if (features) {
+      void* d = nullptr;
+      A3G_CUDA(cudaMalloc(&d, std::max<size_t>(1, n * row_bytes)));
+      g->d_feat = d;
+      g->view.base[0] = static_cast<const uint8_t*>(d);
       g->has_features = true;
       // pitched upload in slabs through a host staging buffer
       const uint64_t slab = std::max<uint64_t>(1, (64ull << 20) / row_bytes);
@@ -334,6 +324,7 @@ a3g_status a3g_graph_create(int device, uint64_t n, uint64_t m, uint32_t F, cons
 void a3g_graph_destroy(a3g_graph* g) {
   if (!g) return;
   cudaSetDevice(g->device);
+  if (g->store) a3g_store_destroy(g->store);
   dfree(g->d_ro);
   dfree(g->d_col);
   dfree(g->d_labels);
@@ -643,6 +634,15 @@ a3g_status a3g_trainer_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds, co
       t.d_logits = dalloc<float>(static_cast<size_t>(max_seeds) * C);
       t.d_dlogits = dalloc<float>(static_cast<size_t>(max_seeds) * C);
       t.d_loss_s = dalloc<float>(max_seeds);
+      t.d_dagg = dalloc<float>(static_cast<size_t>(max_seeds) * H);
+      t.n_entries = static_cast<uint64_t>(max_seeds) * ((L >= 1 ? fanouts[0] : 1) + 1);
+      if (t.n_entries >= (1ull << 31)) raise(A3G_ERR_PARAMETER, "trainer: batch x fanout too large");
+      for (int i = 0; i < 2; ++i) {
+        t.d_keys[i] = dalloc<uint32_t>(t.n_entries);
+        t.d_vals[i] = dalloc<uint32_t>(t.n_entries);
+      }
+      t.sort_tmp_bytes = dh1_sort_temp_bytes(t.n_entries);
+      t.d_sort_tmp = dalloc<uint8_t>(t.sort_tmp_bytes);
       t.nparts = static_cast<uint32_t>(t.sm_count);
       t.d_part = dalloc<float>(static_cast<size_t>(t.nparts) * t.F * H);
       t.d_agg_bytes = dalloc<unsigned long long>(1);
@@ -692,9 +692,16 @@ void a3g_trainer_destroy(a3g_trainer* tr) {
   dfree(t.d_logits);
   dfree(t.d_dlogits);
   dfree(t.d_loss_s);
+  dfree(t.d_dagg);
+  for (int i = 0; i < 2; ++i) {
+    dfree(t.d_keys[i]);
+    dfree(t.d_vals[i]);
+  }
+  if (t.d_sort_tmp) cudaFree(t.d_sort_tmp);
   dfree(t.d_part);
   dfree(t.d_agg_bytes);
   dfree(t.d_losses);
+  dfree(t.d_stats);
   dfree(t.d_seed_buf);
   if (t.h_seed_stage) cudaFreeHost(t.h_seed_stage);
   if (t.h_losses) cudaFreeHost(t.h_losses);
@@ -745,7 +752,7 @@ a3g_status a3g_train_step(a3g_trainer* tr, const uint32_t* seeds, uint32_t n_see
     A3G_CUDA(cudaSetDevice(t.g->device));
     a3g_sampler* smp = t.smp[0];
     sample_impl(smp->st, seeds, n_seeds, on_device != 0, gamma, kind, rng_seed, t.s_comp);
-    launch_train_compute(t, smp, lr < 0 ? t.lr : lr, t.d_losses, t.s_comp, false);
+    launch_train_compute(t, smp, lr < 0 ? t.lr : lr, t.d_losses, nullptr, t.s_comp, false);
     if (loss_out) {
       A3G_CUDA(cudaMemcpyAsync(t.h_losses, t.d_losses, 8, cudaMemcpyDeviceToHost, t.s_comp));
       A3G_CUDA(cudaStreamSynchronize(t.s_comp));
@@ -756,15 +763,27 @@ a3g_status a3g_train_step(a3g_trainer* tr, const uint32_t* seeds, uint32_t n_see
 
 a3g_status a3g_train_steps(a3g_trainer* tr, const uint32_t* seeds, uint32_t B, uint32_t K,
                            const uint64_t* rng_seeds, double gamma, int kind, int on_device, double* losses_out) {
+  std::vector<uint64_t> off(static_cast<size_t>(K) + 1);
+  for (uint32_t i = 0; i <= K; ++i) off[i] = static_cast<uint64_t>(i) * B;
+  return a3g_train_steps_v(tr, seeds, off.data(), K, rng_seeds, gamma, kind, on_device, losses_out);
+}
+
+a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint64_t* off, uint32_t K,
+                             const uint64_t* rng_seeds, double gamma, int kind, int on_device, double* losses_out) {
   return guard([&] {
     TrainerState& t = tr->st;
     A3G_CUDA(cudaSetDevice(t.g->device));
+    t.last_steps = 0;
     if (K == 0) return;
-    if (B > t.max_seeds) raise(A3G_ERR_PARAMETER, "train_steps: batch larger than the arena");
-    const uint64_t total = static_cast<uint64_t>(B) * K;
-    for (uint32_t i = 0; i < K; ++i)
-      validate_sample(t.smp[0]->st, on_device ? nullptr : seeds + static_cast<uint64_t>(i) * B, B,
-                      !on_device, gamma, kind);
+    if (off[0] != 0) raise(A3G_ERR_PARAMETER, "train_steps: offsets[0] must be 0");
+    for (uint32_t i = 0; i < K; ++i) {
+      if (off[i + 1] < off[i]) raise(A3G_ERR_PARAMETER, "train_steps: offsets must be non-decreasing");
+      const uint64_t b = off[i + 1] - off[i];
+      if (b > t.max_seeds) raise(A3G_ERR_PARAMETER, "train_steps: batch larger than the arena");
+      validate_sample(t.smp[0]->st, on_device ? nullptr : seeds + off[i], static_cast<uint32_t>(b), !on_device,
+                      gamma, kind);
+    }
+    const uint64_t total = off[K];
     if (K > t.losses_cap) {
       dfree(t.d_losses);
       cudaFreeHost(t.h_losses);
@@ -772,9 +791,15 @@ a3g_status a3g_train_steps(a3g_trainer* tr, const uint32_t* seeds, uint32_t B, u
       A3G_CUDA(cudaMallocHost(&t.h_losses, K * 8ull));
       t.losses_cap = K;
     }
+    if (K > t.stats_cap) {
+      dfree(t.d_stats);
+      t.d_stats = dalloc<unsigned long long>(static_cast<size_t>(K) * A3G_STEP_STATS);
+      t.stats_cap = K;
+    }
     for (cudaEvent_t e : t.ev_agg) cudaEventDestroy(e);
     t.ev_agg.clear();
     A3G_CUDA(cudaMemsetAsync(t.d_agg_bytes, 0, 8, t.s_comp));
+    A3G_CUDA(cudaMemsetAsync(t.d_stats, 0, static_cast<size_t>(K) * A3G_STEP_STATS * 8, t.s_comp));
     A3G_CUDA(cudaEventRecord(t.ev_t0, t.s_comp));
     A3G_CUDA(cudaStreamWaitEvent(t.s_samp, t.ev_t0, 0));
     const uint32_t* dseeds = seeds;
@@ -782,8 +807,9 @@ a3g_status a3g_train_steps(a3g_trainer* tr, const uint32_t* seeds, uint32_t B, u
       if (total > t.seed_buf_cap) {
         dfree(t.d_seed_buf);
         if (t.h_seed_stage) cudaFreeHost(t.h_seed_stage);
+        t.h_seed_stage = nullptr;
         t.d_seed_buf = dalloc<uint32_t>(total);
-        A3G_CUDA(cudaMallocHost(&t.h_seed_stage, total * 4));
+        A3G_CUDA(cudaMallocHost(&t.h_seed_stage, std::max<uint64_t>(total, 1) * 4));
         t.seed_buf_cap = total;
       }
       std::memcpy(t.h_seed_stage, seeds, total * 4);
@@ -795,15 +821,18 @@ a3g_status a3g_train_steps(a3g_trainer* tr, const uint32_t* seeds, uint32_t B, u
     for (uint32_t i = 0; i < K; ++i) {
       a3g_sampler* smp = t.smp[i & 1];
       if (i >= 2) A3G_CUDA(cudaStreamWaitEvent(t.s_samp, t.ev_consumed[i & 1], 0));
-      sample_impl(smp->st, dseeds + static_cast<uint64_t>(i) * B, B, true, gamma, kind, rng_seeds[i], t.s_samp);
+      sample_impl(smp->st, dseeds + off[i], static_cast<uint32_t>(off[i + 1] - off[i]), true, gamma, kind,
+                  rng_seeds[i], t.s_samp);
       A3G_CUDA(cudaEventRecord(t.ev_sampled[i & 1], t.s_samp));
       A3G_CUDA(cudaStreamWaitEvent(t.s_comp, t.ev_sampled[i & 1], 0));
-      launch_train_compute(t, smp, t.lr, t.d_losses + i, t.s_comp, t.timing);
+      launch_train_compute(t, smp, t.lr, t.d_losses + i, t.d_stats + static_cast<size_t>(i) * A3G_STEP_STATS,
+                           t.s_comp, t.timing);
       A3G_CUDA(cudaEventRecord(t.ev_consumed[i & 1], t.s_comp));
     }
     A3G_CUDA(cudaMemcpyAsync(t.h_losses, t.d_losses, K * 8ull, cudaMemcpyDeviceToHost, t.s_comp));
     A3G_CUDA(cudaEventRecord(t.ev_t1, t.s_comp));
     A3G_CUDA(cudaStreamSynchronize(t.s_comp));
+    t.last_steps = K;
     if (losses_out) std::memcpy(losses_out, t.h_losses, K * 8ull);
     float ms = 0;
     A3G_CUDA(cudaEventElapsedTime(&ms, t.ev_t0, t.ev_t1));
@@ -819,6 +848,29 @@ a3g_status a3g_train_steps(a3g_trainer* tr, const uint32_t* seeds, uint32_t B, u
     unsigned long long bytes = 0;
     A3G_CUDA(cudaMemcpy(&bytes, t.d_agg_bytes, 8, cudaMemcpyDeviceToHost));
     t.last_agg_bytes = t.last_agg_launches ? static_cast<double>(bytes) / t.last_agg_launches : 0;
+  });
+}
+
+a3g_status a3g_trainer_step_stats(a3g_trainer* tr, uint64_t* out, uint32_t K) {
+  return guard([&] {
+    TrainerState& t = tr->st;
+    if (K > t.last_steps) raise(A3G_ERR_PARAMETER, "step_stats: more steps than the last train_steps ran");
+    if (K == 0) return;
+    A3G_CUDA(cudaSetDevice(t.g->device));
+    A3G_CUDA(cudaMemcpy(out, t.d_stats, static_cast<size_t>(K) * A3G_STEP_STATS * 8, cudaMemcpyDeviceToHost));
+    for (uint32_t i = 0; i < K; ++i) {
+      uint64_t* r = out + static_cast<size_t>(i) * A3G_STEP_STATS;
+      r[A3G_STAT_MISSES] = r[A3G_STAT_UNIQUE] - r[A3G_STAT_HITS];
+    }
+  });
+}
+
+a3g_status a3g_evaluate_full_graph(a3g_trainer* tr, const uint8_t* test_mask, double* accuracy) {
+  return guard([&] {
+    TrainerState& t = tr->st;
+    A3G_CUDA(cudaSetDevice(t.g->device));
+    if (!test_mask) raise(A3G_ERR_PARAMETER, "evaluate_full_graph: test_mask required");
+    *accuracy = evaluate_full_graph(t, test_mask);
   });
 }
 

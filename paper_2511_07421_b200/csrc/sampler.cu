@@ -1000,9 +1000,9 @@ __device__ __forceinline__ float to_f32<uint16_t>(uint16_t x) {
 }
 
 template <typename T>
-__global__ void k_gather_unique(const T* feat, uint32_t pitch, uint32_t F, const uint32_t* unique,
-                                const uint32_t* ucount, const uint32_t* bits, int bitmode,
-                                float* out, BatchCounters* ctr) {
+__global__ void k_gather_unique(const __grid_constant__ StoreView view, uint32_t F, const uint32_t* unique,
+                                const uint32_t* ucount, const uint32_t* bits, int bitmode, float* out,
+                                BatchCounters* ctr) {
   const uint32_t U = *ucount;
   const int lane = threadIdx.x & 31;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1010,7 +1010,7 @@ __global__ void k_gather_unique(const T* feat, uint32_t pitch, uint32_t F, const
   uint32_t hits = 0, seen = 0;
   for (uint32_t i = gw; i < U; i += nw) {
     const uint32_t v = unique[i];
-    const T* src = feat + static_cast<uint64_t>(v) * pitch;
+    const T* src = reinterpret_cast<const T*>(row_ptr(view, v));
     float* dst = out + static_cast<uint64_t>(i) * F;
     for (uint32_t c = lane; c < F; c += 32) dst[c] = to_f32<T>(src[c]);
     if (lane == 0) {
@@ -1173,13 +1173,11 @@ void launch_gather_unique(SamplerState& s, float* out, cudaStream_t st) {
   const int bitmode = c->all_cached ? 1 : (c->none_cached ? 0 : 2);
   const uint32_t* uc = &s.d_ctr->ucount[s.L];
   if (g->feat_dtype == A3G_FEAT_BF16)
-    k_gather_unique<uint16_t><<<s.sm_count * 4, 256, 0, st>>>(
-        static_cast<const uint16_t*>(g->d_feat), g->pitch, g->F, s.d_unique, uc, c->d_bits, bitmode,
-        out, s.d_ctr);
+    k_gather_unique<uint16_t><<<s.sm_count * 4, 256, 0, st>>>(g->view, g->F, s.d_unique, uc, c->d_bits,
+                                                               bitmode, out, s.d_ctr);
   else
-    k_gather_unique<float><<<s.sm_count * 4, 256, 0, st>>>(static_cast<const float*>(g->d_feat),
-                                                            g->pitch, g->F, s.d_unique, uc,
-                                                            c->d_bits, bitmode, out, s.d_ctr);
+    k_gather_unique<float><<<s.sm_count * 4, 256, 0, st>>>(g->view, g->F, s.d_unique, uc, c->d_bits, bitmode,
+                                                            out, s.d_ctr);
   A3G_LAUNCH_CHECK("k_gather_unique");
 }
 

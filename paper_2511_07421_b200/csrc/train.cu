@@ -18,6 +18,8 @@
 //   k_sgd         w -= lr * g (trainer.cpp:208-211).
 #include <cmath>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "trainer.cuh"
 
 namespace a3g {
@@ -54,7 +56,7 @@ struct Chunk<uint16_t> {  // bf16
 };
 
 struct AggArgs {
-  const void* feat;
+  StoreView view;  // feature rows: local HBM / NVLink peer / pinned host (store.cu)
   uint32_t pitch, F, H;
   const uint32_t* unique;
   const int32_t* inv1;
@@ -70,7 +72,7 @@ struct AggArgs {
 };
 
 template <typename T, int NCH>
-__global__ void __launch_bounds__(kAggThreads) k_agg1(AggArgs a) {
+__global__ void __launch_bounds__(kAggThreads) k_agg1(const __grid_constant__ AggArgs a) {
   using Ch = Chunk<T>;
   constexpr int EPC = Ch::EPC;
   extern __shared__ float smem[];
@@ -82,8 +84,6 @@ __global__ void __launch_bounds__(kAggThreads) k_agg1(AggArgs a) {
   float* buf = s_buf + static_cast<size_t>(warp) * a.pitch;
   const uint32_t n_inner = *a.n_inner;
   const uint32_t chunks = a.pitch / EPC;  // 16-byte chunks per row
-  const uint4* feat = static_cast<const uint4*>(a.feat);
-  const uint32_t row_chunks = chunks;     // row stride in uint4 units
   unsigned long long nbytes = 0;
   const uint32_t gw = blockIdx.x * kAggWarps + warp, nw = gridDim.x * kAggWarps;
   const uint32_t H = a.H, F = a.F;
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kAggThreads) k_agg1(AggArgs a) {
       for (int e = 0; e < EPC; ++e) acc[i][e] = 0.f;
     float scale = 1.f;
     if (c == 0) {  // self-fallback: own features (trainer.cpp:102-107)
-      const uint4* row = feat + static_cast<uint64_t>(__ldg(a.unique + r)) * row_chunks;
+      const uint4* row = reinterpret_cast<const uint4*>(row_ptr(a.view, __ldg(a.unique + r)));
 #pragma unroll
       for (int i = 0; i < NCH; ++i) {
         const uint32_t q = lane + 32 * i;
@@ -109,8 +109,8 @@ __global__ void __launch_bounds__(kAggThreads) k_agg1(AggArgs a) {
       const uint32_t* srcs = a.S1 + static_cast<uint64_t>(k) * a.f1;
       uint32_t t = 0;
       for (; t + 1 < c; t += 2) {
-        const uint4* r0 = feat + static_cast<uint64_t>(__ldg(srcs + t)) * row_chunks;
-        const uint4* r1 = feat + static_cast<uint64_t>(__ldg(srcs + t + 1)) * row_chunks;
+        const uint4* r0 = reinterpret_cast<const uint4*>(row_ptr(a.view, __ldg(srcs + t)));
+        const uint4* r1 = reinterpret_cast<const uint4*>(row_ptr(a.view, __ldg(srcs + t + 1)));
         uint4 x0[NCH], x1[NCH];
 #pragma unroll
         for (int i = 0; i < NCH; ++i) {
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kAggThreads) k_agg1(AggArgs a) {
         }
       }
       if (t < c) {
-        const uint4* r0 = feat + static_cast<uint64_t>(__ldg(srcs + t)) * row_chunks;
+        const uint4* r0 = reinterpret_cast<const uint4*>(row_ptr(a.view, __ldg(srcs + t)));
 #pragma unroll
         for (int i = 0; i < NCH; ++i) {
           const uint32_t q = lane + 32 * i;
@@ -178,6 +178,31 @@ __global__ void __launch_bounds__(kAggThreads) k_agg1(AggArgs a) {
   if (lane == 0 && nbytes) atomicAdd(a.bytes, nbytes);
 }
 
+// Per-step statistics (a3g_trainer_step_stats): batch sizes from the sampler's
+// counters and the cache hit/miss count over unique_nodes (lookup,
+// cache.cpp:48-68: any-device presence is a hit).
+__global__ void k_step_stats(const BatchCounters* ctr, const uint32_t* unique, const uint32_t* bits, int bitmode,
+                             uint32_t L, unsigned long long* out) {
+  const uint32_t U = ctr->ucount[L];
+  const int lane = threadIdx.x & 31;
+  uint32_t hits = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < U; i += gridDim.x * blockDim.x) {
+    const uint32_t v = unique[i];
+    hits += (bitmode == 1 || (bitmode == 2 && ((__ldg(bits + (v >> 5)) >> (v & 31)) & 1u))) ? 1u : 0u;
+  }
+  hits = __reduce_add_sync(kFull, hits);
+  if (lane == 0 && hits) atomicAdd(out + A3G_STAT_HITS, static_cast<unsigned long long>(hits));
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    uint64_t E = 0;
+    for (uint32_t l = 0; l < L; ++l) E += ctr->edges[l];
+    out[A3G_STAT_UNIQUE] = U;
+    out[A3G_STAT_EDGES] = E;
+    out[A3G_STAT_INNER] = L >= 1 ? ctr->ucount[1] : ctr->ucount[0];
+    out[A3G_STAT_SEEDS] = ctr->ucount[0];
+    // misses = U - hits, derived on the host (a3g_trainer_step_stats)
+  }
+}
+
 struct OuterArgs {
   const float* h1;
   const uint32_t* cnt0;
@@ -192,7 +217,10 @@ struct OuterArgs {
   float* logits;
   float* dlogits;
   float* loss_s;
-  float* dh1;
+  float* dagg;     // [cap_seeds x H] per-edge dh1 contribution of seed s
+  uint32_t* keys;  // [cap_seeds x (f0 + 1)] dh1 row of each scatter entry (kInv: none)
+  uint32_t* vals;  // seed of each scatter entry
+  uint32_t cap_seeds;
   int has_layer0;
 };
 
@@ -241,20 +269,51 @@ __global__ void __launch_bounds__(256) k_outer(OuterArgs a) {
       a.dlogits[static_cast<uint64_t>(s) * C + lane] = d;
     }
     if (lane == 0) a.loss_s[s] = -(zy - mx - logf(den));
-    // dagg_outer = dlogits . W2^T, scatter into dh1
+    // dagg_outer = dlogits . W2^T (trainer.cpp:177-179), pre-scaled by the
+    // outer mean's 1/deg: the contribution of each of the seed's edges
     float dg = 0.f;
     for (uint32_t cc = 0; cc < C; ++cc) {
       const float dc = __shfl_sync(kFull, d, cc);
       if (lane < H) dg = fmaf(dc, a.w2[lane * C + cc], dg);
     }
-    if (lane < H) {
-      if (c0 == 0) {
-        atomicAdd(a.dh1 + static_cast<uint64_t>(s) * H + lane, dg);
-      } else {
-        const float w = 1.f / static_cast<float>(c0);
-        for (uint32_t t = 0; t < c0; ++t) atomicAdd(a.dh1 + static_cast<uint64_t>(srcs[t]) * H + lane, w * dg);
-      }
+    if (lane < H) a.dagg[static_cast<uint64_t>(s) * H + lane] = c0 == 0 ? dg : (1.f / static_cast<float>(c0)) * dg;
+    // scatter entries (dh1 row <- seed s), sorted stably by row next: edge
+    // entries in edge order, then the self-fallback entry (trainer.cpp:182-198)
+    const uint64_t e0 = static_cast<uint64_t>(s) * a.f0;
+    for (uint32_t t = lane; t < a.f0; t += 32) {
+      a.keys[e0 + t] = t < c0 ? srcs[t] : kInv;
+      a.vals[e0 + t] = s;
     }
+    if (lane == 0) {
+      const uint64_t fb = static_cast<uint64_t>(a.cap_seeds) * a.f0 + s;
+      a.keys[fb] = c0 == 0 ? s : kInv;
+      a.vals[fb] = s;
+    }
+  }
+  // pad the unused tail of the entry arrays (rows ns .. cap_seeds)
+  const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(ns) * a.f0 + gt; i < static_cast<uint64_t>(a.cap_seeds) * a.f0; i += nt)
+    a.keys[i] = kInv;
+  for (uint64_t i = static_cast<uint64_t>(a.cap_seeds) * a.f0 + ns + gt;
+       i < static_cast<uint64_t>(a.cap_seeds) * (a.f0 + 1); i += nt)
+    a.keys[i] = kInv;
+}
+
+// dh1[r] = sum of the contributions of the sorted entries with key r, in
+// order (edges in edge order, then the fallback): deterministic, no atomics.
+__global__ void __launch_bounds__(256) k_dh1_gather(const uint32_t* keys, const uint32_t* vals, uint64_t n_entries,
+                                                    const float* dagg, uint32_t H, float* dh1) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t i = gw; i < n_entries; i += nw) {
+    const uint32_t r = keys[i];
+    if (r == kInv) break;  // sorted: the padding is last
+    if (i > 0 && keys[i - 1] == r) continue;  // not the head of its run
+    float acc = 0.f;
+    for (uint64_t j = i; j < n_entries && keys[j] == r; ++j)
+      if (lane < static_cast<int>(H)) acc += dagg[static_cast<uint64_t>(vals[j]) * H + lane];
+    if (lane < static_cast<int>(H)) dh1[static_cast<uint64_t>(r) * H + lane] = acc;
   }
 }
 
@@ -427,14 +486,20 @@ void launch_dw1_h(const Dw1Args& da, int ncol, uint32_t nparts, cudaStream_t st)
 void comm_allreduce_sum(a3g_comm* comm, float* buf, size_t count, cudaStream_t st);
 
 void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* d_loss_slot,
-                          cudaStream_t st, bool record_timing) {
+                          unsigned long long* d_stats, cudaStream_t st, bool record_timing) {
   SamplerState& s = smp->st;
   a3g_graph* g = t.g;
   BatchCounters* ctr = s.d_ctr;
   A3G_CUDA(cudaMemsetAsync(t.d_dh1, 0, t.cap_inner * t.H * sizeof(float), st));
+  if (d_stats) {
+    const a3g_cache* c = t.c;
+    const int bitmode = c->all_cached ? 1 : (c->none_cached ? 0 : 2);
+    k_step_stats<<<t.sm_count, 256, 0, st>>>(ctr, s.d_unique, c->d_bits, bitmode, s.L, d_stats);
+    A3G_LAUNCH_CHECK("k_step_stats");
+  }
   // ---- gather + aggregation + GEMM1 (forward, inner rows)
   AggArgs aa{};
-  aa.feat = g->d_feat;
+  aa.view = g->view;
   aa.pitch = g->pitch;
   aa.F = t.F;
   aa.H = t.H;
@@ -484,9 +549,21 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
   oa.logits = t.d_logits;
   oa.dlogits = t.d_dlogits;
   oa.loss_s = t.d_loss_s;
-  oa.dh1 = t.d_dh1;
+  oa.dagg = t.d_dagg;
+  oa.keys = t.d_keys[0];
+  oa.vals = t.d_vals[0];
+  oa.cap_seeds = t.max_seeds;
+  if (oa.f0 == 0) oa.f0 = 1;  // no layer: fallback entries only (keys of the edge part are all kInv)
   k_outer<<<std::max(1, static_cast<int>((t.max_seeds + 7) / 8)), 256, 0, st>>>(oa);
   A3G_LAUNCH_CHECK("k_outer");
+  // ---- deterministic scatter into dh1: stable radix sort of the entries by row
+  {
+    size_t tmp = t.sort_tmp_bytes;
+    A3G_CUDA(cub::DeviceRadixSort::SortPairs(t.d_sort_tmp, tmp, t.d_keys[0], t.d_keys[1], t.d_vals[0], t.d_vals[1],
+                                             static_cast<int>(t.n_entries), 0, 32, st));
+    k_dh1_gather<<<t.sm_count * 2, 256, 0, st>>>(t.d_keys[1], t.d_vals[1], t.n_entries, t.d_dagg, t.H, t.d_dh1);
+    A3G_LAUNCH_CHECK("k_dh1_gather");
+  }
   // ---- dW1 partials
   Dw1Args da{};
   da.agg_inner = t.d_agg_inner;
@@ -529,4 +606,14 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
   A3G_LAUNCH_CHECK("k_sgd");
 }
 
+}  // namespace a3g
+
+namespace a3g {
+size_t dh1_sort_temp_bytes(uint64_t n_entries) {
+  size_t bytes = 0;
+  A3G_CUDA(cub::DeviceRadixSort::SortPairs(static_cast<void*>(nullptr), bytes, static_cast<const uint32_t*>(nullptr),
+                                           static_cast<uint32_t*>(nullptr), static_cast<const uint32_t*>(nullptr),
+                                           static_cast<uint32_t*>(nullptr), static_cast<int>(n_entries), 0, 32));
+  return bytes;
+}
 }  // namespace a3g

@@ -22,9 +22,17 @@ struct TrainerState {
   float* d_logits = nullptr;     // max_seeds x C
   float* d_dlogits = nullptr;    // max_seeds x C
   float* d_loss_s = nullptr;     // max_seeds
+  float* d_dagg = nullptr;       // max_seeds x H: per-edge dh1 contribution of each seed
+  uint32_t* d_keys[2] = {nullptr, nullptr};  // scatter entries (dh1 row), unsorted / sorted
+  uint32_t* d_vals[2] = {nullptr, nullptr};  // scatter entries (seed), unsorted / sorted
+  uint64_t n_entries = 0;        // max_seeds * (f0 + 1)
+  void* d_sort_tmp = nullptr;
+  size_t sort_tmp_bytes = 0;
   float* d_part = nullptr;       // nparts x F x H
   uint32_t nparts = 0;
   double* d_losses = nullptr;    // per-step losses of train_steps
+  unsigned long long* d_stats = nullptr;  // per-step A3G_STEP_STATS rows of train_steps
+  uint64_t stats_cap = 0, last_steps = 0;
   uint64_t losses_cap = 0;
   unsigned long long* d_agg_bytes = nullptr;  // algorithmic bytes moved by k_agg1 (accumulated)
   uint32_t* d_seed_buf = nullptr;  // device copy of all batches' seeds (train_steps)
@@ -47,8 +55,13 @@ struct TrainerState {
 
 // Compute part of one step on s_comp for the batch in arena `smp`
 // (gather+aggregate -> forward -> backward -> [allreduce] -> sgd).
+// d_stats: this step's A3G_STEP_STATS row (zeroed by the caller) or null.
 void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* d_loss_slot,
-                          cudaStream_t st, bool record_timing);
+                          unsigned long long* d_stats, cudaStream_t st, bool record_timing);
+// CUB temp storage of the dh1 scatter sort for n_entries entries.
+size_t dh1_sort_temp_bytes(uint64_t n_entries);
+// evaluate_full_graph (trainer.cpp:241-303) with the current device weights.
+double evaluate_full_graph(TrainerState& t, const uint8_t* test_mask);
 
 }  // namespace a3g
 

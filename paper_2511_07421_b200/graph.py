@@ -12,7 +12,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from ._lib import check, lib, ptr, u32p, u64p, f32p, vp
+from ._lib import check, f32p, i32p, lib, ptr, u32p, u64p, vp
 
 FEAT_F32, FEAT_BF16 = 0, 1
 
@@ -29,9 +29,9 @@ class GraphStats:
 class DeviceGraph:
     """Owns an ``a3g_graph*`` (device CSR + feature store)."""
 
-    def __init__(self, g: "Graph", device: int, feat_dtype: int):
+    def __init__(self, g: "Graph", device: int, feat_dtype: int, upload_features: bool = True):
         h = vp()
-        feats = g.features if g.features is not None and g.features.size else None
+        feats = g.features if upload_features and g.features is not None and g.features.size else None
         check(lib().a3g_graph_create(device, g.num_nodes, g.num_edges, g.feat_dim, ptr(g.row_offsets, u64p),
                                      ptr(g.col_indices, u32p), None if feats is None else ptr(feats, f32p),
                                      feat_dtype, ptr(g.labels, u32p), C.byref(h)))
@@ -44,6 +44,55 @@ class DeviceGraph:
         try:
             if self.h:
                 lib().a3g_graph_destroy(self.h)
+        except Exception:
+            pass
+
+
+STORE_HBM, STORE_CACHE, STORE_SHARDED = 0, 1, 2
+
+
+class Store:
+    """Tiered feature store (a3g_store_*) attached to a
+    DeviceGraph: the B200 placement of the reference's static cache
+    (cache.cpp:12-46). Policies: STORE_HBM (all rows in HBM), STORE_CACHE
+    (cached rows in HBM, misses in mapped pinned host memory), STORE_SHARDED
+    (rank r holds device_map == r, peers over NVLink, misses on the host)."""
+
+    def __init__(self, dg: DeviceGraph, features: np.ndarray, device_map=None, policy: int = STORE_HBM,
+                 rank: int = 0, nranks: int = 1):
+        f = np.ascontiguousarray(features, dtype=np.float32)
+        dm = None if device_map is None else np.ascontiguousarray(device_map, dtype=np.int32)
+        h = vp()
+        check(lib().a3g_store_create(dg.h, ptr(f, f32p), None if dm is None else ptr(dm, i32p), policy, rank,
+                                     nranks, C.byref(h)))
+        self.h, self.dg, self.policy, self.rank, self.nranks = h, dg, policy, rank, nranks
+
+    def info(self):
+        a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        check(lib().a3g_store_info(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return dict(local_rows=a.value, host_rows=b.value, remote_rows=c.value)
+
+    def local_ptr(self) -> int:
+        p = vp()
+        check(lib().a3g_store_local_ptr(self.h, C.byref(p)))
+        return p.value or 0
+
+    def set_peer(self, rank: int, dev_ptr: int) -> None:
+        check(lib().a3g_store_set_peer(self.h, rank, vp(dev_ptr)))
+
+    def ipc_handle(self) -> bytes:
+        buf = (C.c_uint8 * 64)()
+        check(lib().a3g_store_ipc_handle(self.h, buf))
+        return bytes(buf)
+
+    def open_peer(self, rank: int, handle: bytes) -> None:
+        buf = (C.c_uint8 * 64).from_buffer_copy(handle)
+        check(lib().a3g_store_open_peer(self.h, rank, buf))
+
+    def __del__(self):
+        try:
+            if self.h and self.dg.h:
+                lib().a3g_store_destroy(self.h)
         except Exception:
             pass
 

@@ -12,10 +12,13 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from ._lib import ParameterError, check, f64p, lib, ptr, u32p, u64p, vp
+from ._lib import ConfigError, ParameterError, check, f64p, i32p, lib, ptr, u8p, u32p, u64p, vp
 from .cache import CacheState
-from .graph import Graph
+from .graph import STORE_HBM, DeviceGraph, Graph, Store
 from .sampling import SamplerKind
+
+
+STAT_UNIQUE, STAT_EDGES, STAT_INNER, STAT_SEEDS, STAT_HITS, STAT_MISSES, STEP_STATS = 0, 1, 2, 3, 4, 5, 8
 
 
 @dataclass
@@ -38,6 +41,24 @@ def init_model(spec: ModelSpec, seed: int):
     check(lib().a3g_init_model(spec.feat_dim, spec.hidden_dim, spec.num_classes, seed, ptr(w1, f64p),
                                ptr(w2, f64p)))
     return w1, w2
+
+
+_M64 = (1 << 64) - 1
+
+
+def mix64(z: int) -> int:
+    """rng.hpp:15-22 (host integer arithmetic, for seeds and plans)."""
+    z &= _M64
+    z ^= z >> 30
+    z = (z * 0xbf58476d1ce4e5b9) & _M64
+    z ^= z >> 27
+    z = (z * 0x94d049bb133111eb) & _M64
+    return z ^ (z >> 31)
+
+
+def hash2(a: int, b: int) -> int:
+    """rng.hpp:24-27."""
+    return mix64((a & _M64) ^ mix64((b + 0x9e3779b97f4a7c15) & _M64))
 
 
 def sampling_seed(base: int, epoch: int, step: int, worker: int = 0) -> int:
@@ -82,7 +103,10 @@ class Trainer:
     """Device-resident 2-layer mean-GCN trainer (trainer.hpp:24-60, 63-83)."""
 
     def __init__(self, g: Graph, cache: CacheState, spec: ModelSpec, fanouts, max_seeds: int,
-                 model_seed: int = 1, device: int = 0, feat_dtype: int = 0):
+                 model_seed: int = 1, device: int = 0, feat_dtype: int = 0, placement=None):
+        """placement: None (whole feature table in HBM) or dict(policy=STORE_*,
+        rank=0, nranks=1) -- feature rows placed by the tiered store from the
+        cache's device_map (graph.Store)."""
         if spec.feat_dim != g.feat_dim:
             raise ParameterError("trainer: spec.feat_dim != graph feat_dim")
         self.g, self.cache, self.spec = g, cache, spec
@@ -90,14 +114,29 @@ class Trainer:
         if any(x < 1 for x in self.fanouts):
             raise ParameterError("sample_khop: fanout must be >= 1")
         f = np.asarray(self.fanouts, dtype=np.uint32)
-        dg = g.device(device, feat_dtype)
+        self.store = None
+        if placement is None:
+            dg = g.device(device, feat_dtype)
+            ch = cache.device(g, device, feat_dtype)
+            keep = [dg]
+        else:
+            dg = DeviceGraph(g, device, feat_dtype, upload_features=False)
+            self.store = Store(dg, g.features, cache.device_map, placement.get("policy", STORE_HBM),
+                               placement.get("rank", 0), placement.get("nranks", 1))
+            from .cache import _DeviceCache
+            hc = vp()
+            dm = np.ascontiguousarray(cache.device_map, dtype=np.int32)
+            check(lib().a3g_cache_from_map(dg.h, ptr(dm, i32p), cache.num_devices, C.byref(hc)))
+            dc = _DeviceCache(hc)
+            ch = dc.h
+            keep = [dc, self.store, dg]
         h = vp()
-        check(lib().a3g_trainer_create(dg.h, cache.device(g, device, feat_dtype), max_seeds, ptr(f, u32p), len(f),
+        check(lib().a3g_trainer_create(dg.h, ch, max_seeds, ptr(f, u32p), len(f),
                                        spec.hidden_dim, spec.num_classes, spec.learning_rate, model_seed,
                                        C.byref(h)))
         self.h = h
         self.max_seeds = max_seeds
-        self._keep = [dg]
+        self._keep = keep
 
     def __del__(self):
         try:
@@ -105,6 +144,7 @@ class Trainer:
                 lib().a3g_trainer_destroy(self.h)
         except Exception:
             pass
+        self._keep = None
 
     # -- weights ---------------------------------------------------------------
     def get_weights(self):
@@ -144,6 +184,30 @@ class Trainer:
         check(lib().a3g_train_steps(self.h, ptr(sb, u32p), B, K, ptr(rs, u64p), float(bias_rate), int(kind), 0,
                                     ptr(losses, f64p)))
         return losses
+
+    def steps_v(self, seeds, offsets, rng_seeds, bias_rate=1.0, kind=SamplerKind.weighted_reservoir):
+        """Pipelined steps with per-step batch sizes: batch i = seeds[offsets[i]:offsets[i+1]]."""
+        s = np.ascontiguousarray(seeds, dtype=np.uint32)
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        K = len(off) - 1
+        rs = np.ascontiguousarray(rng_seeds, dtype=np.uint64)
+        losses = np.empty(max(K, 0), dtype=np.float64)
+        check(lib().a3g_train_steps_v(self.h, ptr(s, u32p), ptr(off, u64p), K, ptr(rs, u64p), float(bias_rate),
+                                      int(kind), 0, ptr(losses, f64p)))
+        return losses
+
+    def step_stats(self, K: int) -> np.ndarray:
+        """u64[K, 8] rows (STAT_UNIQUE, EDGES, INNER, SEEDS, HITS, MISSES) of the last steps call."""
+        out = np.zeros((K, STEP_STATS), dtype=np.uint64)
+        check(lib().a3g_trainer_step_stats(self.h, ptr(out, u64p), K))
+        return out
+
+    def evaluate_full_graph(self) -> float:
+        """trainer.cpp:241-303 on the device with the current weights."""
+        m = np.ascontiguousarray(self.g.test_mask, dtype=np.uint8)
+        acc = C.c_double()
+        check(lib().a3g_evaluate_full_graph(self.h, ptr(m, u8p), C.byref(acc)))
+        return acc.value
 
     def last_grads(self):
         gw1 = np.empty(self.spec.feat_dim * self.spec.hidden_dim)
@@ -191,3 +255,67 @@ class Comm:
                 lib().a3g_comm_destroy(self.h)
         except Exception:
             pass
+
+
+@dataclass
+class TrainOptions:
+    """trainer.hpp:85-92 (u = 1: the B200 path is the single-worker algorithm;
+    data parallelism is across GPUs)."""
+    batch_size: int = 64
+    epochs: int = 10
+    u: int = 1
+    model_seed: int = 1
+    reference_accuracy: float = None
+
+
+@dataclass
+class TrainReport:
+    """trainer.hpp:94-103."""
+    test_accuracy: float = 0.0
+    epochs_run: int = 0
+    loss_curve: list = None
+    accuracy_drop: float = float("nan")
+    epoch_hit_rates: list = None
+    max_batch_bytes: int = 0
+    max_activation_bytes: int = 0
+    param_bytes: int = 0
+
+
+def train(g: Graph, spec: ModelSpec, sampler_cfg, cache: CacheState, opts: TrainOptions, device: int = 0,
+          placement=None, feat_dtype: int = 0) -> TrainReport:
+    """train::train (trainer.cpp:350-424) with every step on the device: per
+    epoch the reference's batch plan (plan seed hash2(rng_seed, 0)) and step
+    seeds sampling_seed(rng_seed, epoch, step, 0) run through the CUDA-stream
+    pipeline; loss curve, epoch hit rates, max batch/activation bytes and the
+    final full-graph accuracy as the reference reports them."""
+    if opts.batch_size < 1:
+        raise ParameterError("train: batch_size must be >= 1")
+    if opts.u != 1:
+        raise ConfigError("train: partitioned workers (u > 1) are not part of the B200 path; "
+                          "use data parallelism across GPUs")
+    tn = g.train_nodes
+    if len(tn) == 0:
+        raise ConfigError("train: a worker has no train nodes")
+    spec = ModelSpec(spec.feat_dim, spec.hidden_dim, spec.num_classes, spec.num_layers, spec.learning_rate)
+    tr = Trainer(g, cache, spec, sampler_cfg.fanouts, max_seeds=min(opts.batch_size, len(tn)),
+                 model_seed=opts.model_seed, device=device, feat_dtype=feat_dtype, placement=placement)
+    rep = TrainReport(loss_curve=[], epoch_hit_rates=[], param_bytes=spec.param_bytes(), epochs_run=opts.epochs)
+    F, H, Cc = spec.feat_dim, spec.hidden_dim, spec.num_classes
+    for epoch in range(opts.epochs):
+        order = plan_epoch_order(tn, epoch, hash2(sampler_cfg.rng_seed, 0))  # trainer.cpp:378-379
+        steps = (len(order) + opts.batch_size - 1) // opts.batch_size
+        off = np.minimum(np.arange(steps + 1, dtype=np.uint64) * opts.batch_size, len(order)).astype(np.uint64)
+        rs = [sampling_seed(sampler_cfg.rng_seed, epoch, s, 0) for s in range(steps)]
+        losses = tr.steps_v(order, off, rs, sampler_cfg.bias_rate, sampler_cfg.kind)
+        st = tr.step_stats(steps).astype(np.int64)
+        rep.loss_curve.append(float(losses.mean()) if steps else 0.0)
+        h, m = int(st[:, STAT_HITS].sum()), int(st[:, STAT_MISSES].sum())
+        rep.epoch_hit_rates.append(h / (h + m) if h + m else 0.0)
+        bb = st[:, STAT_UNIQUE] * F * 4 + st[:, STAT_EDGES] * 8   # cache.cpp:84
+        ab = (st[:, STAT_INNER] * (F + H) + st[:, STAT_SEEDS] * (H + Cc)) * 4  # trainer.cpp:134-135
+        rep.max_batch_bytes = max(rep.max_batch_bytes, int(bb.max()))
+        rep.max_activation_bytes = max(rep.max_activation_bytes, int(ab.max()))
+    rep.test_accuracy = tr.evaluate_full_graph()
+    if opts.reference_accuracy is not None:
+        rep.accuracy_drop = opts.reference_accuracy - rep.test_accuracy
+    return rep

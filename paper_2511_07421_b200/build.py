@@ -78,3 +78,56 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+
+
+# ---------------------------------------------------------------- drop-in ----
+# The C++ drop-in (dropin/*.cpp) implements the reference's own declarations
+# (proj/include/a3gnn) over the C-ABI, so it compiles against the reference's
+# headers; built where /root/reference exists (this container), the outputs
+# travel to the GPU box with the repo snapshot.
+REF_INCLUDE = "/root/reference/proj/include"
+DROPIN = os.path.join(PKG, "dropin")
+DROPIN_OUT = os.path.join(DROPIN, "_build")
+DROPIN_LIBS = {
+    # sampler + cache hot functions only: the reference's train()/executor run on them
+    "liba3gnn_b200_sampling.so": ["registry.cpp", "sampler_b200.cpp", "cache_b200.cpp"],
+    # + train() / evaluate_full_graph on the device
+    "liba3gnn_b200.so": ["registry.cpp", "sampler_b200.cpp", "cache_b200.cpp", "trainer_b200.cpp"],
+}
+
+
+def build_dropin(ref_lib_dir: str | None = None, force: bool = False) -> list:
+    """g++ the drop-in libraries (and, given the compiled reference's
+    directory, the dropin_check test driver). Returns the outputs built."""
+    if not os.path.isdir(REF_INCLUDE):
+        return []
+    os.makedirs(DROPIN_OUT, exist_ok=True)
+    cxx = shutil.which("g++") or "g++"
+    common = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-I", REF_INCLUDE, "-I", os.path.join(ROOT, "include"),
+              "-I", DROPIN]
+    srcs_all = glob.glob(os.path.join(DROPIN, "*.cpp")) + glob.glob(os.path.join(DROPIN, "*.hpp"))
+    newest = max([os.path.getmtime(p) for p in srcs_all] + [os.path.getmtime(LIB)])
+    built = []
+    for name, srcs in DROPIN_LIBS.items():
+        out = os.path.join(DROPIN_OUT, name)
+        if not force and os.path.exists(out) and os.path.getmtime(out) >= newest:
+            continue
+        cmd = [cxx] + common + ["-shared", "-o", out] + [os.path.join(DROPIN, s) for s in srcs] + [
+            "-L", PKG, "-la3g_b200", "-Wl,-rpath,$ORIGIN/../.."]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"drop-in build failed: {name}")
+        built.append(out)
+    if ref_lib_dir and os.path.exists(os.path.join(ref_lib_dir, "libref_a3gnn.so")):
+        out = os.path.join(DROPIN_OUT, "dropin_check")
+        if force or not os.path.exists(out) or os.path.getmtime(out) < newest:
+            rel = os.path.relpath(ref_lib_dir, DROPIN_OUT)
+            cmd = [cxx, "-std=c++20", "-O2", "-I", REF_INCLUDE, "-o", out, os.path.join(DROPIN, "dropin_check.cpp"),
+                   "-L", ref_lib_dir, "-lref_a3gnn", f"-Wl,-rpath,$ORIGIN/{rel}", "-lpthread"]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError("dropin_check build failed")
+            built.append(out)
+    return built

@@ -63,6 +63,7 @@ void sampler_alloc(SamplerState& s, a3g_graph* g, a3g_cache* c, uint32_t max_see
   s.L = L;
   s.fanouts.assign(fanouts, fanouts + L);
   s.sm_count = sm_count_of(g->device);
+  s.device = g->device;
   const uint64_t n = g->n;
   uint64_t rows = std::min<uint64_t>(max_seeds, n);
   uint64_t ucap = rows;
@@ -418,7 +419,7 @@ a3g_status a3g_sampler_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds, co
 
 void a3g_sampler_destroy(a3g_sampler* s) {
   if (!s) return;
-  cudaSetDevice(s->st.g->device);
+  cudaSetDevice(s->st.device);
   sampler_free(s->st);
   delete s;
 }

@@ -69,6 +69,7 @@ struct SamplerState {
   uint32_t last_n_seeds = 0;
   bool has_batch = false;
   int sm_count = 148;
+  int device = 0;  // the graph's device (kept so destroy never dereferences the graph)
 };
 
 // Launch the whole k-hop sample for seeds already in s.d_seeds (n_seeds on host).

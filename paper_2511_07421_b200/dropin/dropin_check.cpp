@@ -1,0 +1,114 @@
+// dropin_check.cpp -- TEST DRIVER of the C++ drop-in. Written against the
+// reference's public API only; run three ways (tests/test_dropin.py):
+//   plain                          the reference alone (CPU)
+//   LD_PRELOAD=liba3gnn_b200_sampling.so   sample_khop / retrieve_features /
+//                                  build_static_cache interposed with the
+//                                  device path inside the reference's own
+//                                  train() and execute_pipeline()
+//   LD_PRELOAD=liba3gnn_b200.so    additionally train() / evaluate_full_graph
+// and prints one line per result so the runs can be compared.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "a3gnn/cache.hpp"
+#include "a3gnn/generators.hpp"
+#include "a3gnn/pipeline.hpp"
+#include "a3gnn/sampler.hpp"
+#include "a3gnn/trainer.hpp"
+
+using namespace a3gnn;
+
+static std::uint64_t fnv(const void* p, std::size_t n, std::uint64_t h = 1469598103934665603ull) {
+  const auto* b = static_cast<const unsigned char*>(p);
+  for (std::size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  return h;
+}
+
+int main(int argc, char** argv) {
+  const std::uint64_t n = argc > 1 ? std::stoull(argv[1]) : 20000;
+  const graph::Graph g = graph::generate_power_law(n, 3, 2.5, 32, 1);
+  cache::CacheConfig cc;
+  cc.volume_bytes = (n / 5) * g.feat_dim * 4;
+  const cache::CacheState cache = cache::build_static_cache(g, cc);
+  std::printf("cache total=%llu hash=%016llx\n", (unsigned long long)cache.total_cached(),
+              (unsigned long long)fnv(cache.device_map.data(), cache.device_map.size() * 4));
+  // sampled batches + gathered rows
+  cache::CacheAccounting acc(1);
+  const auto batches = train::plan_epoch_batches(train::make_worker_contexts(g, nullptr, cache)[0].train_nodes, 0,
+                                                 256, 7);
+  for (int i = 0; i < 4; ++i) {
+    sampling::SamplerConfig cfg;
+    cfg.fanouts = {10, 5, 3};
+    cfg.bias_rate = i % 2 ? 8.0 : 1.0;
+    cfg.kind = i == 3 ? sampling::SamplerKind::uniform_baseline : sampling::SamplerKind::weighted_reservoir;
+    cfg.rng_seed = train::sampling_seed(1, 0, i, 0);
+    const auto b = sampling::sample_khop(g, batches[i], cfg, cache);
+    std::uint64_t h = fnv(b.unique_nodes.data(), b.unique_nodes.size() * 4);
+    for (const auto& l : b.layers) h = fnv(l.edges.data(), l.edges.size() * 8, h);
+    const auto [feats, st] = cache::retrieve_features(b, cache, g, acc);
+    std::printf("batch %d unique=%zu edges=%llu dups=%llu hash=%016llx feats=%016llx bytes=%llu\n", i,
+                b.unique_nodes.size(), (unsigned long long)b.total_edges(),
+                (unsigned long long)b.num_duplicates_removed, (unsigned long long)h,
+                (unsigned long long)fnv(feats.data(), feats.size() * 4), (unsigned long long)st.batch_bytes);
+  }
+  std::printf("hit_rate %.17g\n", cache::hit_rate(acc));
+  // reservoir on one list, with the caller's stream advanced like the reference
+  {
+    std::vector<NodeId> nb(300);
+    std::vector<double> w(300);
+    for (int i = 0; i < 300; ++i) {
+      nb[i] = i * 3;
+      w[i] = i % 3 ? 1.0 : 4.0;
+    }
+    RngStream r(5, 9);
+    const auto a = sampling::weighted_reservoir_sample(nb, w, 12, r);
+    const auto b = sampling::uniform_reservoir_sample(nb, 12, r);
+    std::printf("reservoirs %016llx %016llx draws=%llu next=%016llx\n",
+                (unsigned long long)fnv(a.data(), a.size() * 4), (unsigned long long)fnv(b.data(), b.size() * 4),
+                (unsigned long long)r.draws(), (unsigned long long)r.next_u64());
+  }
+  // error mapping (ParameterError, in the reference's order)
+  try {
+    sampling::SamplerConfig cfg;
+    cfg.fanouts = {5};
+    cfg.bias_rate = 0.5;
+    sampling::sample_khop(g, {1, 2}, cfg, cache);
+    std::printf("error none\n");
+  } catch (const ParameterError& e) {
+    std::printf("error ParameterError %s\n", e.what());
+  }
+  // train(): the reference's loop, or the device loop when interposed
+  train::ModelSpec spec;
+  spec.feat_dim = g.feat_dim;
+  spec.hidden_dim = 16;
+  spec.num_classes = 4;
+  sampling::SamplerConfig scfg;
+  scfg.fanouts = {10, 5};
+  scfg.bias_rate = 8.0;
+  scfg.rng_seed = 3;
+  train::TrainOptions opts;
+  opts.batch_size = 512;
+  opts.epochs = 2;
+  const auto rep = train::train(g, spec, scfg, cache, opts);
+  for (std::size_t e = 0; e < rep.loss_curve.size(); ++e)
+    std::printf("train epoch %zu loss %.17g hit %.17g\n", e, rep.loss_curve[e], rep.epoch_hit_rates[e]);
+  std::printf("train accuracy %.17g batch_bytes %llu act_bytes %llu\n", rep.test_accuracy,
+              (unsigned long long)rep.max_batch_bytes, (unsigned long long)rep.max_activation_bytes);
+  // execute_pipeline pmode1 with 4 producer threads: concurrent sample_khop
+  ResolvedDesign d;
+  d.batch_size = 512;
+  d.bias_rate = 8.0;
+  d.workers = 4;
+  d.cache_volume = cc.volume_bytes;
+  d.mode = Mode::pmode1;
+  pipeline::PlatformSpec plat;
+  pipeline::ExecOptions eo;
+  eo.epochs = 1;
+  sampling::SamplerConfig pcfg;
+  pcfg.fanouts = {10, 5};
+  pcfg.rng_seed = 3;
+  const auto ex = pipeline::execute_pipeline(g, d, plat, spec, pcfg, eo);
+  std::printf("pipeline accuracy %.17g hit %.17g\n", ex.metrics.accuracy, ex.hit_rate);
+  return 0;
+}

@@ -1,0 +1,84 @@
+"""The C++ drop-in (paper_2511_07421_b200/dropin): the reference's own
+declarations implemented over the C-ABI, interposed into the UNMODIFIED
+reference (oracle/_ref) with LD_PRELOAD.
+
+* sampling drop-in (sample_khop / retrieve_features / build_static_cache /
+  reservoirs): every line of dropin_check -- including the reference's own
+  train() and execute_pipeline() running on device-sampled batches with 4
+  concurrent producer threads -- is bit-identical to the reference alone;
+* full drop-in (+ train / evaluate_full_graph on the device): batches and
+  hit rates identical, losses within 1e-3 relative (fp32 device vs fp64),
+  accuracies within 3 test nodes.
+"""
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2511_07421_b200 import build as B
+
+CHECK = os.path.join(B.DROPIN_OUT, "dropin_check")
+LIB_SAMPLING = os.path.join(B.DROPIN_OUT, "liba3gnn_b200_sampling.so")
+LIB_FULL = os.path.join(B.DROPIN_OUT, "liba3gnn_b200.so")
+N = 20000
+NTEST = int(0.4 * N)
+
+needs_build = pytest.mark.skipif(not (os.path.exists(CHECK) and os.path.exists(LIB_FULL)),
+                                 reason="drop-in not built (needs the reference headers at build time)")
+
+
+def run(preload=None):
+    env = dict(os.environ)
+    if preload:
+        env["LD_PRELOAD"] = preload
+    r = subprocess.run([CHECK, str(N)], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return r.stdout.strip().splitlines()
+
+
+@needs_build
+def test_dropin_exports_reference_symbols():
+    out = subprocess.run(["nm", "-DC", "--defined-only", LIB_FULL], capture_output=True, text=True).stdout
+    for sym in ("a3gnn::sampling::sample_khop(", "a3gnn::sampling::weighted_reservoir_sample(",
+                "a3gnn::sampling::uniform_reservoir_sample(", "a3gnn::cache::retrieve_features(",
+                "a3gnn::cache::build_static_cache(", "a3gnn::train::train(", "a3gnn::train::evaluate_full_graph("):
+        assert sym in out, sym
+    out = subprocess.run(["nm", "-DC", "--defined-only", LIB_SAMPLING], capture_output=True, text=True).stdout
+    assert "a3gnn::train::train(" not in out and "a3gnn::sampling::sample_khop(" in out
+
+
+@needs_build
+def test_reference_alone_runs_on_cpu():
+    lines = run()
+    assert any(l.startswith("train accuracy") for l in lines)
+    assert "error ParameterError assign_weights: gamma must be >= 1" in lines
+
+
+@needs_build
+@pytest.mark.gpu
+def test_sampling_dropin_bit_identical_inside_reference():
+    assert run(LIB_SAMPLING) == run()
+
+
+def _num(line, key):
+    return float(re.search(rf"{key} ([0-9.e+-]+)", line).group(1))
+
+
+@needs_build
+@pytest.mark.gpu
+def test_full_dropin_matches_reference():
+    ref, dev = run(), run(LIB_FULL)
+    assert len(ref) == len(dev)
+    for a, b in zip(ref, dev):
+        if a.startswith("train epoch"):
+            assert _num(a, "hit") == _num(b, "hit")
+            assert abs(_num(a, "loss") - _num(b, "loss")) <= 1e-3 * abs(_num(a, "loss"))
+        elif a.startswith("train accuracy"):
+            assert abs(_num(a, "accuracy") - _num(b, "accuracy")) <= 3.0 / NTEST
+            assert _num(a, "batch_bytes") == _num(b, "batch_bytes") and _num(a, "act_bytes") == _num(b, "act_bytes")
+        elif a.startswith("pipeline"):  # the reference executor, device evaluate_full_graph at its end
+            assert abs(_num(a, "accuracy") - _num(b, "accuracy")) <= 3.0 / NTEST
+            assert _num(a, "hit") == _num(b, "hit")
+        else:
+            assert a == b

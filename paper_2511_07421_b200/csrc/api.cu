@@ -2,6 +2,7 @@
 // reference-order validation, status <-> exception mapping, host<->device
 // staging. Kernels live in sampler.cu / train.cu.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -622,9 +623,8 @@ a3g_status a3g_trainer_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds, co
         sampler_alloc(t.smp[i]->st, g, c, max_seeds, fanouts, L);
       }
       t.cap_inner = std::max<uint64_t>(1, t.smp[0]->st.cap_inner);
-      t.agg_smem = ((static_cast<size_t>(t.F) * H + 7) / 8 * 8 + 8ull * g->pitch) * sizeof(float);
-      if (t.agg_smem > 227 * 1024)
-        raise(A3G_ERR_PARAMETER, "trainer: feat_dim*hidden_dim too large for the fused aggregation");
+      if (tc_h1_smem(t.F, H) > 227 * 1024)
+        raise(A3G_ERR_PARAMETER, "trainer: feat_dim too large for the tcgen05 dense update (F <= 1280)");
       t.d_w1 = dalloc<float>(static_cast<size_t>(t.F) * H);
       t.d_w2 = dalloc<float>(static_cast<size_t>(H) * C);
       t.d_gw = dalloc<float>(static_cast<size_t>(t.F) * H + H * C + 2);
@@ -645,7 +645,8 @@ a3g_status a3g_trainer_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds, co
       t.sort_tmp_bytes = dh1_sort_temp_bytes(t.n_entries);
       t.d_sort_tmp = dalloc<uint8_t>(t.sort_tmp_bytes);
       t.nparts = static_cast<uint32_t>(t.sm_count);
-      t.d_part = dalloc<float>(static_cast<size_t>(t.nparts) * t.F * H);
+      t.tc_splits = std::max<uint32_t>(1, static_cast<uint32_t>(t.sm_count) / ((t.F + 127) / 128));
+      t.d_part = dalloc<float>(static_cast<size_t>(std::max(t.nparts, t.tc_splits)) * t.F * H);
       t.d_agg_bytes = dalloc<unsigned long long>(1);
       A3G_CUDA(cudaMemset(t.d_agg_bytes, 0, 8));
       t.losses_cap = 1;

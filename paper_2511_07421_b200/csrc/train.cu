@@ -1,25 +1,26 @@
-// train.cu -- fused gather + mean aggregation + dense update, forward and
-// backward, for the reference's 2-layer mean-GCN (proj/src/trainer.cpp:59-211)
-// in fp32 on sm_100a.
+// train.cu -- one training step of the reference's 2-layer mean-GCN
+// (proj/src/trainer.cpp:59-211) on sm_100a, after the sampler:
 //
-//   k_agg1        inner rows: gather the layer-1 source rows straight from the
-//                 HBM feature store (128-bit loads), mean (self-fallback when
-//                 empty, trainer.cpp:93-107), store agg_inner, then
-//                 h1 = ReLU(agg_inner . W1) from shared-memory W1
-//                 (trainer.cpp:110-113). THE roofline kernel (HBM-bound).
+//   k_step_stats  batch sizes + cache hit/miss count over unique_nodes.
+//   k_agg1        inner rows: gather the layer-1 source rows through the
+//                 feature store (128-bit loads, several rows in flight), mean
+//                 (self-fallback when empty, trainer.cpp:93-107) -> agg_inner.
+//                 THE roofline kernel (HBM-bound).
+//   k_h1_tc       h1 = ReLU(agg_inner . W1) on tcgen05 (gemm_tc.cu).
 //   k_outer       per seed: agg_outer (trainer.cpp:116-127), logits,
-//                 softmax-CE + dlogits (trainer.cpp:153-171),
-//                 dagg_outer = dlogits . W2^T (:177-179) and its scatter into
-//                 dh1 with 1/deg + fallback (:182-198).
-//   k_dw1_partial dW1 = agg_inner^T . (dh1 * [h1>0]) (:200-204), per-block
-//                 partials over row ranges.
-//   k_reduce      deterministic reduction of the partials, dW2 (:174-175),
+//                 softmax-CE + dlogits (:153-171), dagg_outer = dlogits . W2^T
+//                 (:177-179) pre-scaled by 1/deg, and the scatter entries.
+//   k_dh1_gather  dh1 rows from the stably sorted scatter entries (:182-198),
+//                 deterministic (no float atomics).
+//   k_dw1_tc      dW1 = agg_inner^T . (dh1 * [h1>0]) on tcgen05 (:200-204).
+//   k_reduce      fixed-order reduction of the dW1 partials, dW2 (:174-175),
 //                 mean loss.
 //   k_sgd         w -= lr * g (trainer.cpp:208-211).
 #include <cmath>
 
 #include <cub/device/device_radix_sort.cuh>
 
+#include "ptx.cuh"
 #include "trainer.cuh"
 
 namespace a3g {
@@ -64,117 +65,150 @@ struct AggArgs {
   const uint32_t* S1;
   uint32_t f1;
   const uint32_t* n_inner;
-  const float* w1;
+  const uint32_t* n_distinct;  // distinct layer-1 sources (nfront[2]), or null
   float* agg_inner;
-  float* h1;
   unsigned long long* bytes;
   int has_layer1;
 };
 
+// Gather + mean of the layer-1 source rows of every inner row (trainer.cpp:
+// 93-107). Each warp streams its source rows through a ring of kAggSlots row
+// buffers in shared memory with cp.async (LDGSTS): every lane copies its own
+// 16-byte chunks of a row (chunk q = lane + 32 i) and later sums exactly those
+// chunks, so the pipeline needs no barriers -- per-lane cp.async groups, one
+// per source row, with kAggSlots - 1 rows in flight behind the one being
+// summed, across row boundaries. No registers are held by in-flight loads:
+// 8 warps x 8 rows (~155 KB for 2.4 KB rows) are in flight per SM, and the
+// random-row gather runs at HBM (or NVLink / PCIe, store.cu) bandwidth
+// rather than load latency. Sum in edge order, then x (1/c): the reference's
+// scale(1.0/deg) (trainer.cpp:41-54).
+constexpr int kAggSlots = 8;
+
+__device__ __forceinline__ void ldgsts16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void ldgsts_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void ldgsts_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 template <typename T, int NCH>
-__global__ void __launch_bounds__(kAggThreads) k_agg1(const __grid_constant__ AggArgs a) {
+__global__ void __launch_bounds__(kAggThreads, 1) k_agg1(const __grid_constant__ AggArgs a) {
   using Ch = Chunk<T>;
   constexpr int EPC = Ch::EPC;
-  extern __shared__ float smem[];
-  float* s_w1 = smem;                                   // F x H
-  float* s_buf = smem + (static_cast<size_t>(a.F) * a.H + 7) / 8 * 8;  // kAggWarps x pitch, 32B aligned
+  constexpr uint32_t S = kAggSlots;
+  extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint32_t i = threadIdx.x; i < a.F * a.H; i += kAggThreads) s_w1[i] = a.w1[i];
-  __syncthreads();
-  float* buf = s_buf + static_cast<size_t>(warp) * a.pitch;
+  const uint32_t rb = a.view.row_bytes;
+  const uint32_t ring = ptx::smem_u32(smem) + static_cast<uint32_t>(warp) * S * rb;
+  const uint8_t* ring_p = smem + static_cast<size_t>(warp) * S * rb;
   const uint32_t n_inner = *a.n_inner;
   const uint32_t chunks = a.pitch / EPC;  // 16-byte chunks per row
-  unsigned long long nbytes = 0;
   const uint32_t gw = blockIdx.x * kAggWarps + warp, nw = gridDim.x * kAggWarps;
-  const uint32_t H = a.H, F = a.F;
-  const bool pow2 = H <= 32 && (32 % H) == 0;
-  for (uint32_t r = gw; r < n_inner; r += nw) {
-    const int32_t k = a.has_layer1 ? __ldg(a.inv1 + r) : -1;
-    const uint32_t c = k >= 0 ? __ldg(a.cnt1 + k) : 0u;
-    float acc[NCH][EPC];
+  const uint32_t nrows = gw < n_inner ? (n_inner - gw + nw - 1) / nw : 0;  // this warp's rows gw + j*nw
+  unsigned long long nbytes = 0;
+  // producer: row j, source t; lanes hold the (layer row, count) of rows
+  // 32*batch + lane and the current row's source ids; lane s holds the
+  // (row, count, last) record of ring slot s for the consumer
+  uint32_t pj = 0, pt = 0, pc = 0, batch = ~0u, src_lane = 0;
+  int32_t meta_k = -1, pk = -1;
+  uint32_t meta_c = 0;
+  bool row_ready = false;
+  uint32_t slot_row = 0, slot_c = 0;
+  uint32_t issued = 0, consumed = 0;
+  float acc[NCH][EPC];
 #pragma unroll
-    for (int i = 0; i < NCH; ++i)
+  for (int i = 0; i < NCH; ++i)
 #pragma unroll
-      for (int e = 0; e < EPC; ++e) acc[i][e] = 0.f;
-    float scale = 1.f;
-    if (c == 0) {  // self-fallback: own features (trainer.cpp:102-107)
-      const uint4* row = reinterpret_cast<const uint4*>(row_ptr(a.view, __ldg(a.unique + r)));
+    for (int e = 0; e < EPC; ++e) acc[i][e] = 0.f;
+  for (;;) {
+    // ---- producer: fill the ring
+    while (issued - consumed < S && pj < nrows) {
+      const uint32_t r = gw + pj * nw;
+      if (!row_ready) {
+        if ((pj >> 5) != batch) {
+          batch = pj >> 5;
+          const uint32_t rr = gw + (batch * 32 + lane) * nw;
+          meta_k = -1;
+          meta_c = 0;
+          if (batch * 32 + lane < nrows && a.has_layer1) {
+            meta_k = __ldg(a.inv1 + rr);
+            meta_c = meta_k >= 0 ? __ldg(a.cnt1 + meta_k) : 0u;
+          }
+        }
+        pk = __shfl_sync(kFull, meta_k, pj & 31);
+        pc = __shfl_sync(kFull, meta_c, pj & 31);
+        src_lane = lane < static_cast<int>(pc) ? __ldg(a.S1 + static_cast<uint64_t>(pk) * a.f1 + lane) : 0u;
+        nbytes += pc ? static_cast<unsigned long long>(pc) * 4 + 8 : static_cast<unsigned long long>(a.F) * sizeof(T) + 4;
+        row_ready = true;
+      }
+      uint32_t v = __shfl_sync(kFull, src_lane, pt & 31);
+      if (pc == 0) v = __ldg(a.unique + r);  // self-fallback: own features (trainer.cpp:102-107)
+      else if (pt >= 32) v = __ldg(a.S1 + static_cast<uint64_t>(pk) * a.f1 + pt);  // fanout > 32
+      const uint32_t slot = issued % S;
+      const bool last = pt + 1 >= (pc ? pc : 1u);
+      const uint8_t* src = row_ptr(a.view, v);
+      const uint32_t dst = ring + slot * rb;
 #pragma unroll
       for (int i = 0; i < NCH; ++i) {
         const uint32_t q = lane + 32 * i;
-        if (q < chunks) Ch::add(acc[i], __ldg(row + q));
+        if (q < chunks) ldgsts16(dst + q * 16, src + q * 16);
       }
-      nbytes += static_cast<unsigned long long>(F) * sizeof(T) + 4;
-    } else {
-      const uint32_t* srcs = a.S1 + static_cast<uint64_t>(k) * a.f1;
-      uint32_t t = 0;
-      for (; t + 1 < c; t += 2) {
-        const uint4* r0 = reinterpret_cast<const uint4*>(row_ptr(a.view, __ldg(srcs + t)));
-        const uint4* r1 = reinterpret_cast<const uint4*>(row_ptr(a.view, __ldg(srcs + t + 1)));
-        uint4 x0[NCH], x1[NCH];
-#pragma unroll
-        for (int i = 0; i < NCH; ++i) {
-          const uint32_t q = lane + 32 * i;
-          if (q < chunks) {
-            x0[i] = __ldg(r0 + q);
-            x1[i] = __ldg(r1 + q);
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < NCH; ++i) {
-          const uint32_t q = lane + 32 * i;
-          if (q < chunks) {
-            Ch::add(acc[i], x0[i]);
-            Ch::add(acc[i], x1[i]);
-          }
-        }
+      ldgsts_commit();
+      if (lane == static_cast<int>(slot)) {
+        slot_row = r;
+        slot_c = pc | (last ? 0x80000000u : 0u);
       }
-      if (t < c) {
-        const uint4* r0 = reinterpret_cast<const uint4*>(row_ptr(a.view, __ldg(srcs + t)));
-#pragma unroll
-        for (int i = 0; i < NCH; ++i) {
-          const uint32_t q = lane + 32 * i;
-          if (q < chunks) Ch::add(acc[i], __ldg(r0 + q));
-        }
+      ++issued;
+      if (last) {
+        ++pj;
+        pt = 0;
+        row_ready = false;
+      } else {
+        ++pt;
       }
-      scale = 1.f / static_cast<float>(c);
-      nbytes += static_cast<unsigned long long>(c) * (static_cast<unsigned long long>(F) * sizeof(T) + 4) + 8;
     }
-    // agg_inner row (pitched f32) + smem copy for the GEMM
-    float4* out = reinterpret_cast<float4*>(a.agg_inner + static_cast<uint64_t>(r) * a.pitch);
+    if (consumed == issued) break;
+    // ---- consumer: the oldest source row (this lane's chunks of it)
+    if (issued - consumed == S)
+      ldgsts_wait<S - 1>();
+    else
+      ldgsts_wait<0>();
+    const uint32_t slot = consumed % S;
+    const uint4* row = reinterpret_cast<const uint4*>(ring_p + static_cast<size_t>(slot) * rb);
 #pragma unroll
     for (int i = 0; i < NCH; ++i) {
       const uint32_t q = lane + 32 * i;
-      if (q < chunks) {
+      if (q < chunks) Ch::add(acc[i], row[q]);
+    }
+    const uint32_t srow = __shfl_sync(kFull, slot_row, slot);
+    const uint32_t sc = __shfl_sync(kFull, slot_c, slot);
+    ++consumed;
+    if (sc & 0x80000000u) {
+      const uint32_t c = sc & 0x7fffffffu;
+      const float scale = c ? 1.f / static_cast<float>(c) : 1.f;
+      float4* out = reinterpret_cast<float4*>(a.agg_inner + static_cast<uint64_t>(srow) * a.pitch);
 #pragma unroll
-        for (int e = 0; e < EPC; e += 4) {
-          const float4 v = make_float4(acc[i][e] * scale, acc[i][e + 1] * scale, acc[i][e + 2] * scale,
-                                       acc[i][e + 3] * scale);
-          out[q * (EPC / 4) + e / 4] = v;
-          reinterpret_cast<float4*>(buf)[q * (EPC / 4) + e / 4] = v;
+      for (int i = 0; i < NCH; ++i) {
+        const uint32_t q = lane + 32 * i;
+        if (q < chunks) {
+#pragma unroll
+          for (int e = 0; e < EPC; e += 4)
+            out[q * (EPC / 4) + e / 4] = make_float4(acc[i][e] * scale, acc[i][e + 1] * scale,
+                                                     acc[i][e + 2] * scale, acc[i][e + 3] * scale);
         }
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) acc[i][e] = 0.f;
       }
+      nbytes += static_cast<unsigned long long>(a.F) * 4;  // agg_inner row written
     }
-    __syncwarp();
-    // h1 = ReLU(agg . W1)
-    if (pow2) {
-      const uint32_t G = 32 / H, o = lane % H, g = lane / H;
-      const uint32_t KF = (F + G - 1) / G;
-      const uint32_t f0 = g * KF, f1e = min(F, f0 + KF);
-      float sum = 0.f;
-      for (uint32_t f = f0; f < f1e; ++f) sum = fmaf(buf[f], s_w1[f * H + o], sum);
-      for (uint32_t off = H; off < 32; off <<= 1) sum += __shfl_xor_sync(kFull, sum, off);
-      if (g == 0) a.h1[static_cast<uint64_t>(r) * H + o] = fmaxf(sum, 0.f);
-    } else {
-      for (uint32_t o = lane; o < H; o += 32) {
-        float sum = 0.f;
-        for (uint32_t f = 0; f < F; ++f) sum = fmaf(buf[f], s_w1[f * H + o], sum);
-        a.h1[static_cast<uint64_t>(r) * H + o] = fmaxf(sum, 0.f);
-      }
-    }
-    nbytes += static_cast<unsigned long long>(F) * 4 + static_cast<unsigned long long>(H) * 4;
-    __syncwarp();
   }
+  // algorithmic feature bytes: every DISTINCT layer-1 source row once -- the
+  // layer-2 frontier is exactly the first-seen set of layer-1 sources
+  // (sampler.cpp:128-131); duplicates are re-reads the caches may absorb
+  if (blockIdx.x == 0 && threadIdx.x == 0 && a.n_distinct)
+    nbytes += *a.n_distinct * static_cast<unsigned long long>(a.F) * sizeof(T);
   if (lane == 0 && nbytes) atomicAdd(a.bytes, nbytes);
 }
 
@@ -317,62 +351,6 @@ __global__ void __launch_bounds__(256) k_dh1_gather(const uint32_t* keys, const 
   }
 }
 
-struct Dw1Args {
-  const float* agg_inner;
-  const float* h1;
-  const float* dh1;
-  const uint32_t* n_inner;
-  uint32_t pitch, F, H;
-  float* part;
-};
-
-template <int HT, int NCOL>
-__global__ void __launch_bounds__(256) k_dw1_partial(Dw1Args a) {
-  __shared__ float s_dh[32][HT];
-  const uint32_t n = *a.n_inner;
-  const uint32_t per = (n + gridDim.x - 1) / gridDim.x;
-  const uint32_t r_beg = blockIdx.x * per, r_end = min(n, r_beg + per);
-  float acc[NCOL][HT];
-#pragma unroll
-  for (int c = 0; c < NCOL; ++c)
-#pragma unroll
-    for (int j = 0; j < HT; ++j) acc[c][j] = 0.f;
-  const uint32_t H = a.H;
-  for (uint32_t r0 = r_beg; r0 < r_end; r0 += 32) {
-    for (uint32_t i = threadIdx.x; i < 32 * HT; i += blockDim.x) {
-      const uint32_t rr = r0 + i / HT, j = i % HT;
-      float v = 0.f;
-      if (rr < r_end && j < H) {
-        const uint64_t o = static_cast<uint64_t>(rr) * H + j;
-        v = a.h1[o] > 0.f ? a.dh1[o] : 0.f;  // relu_mask (trainer.cpp:200)
-      }
-      s_dh[i / HT][j] = v;
-    }
-    __syncthreads();
-    const uint32_t nr = min(32u, r_end - r0);
-    for (uint32_t i = 0; i < nr; ++i) {
-      const float* arow = a.agg_inner + static_cast<uint64_t>(r0 + i) * a.pitch;
-#pragma unroll
-      for (int c = 0; c < NCOL; ++c) {
-        const uint32_t f = threadIdx.x + 256 * c;
-        const float x = f < a.F ? arow[f] : 0.f;
-#pragma unroll
-        for (int j = 0; j < HT; ++j) acc[c][j] = fmaf(x, s_dh[i][j], acc[c][j]);
-      }
-    }
-    __syncthreads();
-  }
-  float* out = a.part + static_cast<uint64_t>(blockIdx.x) * a.F * H;
-#pragma unroll
-  for (int c = 0; c < NCOL; ++c) {
-    const uint32_t f = threadIdx.x + 256 * c;
-    if (f < a.F)
-#pragma unroll
-      for (int j = 0; j < HT; ++j)
-        if (j < static_cast<int>(H)) out[static_cast<uint64_t>(f) * H + j] = acc[c][j];
-  }
-}
-
 struct ReduceArgs {
   const float* part;
   uint32_t nparts;
@@ -384,36 +362,43 @@ struct ReduceArgs {
   float* gw;  // [F*H | H*C | n | loss_mean*n]
 };
 
-__global__ void k_reduce(ReduceArgs a) {
+// blocks [0, nb1): dW1 = sum of the row-split partials (fixed order);
+// blocks [nb1, nb1 + H*C): one dW2 entry each, agg_outer^T . dlogits as a
+// fixed-shape block tree (trainer.cpp:174-175); last block: the loss sum.
+__global__ void __launch_bounds__(256) k_reduce(ReduceArgs a, uint32_t nb1) {
+  __shared__ float s_l[256];
   const uint32_t FH = a.F * a.H, HC = a.H * a.C;
   const uint32_t ns = *a.ns;
-  if (blockIdx.x == gridDim.x - 1) {  // mean loss, fixed-order tree
-    __shared__ float s_l[256];
-    float x = 0.f;
-    for (uint32_t s = threadIdx.x; s < ns; s += blockDim.x) x += a.loss_s[s];
-    s_l[threadIdx.x] = x;
-    __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-      if (threadIdx.x < w) s_l[threadIdx.x] += s_l[threadIdx.x + w];
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      a.gw[FH + HC] = static_cast<float>(ns);
-      a.gw[FH + HC + 1] = s_l[0];  // sum of per-seed losses = mean * n
+  if (blockIdx.x < nb1) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < FH; i += nb1 * blockDim.x) {
+      float s = 0.f;
+      for (uint32_t p = 0; p < a.nparts; ++p) s += a.part[static_cast<uint64_t>(p) * FH + i];
+      a.gw[i] = s;
     }
     return;
   }
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < FH + HC;
-       i += (gridDim.x - 1) * blockDim.x) {
-    float s = 0.f;
-    if (i < FH) {
-      for (uint32_t p = 0; p < a.nparts; ++p) s += a.part[static_cast<uint64_t>(p) * FH + i];
+  const uint32_t q = blockIdx.x - nb1;
+  float x = 0.f;
+  if (q < HC) {
+    const uint32_t j = q / a.C, c = q % a.C;
+    for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x)
+      x = fmaf(a.agg_outer[static_cast<uint64_t>(t) * a.H + j], a.dlogits[static_cast<uint64_t>(t) * a.C + c], x);
+  } else {
+    for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) x += a.loss_s[t];
+  }
+  s_l[threadIdx.x] = x;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) s_l[threadIdx.x] += s_l[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (q < HC) {
+      a.gw[FH + q] = s_l[0];
     } else {
-      const uint32_t q = i - FH, j = q / a.C, c = q % a.C;
-      for (uint32_t t = 0; t < ns; ++t)
-        s = fmaf(a.agg_outer[static_cast<uint64_t>(t) * a.H + j], a.dlogits[static_cast<uint64_t>(t) * a.C + c], s);
+      a.gw[FH + HC] = static_cast<float>(ns);
+      a.gw[FH + HC + 1] = s_l[0];  // sum of per-seed losses = mean * n
     }
-    a.gw[i] = s;
   }
 }
 
@@ -442,14 +427,14 @@ __global__ void k_sgd(float* w1, float* w2, float* gw, uint32_t FH, uint32_t HC,
 }
 
 template <typename T>
-void launch_agg(TrainerState& t, const AggArgs& aa, int nch, cudaStream_t st) {
-  const int grid = t.sm_count * 2;
-  const size_t smem = t.agg_smem;
-#define A3G_AGG_CASE(N)                                                                          \
-  case N:                                                                                        \
-    A3G_CUDA(cudaFuncSetAttribute(k_agg1<T, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                                  static_cast<int>(smem)));                                      \
-    k_agg1<T, N><<<grid, kAggThreads, smem, st>>>(aa);                                           \
+void launch_agg(TrainerState& t, AggArgs aa, int nch, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(kAggWarps) * kAggSlots * aa.view.row_bytes;
+  if (smem > 227 * 1024) raise(A3G_ERR_PARAMETER, "feature row too wide for k_agg1's shared-memory ring");
+  const int grid = t.sm_count * (smem * 2 <= 227 * 1024 ? 2 : 1);
+#define A3G_AGG_CASE(N)                                                                                       \
+  case N:                                                                                                     \
+    A3G_CUDA(cudaFuncSetAttribute(k_agg1<T, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))); \
+    k_agg1<T, N><<<grid, kAggThreads, smem, st>>>(aa);                                                        \
     break;
   switch (nch) {
     A3G_AGG_CASE(1)
@@ -465,19 +450,6 @@ void launch_agg(TrainerState& t, const AggArgs& aa, int nch, cudaStream_t st) {
   }
 #undef A3G_AGG_CASE
   A3G_LAUNCH_CHECK("k_agg1");
-}
-
-template <int HT>
-void launch_dw1_h(const Dw1Args& da, int ncol, uint32_t nparts, cudaStream_t st) {
-  switch (ncol) {
-    case 1: k_dw1_partial<HT, 1><<<nparts, 256, 0, st>>>(da); break;
-    case 2: k_dw1_partial<HT, 2><<<nparts, 256, 0, st>>>(da); break;
-    case 3: k_dw1_partial<HT, 3><<<nparts, 256, 0, st>>>(da); break;
-    case 4: k_dw1_partial<HT, 4><<<nparts, 256, 0, st>>>(da); break;
-    case 5: case 6: case 7: case 8: k_dw1_partial<HT, 8><<<nparts, 256, 0, st>>>(da); break;
-    default: raise(A3G_ERR_PARAMETER, "feat_dim too large for k_dw1_partial");
-  }
-  A3G_LAUNCH_CHECK("k_dw1_partial");
 }
 
 }  // namespace
@@ -510,9 +482,8 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
   aa.S1 = s.L >= 2 ? s.layer[1].S : nullptr;
   aa.f1 = s.L >= 2 ? s.layer[1].f : 0;
   aa.n_inner = s.L >= 1 ? &ctr->ucount[1] : &ctr->ucount[0];
-  aa.w1 = t.d_w1;
+  aa.n_distinct = s.L >= 2 ? &ctr->nfront[2] : nullptr;
   aa.agg_inner = t.d_agg_inner;
-  aa.h1 = t.d_h1;
   aa.bytes = t.d_agg_bytes;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (record_timing) {
@@ -532,6 +503,7 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
     t.ev_agg.push_back(e0);
     t.ev_agg.push_back(e1);
   }
+  launch_h1_tc(t, t.d_agg_inner, aa.n_inner, t.d_h1, st);
   // ---- outer aggregation, logits, loss, dlogits, scatter to dh1
   OuterArgs oa{};
   oa.h1 = t.d_h1;
@@ -564,25 +536,13 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
     k_dh1_gather<<<t.sm_count * 2, 256, 0, st>>>(t.d_keys[1], t.d_vals[1], t.n_entries, t.d_dagg, t.H, t.d_dh1);
     A3G_LAUNCH_CHECK("k_dh1_gather");
   }
-  // ---- dW1 partials
-  Dw1Args da{};
-  da.agg_inner = t.d_agg_inner;
-  da.h1 = t.d_h1;
-  da.dh1 = t.d_dh1;
-  da.n_inner = aa.n_inner;
-  da.pitch = g->pitch;
-  da.F = t.F;
-  da.H = t.H;
-  da.part = t.d_part;
-  const int ncol = static_cast<int>((t.F + 255) / 256);
-  if (t.H <= 16)
-    launch_dw1_h<16>(da, ncol, t.nparts, st);
-  else
-    launch_dw1_h<32>(da, ncol, t.nparts, st);
+  // ---- dW1 = agg_inner^T . (dh1 * [h1 > 0]) on tcgen05, partials per row split
+  const uint32_t nparts = t.tc_splits;
+  launch_dw1_tc(t, t.d_agg_inner, aa.n_inner, t.d_h1, t.d_dh1, t.d_part, nparts, st);
   // ---- reduce -> grads, loss
   ReduceArgs ra{};
   ra.part = t.d_part;
-  ra.nparts = t.nparts;
+  ra.nparts = nparts;
   ra.agg_outer = t.d_agg_outer;
   ra.dlogits = t.d_dlogits;
   ra.loss_s = t.d_loss_s;
@@ -592,8 +552,8 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
   ra.C = t.C;
   ra.gw = t.d_gw;
   const uint32_t FH = t.F * t.H, HC = t.H * t.C;
-  const int rgrid = static_cast<int>(std::min<uint32_t>(t.sm_count, (FH + HC + 255) / 256)) + 1;
-  k_reduce<<<rgrid, 256, 0, st>>>(ra);
+  const uint32_t nb1 = std::min<uint32_t>(t.sm_count, (FH + 255) / 256);
+  k_reduce<<<nb1 + HC + 1, 256, 0, st>>>(ra, nb1);
   A3G_LAUNCH_CHECK("k_reduce");
   const bool synced = t.comm != nullptr;
   if (synced) {

@@ -49,8 +49,7 @@ struct TrainerState {
   uint64_t last_agg_launches = 0;
   a3g_comm* comm = nullptr;
   int sm_count = 148;
-  size_t agg_smem = 0;
-  bool fused_gemm = true;
+  uint32_t tc_splits = 1;   // row splits of the dW1 tcgen05 GEMM (partials in d_part)
 };
 
 // Compute part of one step on s_comp for the batch in arena `smp`
@@ -58,6 +57,12 @@ struct TrainerState {
 // d_stats: this step's A3G_STEP_STATS row (zeroed by the caller) or null.
 void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* d_loss_slot,
                           unsigned long long* d_stats, cudaStream_t st, bool record_timing);
+// tcgen05 dense update (gemm_tc.cu)
+size_t tc_h1_smem(uint32_t F, uint32_t H);
+size_t tc_dw1_smem(uint32_t H);
+void launch_h1_tc(const TrainerState& t, const float* agg, const uint32_t* n_inner, float* h1, cudaStream_t st);
+void launch_dw1_tc(const TrainerState& t, const float* agg, const uint32_t* n_inner, const float* h1,
+                   const float* dh1, float* part, uint32_t nsplit, cudaStream_t st);
 // CUB temp storage of the dh1 scatter sort for n_entries entries.
 size_t dh1_sort_temp_bytes(uint64_t n_entries);
 // evaluate_full_graph (trainer.cpp:241-303) with the current device weights.

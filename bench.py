@@ -124,38 +124,6 @@ def make_graph(cfg_name):
     return G.generate_power_law(n, m, 2.5, F, BASE_SEED)
 
 
-def step_batches(g, B, world, steps, offset=0):
-    """Global batches of world*B seeds (epoch plans, trainer.cpp:330-343) and
-    their step seeds sampling_seed(base, epoch, step, 0) (trainer.cpp:345)."""
-    from paper_2511_07421_b200 import train as T
-    gb = B * world
-    tn = g.train_nodes
-    per_epoch = len(tn) // gb
-    out, seeds = [], []
-    cache = {}
-    for i in range(offset, offset + steps):
-        e, s = divmod(i, per_epoch)
-        if e not in cache:  # plan seed hash2(base, worker 0) (trainer.cpp:378-379)
-            cache[e] = T.plan_epoch_order(tn, e, _hash2(BASE_SEED, 0))
-        out.append(cache[e][s * gb:(s + 1) * gb])
-        seeds.append(T.sampling_seed(BASE_SEED, e, s, 0))
-    return np.stack(out), np.array(seeds, dtype=np.uint64)
-
-
-def _mix64(z):
-    M = (1 << 64) - 1
-    z ^= z >> 30
-    z = (z * 0xbf58476d1ce4e5b9) & M
-    z ^= z >> 27
-    z = (z * 0x94d049bb133111eb) & M
-    z ^= z >> 31
-    return z
-
-
-def _hash2(a, b):
-    return _mix64(a ^ _mix64((b + 0x9e3779b97f4a7c15) & ((1 << 64) - 1)))
-
-
 def cpu_reference_run(g, cfg_name, gamma, units, producers, tmpdir="/tmp"):
     """Time the reference's own CPU path (oracle/_ref, the unmodified reference
     compiled in place) on `units` batches of the same workload."""
@@ -227,8 +195,9 @@ def run_ours(args):
         comm = T.Comm(bytes(uid.cpu().numpy().tobytes()), world, rank, local)
         tr.set_comm(comm)
     W, K = args.warmup, args.steps
-    gbatches, gseeds = step_batches(g, B, world, W + 2 * K)
-    mine = np.ascontiguousarray(gbatches[:, rank * B:(rank + 1) * B])
+    from paper_2511_07421_b200 import dp
+    gbatches, gseeds = dp.global_batches(g.train_nodes, B, world, W + 2 * K, BASE_SEED)
+    mine = np.ascontiguousarray(np.stack([dp.shard_of(gb, rank, world) for gb in gbatches]))
     # ---- warmup (untimed)
     tr.steps(mine[:W], gseeds[:W], args.gamma, 0)
 

@@ -17,6 +17,7 @@
 //                 mean loss.
 //   k_sgd         w -= lr * g (trainer.cpp:208-211).
 #include <cmath>
+#include <cstdlib>
 
 #include <cub/device/device_radix_sort.cuh>
 
@@ -72,18 +73,16 @@ struct AggArgs {
 };
 
 // Gather + mean of the layer-1 source rows of every inner row (trainer.cpp:
-// 93-107). Each warp streams its source rows through a ring of kAggSlots row
+// 93-107). Each warp streams its source rows through a ring of S row
 // buffers in shared memory with cp.async (LDGSTS): every lane copies its own
 // 16-byte chunks of a row (chunk q = lane + 32 i) and later sums exactly those
 // chunks, so the pipeline needs no barriers -- per-lane cp.async groups, one
-// per source row, with kAggSlots - 1 rows in flight behind the one being
-// summed, across row boundaries. No registers are held by in-flight loads:
-// 8 warps x 8 rows (~155 KB for 2.4 KB rows) are in flight per SM, and the
+// per source row, with S - 1 rows in flight behind the one being summed,
+// across row boundaries. No registers are held by in-flight loads: 24 warps
+// x 3 rows (~175 KB for 2.4 KB rows) are in flight per SM, and the
 // random-row gather runs at HBM (or NVLink / PCIe, store.cu) bandwidth
 // rather than load latency. Sum in edge order, then x (1/c): the reference's
 // scale(1.0/deg) (trainer.cpp:41-54).
-constexpr int kAggSlots = 8;
-
 __device__ __forceinline__ void ldgsts16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
@@ -93,11 +92,10 @@ __device__ __forceinline__ void ldgsts_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <typename T, int NCH>
-__global__ void __launch_bounds__(kAggThreads, 1) k_agg1(const __grid_constant__ AggArgs a) {
+template <typename T, int NCH, int WARPS, int S>
+__global__ void __launch_bounds__(WARPS * 32, 1) k_agg1(const __grid_constant__ AggArgs a) {
   using Ch = Chunk<T>;
   constexpr int EPC = Ch::EPC;
-  constexpr uint32_t S = kAggSlots;
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t rb = a.view.row_bytes;
@@ -105,7 +103,7 @@ __global__ void __launch_bounds__(kAggThreads, 1) k_agg1(const __grid_constant__
   const uint8_t* ring_p = smem + static_cast<size_t>(warp) * S * rb;
   const uint32_t n_inner = *a.n_inner;
   const uint32_t chunks = a.pitch / EPC;  // 16-byte chunks per row
-  const uint32_t gw = blockIdx.x * kAggWarps + warp, nw = gridDim.x * kAggWarps;
+  const uint32_t gw = blockIdx.x * WARPS + warp, nw = gridDim.x * WARPS;
   const uint32_t nrows = gw < n_inner ? (n_inner - gw + nw - 1) / nw : 0;  // this warp's rows gw + j*nw
   unsigned long long nbytes = 0;
   // producer: row j, source t; lanes hold the (layer row, count) of rows
@@ -426,15 +424,36 @@ __global__ void k_sgd(float* w1, float* w2, float* gw, uint32_t FH, uint32_t HC,
   if (blockIdx.x == 0 && threadIdx.x == 0 && loss_slot) *loss_slot = static_cast<double>(gw[FH + HC + 1]) / n;
 }
 
+template <typename T, int N, int W, int S>
+void launch_agg_cfg(TrainerState& t, const AggArgs& aa, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(W) * S * aa.view.row_bytes;
+  if (smem > 227 * 1024) raise(A3G_ERR_PARAMETER, "feature row too wide for k_agg1's shared-memory ring");
+  const int grid = t.sm_count * (smem * 2 <= 227 * 1024 && W <= 32 ? 2 : 1);
+  A3G_CUDA(cudaFuncSetAttribute(k_agg1<T, N, W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+  k_agg1<T, N, W, S><<<grid, W * 32, smem, st>>>(aa);
+}
+
+// 24 warps per CTA (more warps beat a deeper ring: r01 sweep 8x8 63 us,
+// 16x4 53 us, 24x3 51 us on C2); ring depth from the row size.
+template <typename T, int N>
+void launch_agg_n(TrainerState& t, const AggArgs& aa, cudaStream_t st) {
+  const uint64_t per_slot = 24ull * aa.view.row_bytes;
+  if (per_slot * 8 <= 176 * 1024)
+    launch_agg_cfg<T, N, 24, 8>(t, aa, st);
+  else if (per_slot * 6 <= 176 * 1024)
+    launch_agg_cfg<T, N, 24, 6>(t, aa, st);
+  else if (per_slot * 4 <= 176 * 1024)
+    launch_agg_cfg<T, N, 24, 4>(t, aa, st);
+  else
+    launch_agg_cfg<T, N, 24, 3>(t, aa, st);
+}
+
 template <typename T>
 void launch_agg(TrainerState& t, AggArgs aa, int nch, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(kAggWarps) * kAggSlots * aa.view.row_bytes;
-  if (smem > 227 * 1024) raise(A3G_ERR_PARAMETER, "feature row too wide for k_agg1's shared-memory ring");
-  const int grid = t.sm_count * (smem * 2 <= 227 * 1024 ? 2 : 1);
-#define A3G_AGG_CASE(N)                                                                                       \
-  case N:                                                                                                     \
-    A3G_CUDA(cudaFuncSetAttribute(k_agg1<T, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))); \
-    k_agg1<T, N><<<grid, kAggThreads, smem, st>>>(aa);                                                        \
+#define A3G_AGG_CASE(N)                  \
+  case N:                                \
+    launch_agg_n<T, N>(t, aa, st);       \
     break;
   switch (nch) {
     A3G_AGG_CASE(1)

@@ -183,3 +183,21 @@ def test_train_rejects_partitioned_workers():
     c = CA.CacheState(rec["train_device_map"], 1)
     with pytest.raises(T.ConfigError):
         T.train(g, T.ModelSpec(g.feat_dim, 8, 4), S.SamplerConfig([10, 5], 8.0, 5), c, T.TrainOptions(u=2))
+
+
+def test_nccl_gradient_sync_world1(c1):
+    """The DP exchange on the device (k_scale_for_sync -> ncclAllReduce ->
+    k_sgd dividing by sum n_k) on a 1-rank communicator equals the local step."""
+    g = c1
+    cache = CA.build_static_cache(g, CA.CacheConfig(int(0.2 * g.num_nodes) * g.feat_dim * 4, 1))
+    spec = T.ModelSpec(g.feat_dim, 16, 4)
+    a = T.Trainer(g, cache, spec, [10, 5], max_seeds=512)
+    la, (a1, a2), _ = _steps(a, g, K=3)
+    b = T.Trainer(g, cache, spec, [10, 5], max_seeds=512)
+    comm = T.Comm(T.Comm.unique_id(), 1, 0, 0)
+    b.set_comm(comm)
+    lb, (b1, b2), _ = _steps(b, g, K=3)
+    np.testing.assert_allclose(lb, la, rtol=1e-6)
+    assert rel_err(b1, a1) < 1e-6 and rel_err(b2, a2) < 1e-6
+    b.set_comm(None)
+    del comm

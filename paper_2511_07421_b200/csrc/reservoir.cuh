@@ -61,6 +61,8 @@ __device__ __forceinline__ double gamma_lo(double thr, double gamma) {
 
 struct PolUnit {
   using K = uint64_t;
+  static constexpr bool kNearTies = false;
+  static constexpr uint64_t tie = 0;
   __device__ __forceinline__ K inf() const { return ~0ull; }
   __device__ __forceinline__ K fill_key(uint64_t x, uint32_t, uint64_t) const { return x >> 11; }
   __device__ __forceinline__ bool eval(uint64_t x, uint32_t, uint64_t, K thr, K& k) const {
@@ -77,6 +79,7 @@ struct PolUnit {
 
 struct PolGammaAll {
   using K = uint64_t;
+  static constexpr bool kNearTies = true;
   double inv_g;
   uint64_t tie;
   __device__ __forceinline__ K inf() const { return ~0ull; }
@@ -165,9 +168,11 @@ struct WState {
   int mp; // min_pos
 };
 
+// Emit interface: (node id, key, lane holding it, row position). Hub-segment
+// records store the position; the merge translates the final slots to ids.
 struct NoEmit {
   template <typename K>
-  __device__ __forceinline__ void operator()(uint32_t, K, int) const {}
+  __device__ __forceinline__ void operator()(uint32_t, K, int, uint64_t) const {}
 };
 
 // Fill slots [0, nf) with positions j0 + lane (sampler.cpp:30-33). The draw of
@@ -183,7 +188,7 @@ __device__ __forceinline__ void fill_slots(const uint32_t* nb, uint64_t j0, uint
     const uint32_t v = nb[j];
     s.my_key = pol.fill_key(mix64(key + (c0 + j + 1) * kPhi), v, j);
     s.my_id = v;
-    emit(v, s.my_key, lane);
+    emit(v, s.my_key, lane, j);
   }
   pol.argmin(s.thr, s.mp, s.my_key, lane);
 }
@@ -225,7 +230,7 @@ __device__ __forceinline__ void replay_range(const uint32_t* nb, uint64_t jb, ui
               s.my_key = kv;
               s.my_id = iv;
             }
-            emit(iv, kv, src);
+            emit(iv, kv, src, b + q * 32 + src);
             pol.argmin(s.thr, s.mp, s.my_key, lane);
             changed = true;
             mask &= __ballot_sync(kFull, cand[q] && pol.cheap_gt(kk[q], s.thr));

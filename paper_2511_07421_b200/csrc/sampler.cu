@@ -26,6 +26,8 @@
 // Counts stay on the device: no host sync inside a batch.
 #include <cmath>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "ptx.cuh"
 #include "reservoir.cuh"
 #include "sampler.cuh"
@@ -152,10 +154,10 @@ struct SegEmit {
   uint32_t* cnt;  // warp-uniform counter
   uint32_t cap;
   int lane;
-  __device__ __forceinline__ void operator()(uint32_t id, K key, int src) const {
+  __device__ __forceinline__ void operator()(uint32_t, K key, int src, uint64_t pos) const {
     const uint32_t c = *cnt;
     if (lane == src && c < cap) {
-      rid[c] = id;
+      rid[c] = static_cast<uint32_t>(pos);
       rkey[c] = *reinterpret_cast<const uint64_t*>(&key);
     }
     *cnt = c + 1;
@@ -165,8 +167,8 @@ template <typename K>
 struct FillEmit {  // fills: lane i writes record i
   uint32_t* rid;
   uint64_t* rkey;
-  __device__ __forceinline__ void operator()(uint32_t id, K key, int lane) const {
-    rid[lane] = id;
+  __device__ __forceinline__ void operator()(uint32_t, K key, int lane, uint64_t pos) const {
+    rid[lane] = static_cast<uint32_t>(pos);
     rkey[lane] = *reinterpret_cast<const uint64_t*>(&key);
   }
 };
@@ -450,6 +452,363 @@ __global__ void __launch_bounds__(kStreamWarps * 32) k_stream(SampleArgs a) {
   }
 }
 
+// ------------------------------------------------------------ stream (int) -
+// Items of the integer-key policies (all weights 1 -- PolUnit -- or all gamma
+// -- PolGammaAll -- and Algorithm R): a key depends only on (row key,
+// position), never on the neighbour id, so the hot loop hashes positions
+// without touching the adjacency. Each lane evaluates kIntU keys per group
+// (independent mix64 chains); one vote decides whether any beats the current
+// minimum (x > (thr << 11 | 0x7ff) <=> x >> 11 > thr). Only groups with
+// candidates load the candidates' ids (one coalesced round trip) and run the
+// ordered insertion replay of reservoir.cuh -- the same slot history as the
+// reference (sampler.cpp:24-40).
+constexpr int kIntU = 4;
+
+template <typename P, typename Emit>
+__device__ __forceinline__ void replay_int(const uint32_t* nb, uint64_t jb, uint64_t je, uint64_t key, int lane,
+                                           P& pol, rsv::WState<uint64_t>& s, const Emit& emit) {
+  constexpr uint64_t kStep = 32ull * kPhi;
+  uint64_t thrx = (s.thr << 11) | 0x7ffull;
+  uint64_t ctr = key + (jb + lane + 1) * kPhi;
+  for (uint64_t b = jb; b < je; b += 32 * kIntU, ctr += kIntU * kStep) {
+    uint64_t x[kIntU];
+    bool c[kIntU];
+    bool anyc = false;
+#pragma unroll
+    for (int q = 0; q < kIntU; ++q) {
+      x[q] = mix64(ctr + q * kStep);
+      c[q] = b + q * 32 + lane < je && x[q] > thrx;
+      anyc |= c[q];
+    }
+    if (!__any_sync(kFull, anyc)) continue;
+    uint32_t v[kIntU];
+#pragma unroll
+    for (int q = 0; q < kIntU; ++q) v[q] = c[q] ? __ldg(nb + b + q * 32 + lane) : 0u;
+#pragma unroll
+    for (int q = 0; q < kIntU; ++q) {
+      const uint64_t kk = x[q] >> 11;
+      unsigned mask = __ballot_sync(kFull, c[q] && kk > s.thr);
+      while (mask) {
+        const int src = __ffs(mask) - 1;
+        const uint64_t kv = __shfl_sync(kFull, kk, src);
+        const uint32_t iv = __shfl_sync(kFull, v[q], src);
+        if (pol.gt(kv, s.thr)) {
+          if (lane == s.mp) {
+            s.my_key = kv;
+            s.my_id = iv;
+          }
+          emit(iv, kv, src, b + q * 32 + src);
+          pol.argmin(s.thr, s.mp, s.my_key, lane);
+          mask &= __ballot_sync(kFull, c[q] && kk > s.thr);
+        }
+        mask &= ~((2u << src) - 1u);
+      }
+    }
+    thrx = (s.thr << 11) | 0x7ffull;
+  }
+}
+
+template <int WM>
+__global__ void __launch_bounds__(256) k_stream_int(SampleArgs a) {
+  using P = typename PolOf<WM>::P;
+  static_assert(sizeof(typename P::K) == 8, "integer-key policy");
+  const int lane = threadIdx.x & 31;
+  const uint32_t nitems = min(*a.item_count, a.hub.item_cap);
+  const uint32_t m = a.f;
+  const uint32_t nwarps_total = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t claim = max(1u, min(8u, nitems / (8 * nwarps_total)));
+  for (;;) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(a.item_work, claim);
+    base = __shfl_sync(kFull, base, 0);
+    if (base >= nitems) break;
+    const uint32_t iend = min(nitems, base + claim);
+    for (uint32_t it = base; it < iend; ++it) {
+      const uint4 im = a.hub.items[it];
+      const uint32_t dst = __ldg(a.front + im.x);
+      const uint64_t beg = __ldg(a.ro + dst);
+      const uint32_t* nb = a.col + beg;
+      const uint64_t key = hash2(a.seed, hash2(a.layer, dst));
+      const bool seg = im.w != kInv;
+      if (a.kind == A3G_SAMPLER_UNIFORM) {
+        if (!seg) {
+          uint32_t uid = lane < static_cast<int>(m) ? __ldg(nb + lane) : 0u;
+          rsv::uniform_range(nb, m, im.z, m, key, lane, 0, uid);
+          const uint64_t row0 = static_cast<uint64_t>(im.x) * m;
+          if (lane < static_cast<int>(m)) {
+            a.S[row0 + lane] = uid;
+            mark_first(a.first, uid, a.tag, static_cast<uint32_t>(row0 + lane));
+          }
+          if (lane == 0) a.cnt[im.x] = m;
+        } else {
+          uint32_t ulast = kInv;
+          const uint64_t jb0 = im.y > m ? im.y : static_cast<uint64_t>(m);
+          for (uint64_t b = jb0; b < im.z; b += 32) {
+            const uint64_t j = b + lane;
+            uint32_t r = kInv;
+            if (j < im.z) r = static_cast<uint32_t>(__umul64hi(draw(key, j - m + 1), j + 1));
+            unsigned mask = __ballot_sync(kFull, j < im.z && r < m);
+            while (mask) {
+              const int src = __ffs(mask) - 1;
+              const uint32_t slot = __shfl_sync(kFull, r, src);
+              if (lane == static_cast<int>(slot)) ulast = static_cast<uint32_t>(b + src);
+              mask &= mask - 1;
+            }
+          }
+          a.hub.slot_last[static_cast<uint64_t>(im.w) * 32 + lane] = ulast;
+        }
+        continue;
+      }
+      P pol = PolOf<WM>::make(a);
+      rsv::WState<uint64_t> wst;
+      if (seg) {
+        uint32_t* rid = a.hub.rec_id + static_cast<uint64_t>(im.w) * kRecCap;
+        uint64_t* rkey = a.hub.rec_key + static_cast<uint64_t>(im.w) * kRecCap;
+        const uint32_t nf = min(m, im.z - im.y);
+        rsv::fill_slots(nb, im.y, nf, key, 0, lane, pol, wst, FillEmit<uint64_t>{rid, rkey});
+        uint32_t rcnt = nf;
+        if (im.z - im.y >= m) {
+          SegEmit<uint64_t> em{rid, rkey, &rcnt, kRecCap, lane};
+          replay_int(nb, im.y + nf, im.z, key, lane, pol, wst, em);
+        }
+        if (lane == 0) {
+          a.hub.rec_cnt[im.w] = rcnt;
+          a.hub.tau[im.w] = wst.thr;
+          a.hub.tau_ok[im.w] = (im.z - im.y >= m) ? 1u : 0u;
+        }
+      } else {
+        rsv::fill_slots(nb, 0, m, key, 0, lane, pol, wst, rsv::NoEmit{});
+        replay_int(nb, m, im.z, key, lane, pol, wst, rsv::NoEmit{});
+        const uint64_t row0 = static_cast<uint64_t>(im.x) * m;
+        if (lane < static_cast<int>(m)) {
+          a.S[row0 + lane] = wst.my_id;
+          mark_first(a.first, wst.my_id, a.tag, static_cast<uint32_t>(row0 + lane));
+        }
+        if (lane == 0) a.cnt[im.x] = m;
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------- stream (group) -
+// Integer-key items (PolUnit / PolGammaAll weights, Algorithm R) processed by
+// lane groups of G = next_pow2(m) lanes: a warp carries 32/G items at once,
+// each group owning one item's reservoir (slot = lane in group). A key
+// depends only on (row key, position), so the hot loop hashes positions
+// without reading the adjacency: lane g hashes positions b + u*G + g for
+// u < 32/G (independent mix64 chains), and one vote tells whether any group
+// holds a key above its minimum (x > (thr << 11 | 0x7ff) <=> x >> 11 > thr).
+// Candidates are then replayed in position order in every group at once --
+// per step one insertion per group, with a G-lane butterfly argmin (first
+// minimum, as std::min_element) -- the exact sequential slot history of
+// sampler.cpp:24-40. Items are length-sorted so a warp's groups carry equal
+// work; records of hub segments store row positions (the merge translates).
+// (key, slot) minimum over the G lanes of a group, first index on K-ties:
+// an integer butterfly (64-bit compare, lower slot on equal integers); keys
+// are K-monotone, so only another slot within the policy's tie window of the
+// minimum can share its K value -- then (rare) the exact K-order decides
+// (PolGammaAll; PolUnit keys are exact integers).
+template <int G, typename P>
+__device__ __forceinline__ void grp_argmin(const P& pol, uint64_t my, uint32_t gl, uint64_t& thr, uint32_t& mp) {
+  uint64_t k = my;
+  uint32_t i = gl;
+#pragma unroll
+  for (int off = G / 2; off > 0; off >>= 1) {
+    const uint64_t ok = __shfl_xor_sync(kFull, k, off, G);
+    const uint32_t oi = __shfl_xor_sync(kFull, i, off, G);
+    if (ok < k || (ok == k && oi < i)) {
+      k = ok;
+      i = oi;
+    }
+  }
+  if (P::kNearTies && __any_sync(kFull, my != ~0ull && my != k && my - k <= pol.tie)) {
+    // exact pass: first slot whose K equals the minimum's K
+    uint64_t kk = my;
+    uint32_t ii = gl;
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) {
+      const uint64_t ok = __shfl_xor_sync(kFull, kk, off, G);
+      const uint32_t oi = __shfl_xor_sync(kFull, ii, off, G);
+      if (pol.gt(kk, ok) || (!pol.gt(ok, kk) && oi < ii)) {
+        kk = ok;
+        ii = oi;
+      }
+    }
+    k = kk;
+    i = ii;
+  }
+  thr = k;
+  mp = i;
+}
+
+template <int WM, int G>
+__global__ void __launch_bounds__(256) k_stream_grp(SampleArgs a, const uint32_t* order) {
+  using P = typename PolOf<WM>::P;
+  constexpr int NG = 32 / G;
+  constexpr uint64_t kStepG = static_cast<uint64_t>(G) * kPhi;
+  const int lane = threadIdx.x & 31;
+  const uint32_t gl = lane % G, grp = lane / G;
+  const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << (grp * G));
+  const uint32_t nitems = min(*a.item_count, a.hub.item_cap);
+  const uint32_t m = a.f;
+  const P pol = PolOf<WM>::make(a);
+  for (;;) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(a.item_work, static_cast<uint32_t>(NG));
+    base = __shfl_sync(kFull, base, 0);
+    if (base >= nitems) break;
+    const uint32_t ii = base + grp;
+    const bool live = ii < nitems;
+    uint4 im = make_uint4(0, 0, 0, kInv);
+    uint32_t dst = 0;
+    uint64_t beg = 0;
+    if (live) {
+      im = a.hub.items[__ldg(order + ii)];
+      dst = __ldg(a.front + im.x);
+      beg = __ldg(a.ro + dst);
+    }
+    const uint32_t* nb = a.col + beg;
+    const uint64_t key = hash2(a.seed, hash2(a.layer, dst));
+    const bool seg = im.w != kInv;
+    const uint64_t row0 = static_cast<uint64_t>(im.x) * m;
+    const uint32_t p0 = im.y, p1 = im.z;
+    if (a.kind == A3G_SAMPLER_UNIFORM) {  // Algorithm R (sampler.cpp:44-58)
+      uint32_t my_pos = seg ? kInv : gl;
+      const uint32_t j0 = p0 > m ? p0 : m;
+      // all groups iterate to the warp's longest item
+      uint32_t len = live && p1 > j0 ? p1 - j0 : 0u;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) len = max(len, __shfl_xor_sync(kFull, len, off));
+      for (uint32_t b = 0; b < len; b += G) {
+        const uint32_t j = j0 + b + gl;
+        uint32_t r = kInv;
+        if (live && j < p1) r = static_cast<uint32_t>(__umul64hi(draw(key, j - m + 1), static_cast<uint64_t>(j) + 1));
+        unsigned mask = __ballot_sync(kFull, r < m) & gmask;
+        while (__any_sync(kFull, mask != 0)) {
+          const int src = mask ? __ffs(mask) - 1 : lane;
+          const uint32_t slot = __shfl_sync(kFull, r, src);
+          if (mask && gl == slot) my_pos = j0 + b + (src % G);
+          if (mask) mask &= mask - 1;
+        }
+      }
+      if (live) {
+        if (seg) {
+          a.hub.slot_last[static_cast<uint64_t>(im.w) * 32 + gl] = gl < m ? my_pos : kInv;
+          if (G < 32)
+            for (uint32_t s2 = G + gl; s2 < 32; s2 += G) a.hub.slot_last[static_cast<uint64_t>(im.w) * 32 + s2] = kInv;
+        } else if (gl < m) {
+          const uint32_t id = __ldg(nb + my_pos);
+          a.S[row0 + gl] = id;
+          mark_first(a.first, id, a.tag, static_cast<uint32_t>(row0 + gl));
+          if (gl == 0) a.cnt[im.x] = m;
+        }
+      }
+      continue;
+    }
+    // ---- weighted reservoir, integer keys: fill
+    const uint32_t nf = live ? min(m, p1 - p0) : 0u;
+    uint64_t my_key = ~0ull;
+    uint32_t my_pos = 0;
+    uint32_t* rid = a.hub.rec_id + static_cast<uint64_t>(seg ? im.w : 0) * kRecCap;
+    uint64_t* rkey = a.hub.rec_key + static_cast<uint64_t>(seg ? im.w : 0) * kRecCap;
+    if (gl < nf) {
+      my_key = draw(key, static_cast<uint64_t>(p0) + gl + 1) >> 11;
+      my_pos = p0 + gl;
+      if (seg) {
+        rid[gl] = my_pos;
+        rkey[gl] = my_key;
+      }
+    }
+    uint64_t thr;
+    uint32_t mp;
+    grp_argmin<G>(pol, my_key, gl, thr, mp);
+    uint32_t rcnt = nf;
+    // ---- replay positions [p0 + nf, p1): lane g hashes b + u*G + g, u < 32/G;
+    // candidates are replayed block by block (u), one insertion per group per
+    // step (r01 measurements: cheaper than one 32-bit group mask over all u)
+    constexpr int U = 32 / G;
+    const uint32_t jb = p0 + nf;
+    uint32_t len = live && p1 > jb ? p1 - jb : 0u;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) len = max(len, __shfl_xor_sync(kFull, len, off));
+    uint64_t thrx = (thr << 11) | 0x7ffull;
+    uint64_t ctr = key + (static_cast<uint64_t>(jb) + gl + 1) * kPhi;
+    for (uint32_t b = 0; b < len; b += 32, ctr += 32 * kPhi) {
+      uint64_t x[U];
+      bool c[U];
+      bool anyc = false;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        x[u] = mix64(ctr + u * kStepG);
+        c[u] = jb + b + u * G + gl < p1 && x[u] > thrx;
+        anyc |= c[u];
+      }
+      if (!__any_sync(kFull, anyc)) continue;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t kk = x[u] >> 11;
+        unsigned mask = __ballot_sync(kFull, c[u] && kk > thr) & gmask;
+        while (__any_sync(kFull, mask != 0)) {
+          const int src = mask ? __ffs(mask) - 1 : lane;
+          const uint64_t kv = __shfl_sync(kFull, kk, src);
+          const bool ins = mask != 0 && pol.gt(kv, thr);
+          const uint32_t pos = jb + b + u * G + (src % G);
+          if (ins && gl == mp) {
+            my_key = kv;
+            my_pos = pos;
+          }
+          if (ins && seg && lane == src) {
+            if (rcnt < kRecCap) {
+              rid[rcnt] = pos;
+              rkey[rcnt] = kv;
+            }
+          }
+          if (ins) ++rcnt;
+          uint64_t nthr;
+          uint32_t nmp;
+          grp_argmin<G>(pol, my_key, gl, nthr, nmp);
+          if (ins) {
+            thr = nthr;
+            mp = nmp;
+          }
+          if (mask) mask &= ~((2u << src) - 1u);
+          mask &= __ballot_sync(kFull, c[u] && kk > thr) & gmask;
+        }
+      }
+      thrx = (thr << 11) | 0x7ffull;
+    }
+    if (!live) continue;
+    if (seg) {
+      if (gl == 0) {
+        a.hub.rec_cnt[im.w] = rcnt;
+        a.hub.tau[im.w] = thr;
+        a.hub.tau_ok[im.w] = (p1 - p0 >= m) ? 1u : 0u;
+      }
+    } else if (gl < m) {
+      const uint32_t id = __ldg(nb + my_pos);
+      a.S[row0 + gl] = id;
+      mark_first(a.first, id, a.tag, static_cast<uint32_t>(row0 + gl));
+      if (gl == 0) a.cnt[im.x] = m;
+    }
+  }
+}
+
+// Sort keys of the layer's items (length, clamped; 0 = no item) for the
+// descending radix sort that feeds k_stream_thr.
+__global__ void k_item_keys(const uint4* items, const uint32_t* item_count, uint32_t cap, uint32_t* keys,
+                            uint32_t* vals) {
+  const uint32_t n = min(*item_count, cap);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) {
+    uint32_t len = 0;
+    if (i < n) {
+      const uint4 it = items[i];
+      len = min(it.z - it.y, 4095u) + 1;
+    }
+    keys[i] = len;
+    vals[i] = i;
+  }
+}
+
 // Warp per hub with few segments (<= kMergeFilterWarps): replay the records in
 // segment order, dropping those that cannot beat max_{s'<s} tau_{s'}.
 template <int WM>
@@ -645,8 +1004,9 @@ __global__ void __launch_bounds__(kMergeThreads) k_hub_merge(SampleArgs a) {
     }
     if (warp == 0) {
       if (lane < static_cast<int>(m)) {
-        a.S[row0 + lane] = st.my_id;
-        mark_first(a.first, st.my_id, a.tag, static_cast<uint32_t>(row0 + lane));
+        const uint32_t id = __ldg(nb + st.my_id);  // records hold row positions
+        a.S[row0 + lane] = id;
+        mark_first(a.first, id, a.tag, static_cast<uint32_t>(row0 + lane));
       }
       if (lane == 0) a.cnt[k] = m;
     }
@@ -736,7 +1096,7 @@ __global__ void __launch_bounds__(256) k_hub_merge_warp(SampleArgs a) {
           lok = true;
         }
       }
-      my_id = st.my_id;
+      my_id = lane < static_cast<int>(m) ? __ldg(nb + st.my_id) : 0u;  // records hold row positions
     }
     if (lane < static_cast<int>(m)) {
       a.S[row0 + lane] = my_id;
@@ -838,20 +1198,40 @@ struct Flags {
   uint32_t v;
 };
 
-__device__ __forceinline__ Flags fin_flags(const FinArgs& a, uint64_t P, uint64_t p) {
-  Flags fl{false, false, false, 0};
-  if (p >= P) return fl;
-  if (a.cnt) {
-    const uint64_t row = p / a.f;
-    const uint32_t slot = static_cast<uint32_t>(p - row * a.f);
-    if (slot >= __ldg(a.cnt + row)) return fl;
+// Flags of the kFinRounds positions base + r*kFinThreads + tid, with the three
+// dependent loads (slot id -> first-position word -> interner word) issued
+// as three batches of independent loads instead of 3 x kFinRounds serial
+// round trips (the tables are L2-resident; the kernel is latency-bound).
+__device__ __forceinline__ void fin_flags_all(const FinArgs& a, uint64_t P, uint64_t base, Flags (&fl)[kFinRounds]) {
+  uint32_t valid = 0;
+#pragma unroll
+  for (int r = 0; r < kFinRounds; ++r) {
+    const uint64_t p = base + r * kFinThreads + threadIdx.x;
+    fl[r] = Flags{false, false, false, 0};
+    bool ok = p < P;
+    if (ok && a.cnt) {
+      const uint64_t row = p / a.f;
+      ok = static_cast<uint32_t>(p - row * a.f) < __ldg(a.cnt + row);
+    }
+    if (ok) {
+      valid |= 1u << r;
+      fl[r].v = __ldg(a.S + p);
+    }
   }
-  fl.valid = true;
-  fl.v = __ldg(a.S + p);
-  const uint64_t want = (static_cast<uint64_t>(a.tag) << 32) | static_cast<uint32_t>(~static_cast<uint32_t>(p));
-  fl.first = a.first[fl.v] == want;
-  if (fl.first) fl.isnew = static_cast<uint32_t>(a.gidx[fl.v] >> 32) != a.gtag;
-  return fl;
+  uint64_t fw[kFinRounds];
+#pragma unroll
+  for (int r = 0; r < kFinRounds; ++r) fw[r] = (valid >> r) & 1u ? a.first[fl[r].v] : 0ull;
+  uint64_t gw[kFinRounds];
+#pragma unroll
+  for (int r = 0; r < kFinRounds; ++r) {
+    const uint64_t p = base + r * kFinThreads + threadIdx.x;
+    const uint64_t want = (static_cast<uint64_t>(a.tag) << 32) | static_cast<uint32_t>(~static_cast<uint32_t>(p));
+    fl[r].valid = (valid >> r) & 1u;
+    fl[r].first = fl[r].valid && fw[r] == want;
+    gw[r] = fl[r].first ? a.gidx[fl[r].v] : 0ull;
+  }
+#pragma unroll
+  for (int r = 0; r < kFinRounds; ++r) fl[r].isnew = fl[r].first && static_cast<uint32_t>(gw[r] >> 32) != a.gtag;
 }
 
 __global__ void __launch_bounds__(kFinThreads) k_fin_count(FinArgs a) {
@@ -863,12 +1243,13 @@ __global__ void __launch_bounds__(kFinThreads) k_fin_count(FinArgs a) {
   __syncthreads();
   uint32_t cv = 0, cf = 0, cn = 0;
   const int lane = threadIdx.x & 31;
+  Flags fl[kFinRounds];
+  fin_flags_all(a, P, base, fl);
 #pragma unroll
   for (int r = 0; r < kFinRounds; ++r) {
-    const Flags fl = fin_flags(a, P, base + r * kFinThreads + threadIdx.x);
-    cv += __popc(__ballot_sync(kFull, fl.valid));
-    cf += __popc(__ballot_sync(kFull, fl.first));
-    cn += __popc(__ballot_sync(kFull, fl.isnew));
+    cv += __popc(__ballot_sync(kFull, fl[r].valid));
+    cf += __popc(__ballot_sync(kFull, fl[r].first));
+    cn += __popc(__ballot_sync(kFull, fl[r].isnew));
   }
   if (lane == 0) {
     atomicAdd(&s_cnt[0], cv);
@@ -926,8 +1307,11 @@ __global__ void __launch_bounds__(kFinThreads) k_fin_emit(FinArgs a) {
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kFinTile;
   const unsigned lt = (1u << lane) - 1u;
   uint32_t run_f = pf, run_n = pn;
+  Flags fla[kFinRounds];
+  fin_flags_all(a, P, base, fla);
+#pragma unroll
   for (int r = 0; r < kFinRounds; ++r) {
-    const Flags fl = fin_flags(a, P, base + r * kFinThreads + threadIdx.x);
+    const Flags& fl = fla[r];
     const unsigned bf = __ballot_sync(kFull, fl.first);
     const unsigned bn = __ballot_sync(kFull, fl.isnew);
     if (lane == 0) {
@@ -1038,8 +1422,29 @@ void launch_layer_kernels(const SampleArgs& sa, int sm_count, cudaStream_t st) {
                                     static_cast<int>(kMergeSmem)));
       attr_set = true;
     }
-    k_stream<WM><<<sm_count * 3, kStreamWarps * 32, kStreamSmem, st>>>(sa);
-    A3G_LAUNCH_CHECK("k_stream");
+    if (WM != 2 || sa.kind == A3G_SAMPLER_UNIFORM) {
+      // integer keys: thread per item over the length-sorted items
+      const HubArena& hb = sa.hub;
+      k_item_keys<<<sm_count * 2, 256, 0, st>>>(hb.items, sa.item_count, hb.item_cap, hb.sort_keys[0],
+                                                hb.sort_vals[0]);
+      A3G_LAUNCH_CHECK("k_item_keys");
+      size_t tmp = hb.sort_tmp_bytes;
+      A3G_CUDA(cub::DeviceRadixSort::SortPairsDescending(hb.sort_tmp, tmp, hb.sort_keys[0], hb.sort_keys[1],
+                                                         hb.sort_vals[0], hb.sort_vals[1],
+                                                         static_cast<int>(hb.item_cap), 0, 13, st));
+      constexpr int W = WM == 2 ? 0 : WM;
+      const int grid = sm_count * 8;
+      if (sa.f <= 8)
+        k_stream_grp<W, 8><<<grid, 256, 0, st>>>(sa, hb.sort_vals[1]);
+      else if (sa.f <= 16)
+        k_stream_grp<W, 16><<<grid, 256, 0, st>>>(sa, hb.sort_vals[1]);
+      else
+        k_stream_grp<W, 32><<<grid, 256, 0, st>>>(sa, hb.sort_vals[1]);
+      A3G_LAUNCH_CHECK("k_stream_grp");
+    } else {
+      k_stream<WM><<<sm_count * 3, kStreamWarps * 32, kStreamSmem, st>>>(sa);
+      A3G_LAUNCH_CHECK("k_stream");
+    }
     k_hub_merge_warp<WM><<<sm_count * 2, 256, 0, st>>>(sa);
     A3G_LAUNCH_CHECK("k_hub_merge_warp");
     k_hub_merge<WM><<<sm_count * 2, kMergeThreads, kMergeSmem, st>>>(sa);
@@ -1188,4 +1593,16 @@ void launch_reservoir_list(const uint32_t* d_nb, const double* d_w, uint64_t deg
   A3G_LAUNCH_CHECK("k_reservoir_list");
 }
 
+}  // namespace a3g
+
+namespace a3g {
+size_t item_sort_temp_bytes(uint32_t n) {
+  size_t bytes = 0;
+  A3G_CUDA(cub::DeviceRadixSort::SortPairsDescending(static_cast<void*>(nullptr), bytes,
+                                                     static_cast<const uint32_t*>(nullptr),
+                                                     static_cast<uint32_t*>(nullptr),
+                                                     static_cast<const uint32_t*>(nullptr),
+                                                     static_cast<uint32_t*>(nullptr), static_cast<int>(n), 0, 13));
+  return bytes;
+}
 }  // namespace a3g

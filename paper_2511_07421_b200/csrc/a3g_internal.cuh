@@ -89,6 +89,8 @@ struct BatchCounters {
   uint32_t segs[kMaxLayers];        // hub segments reserved per layer
   uint32_t items[kMaxLayers];       // stream items appended per layer
   uint32_t iwork[kMaxLayers];       // stream items claimed per layer
+  uint32_t hub_big[kMaxLayers];     // hubs with > 8 segments (block merge)
+  uint32_t hub_small[kMaxLayers];   // hubs with 1..8 segments (warp merge)
   uint32_t n_seeds;                 // seeds given (incl. duplicates)
   uint32_t hits, misses;            // retrieve_features accounting
   uint32_t pad;

@@ -109,6 +109,8 @@ void sampler_alloc(SamplerState& s, a3g_graph* g, a3g_cache* c, uint32_t max_see
   hb.row = dalloc<uint32_t>(hb.hub_cap);
   hb.seg0 = dalloc<uint32_t>(hb.hub_cap);
   hb.nseg = dalloc<uint32_t>(hb.hub_cap);
+  hb.big = dalloc<uint32_t>(hb.hub_cap);
+  hb.small = dalloc<uint32_t>(hb.hub_cap);
   hb.seg_hub = dalloc<uint32_t>(hb.seg_cap);
   hb.rec_cnt = dalloc<uint32_t>(hb.seg_cap);
   hb.tau = dalloc<uint64_t>(hb.seg_cap);
@@ -150,6 +152,8 @@ void sampler_free(SamplerState& s) {
   dfree(s.hub.row);
   dfree(s.hub.seg0);
   dfree(s.hub.nseg);
+  dfree(s.hub.big);
+  dfree(s.hub.small);
   dfree(s.hub.seg_hub);
   dfree(s.hub.rec_cnt);
   dfree(s.hub.tau);

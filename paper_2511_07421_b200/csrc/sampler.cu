@@ -37,6 +37,7 @@ namespace {
 
 using rsv::kFull;
 constexpr int kRowChunk = 4;  // rows claimed per atomic by a warp
+constexpr uint32_t kMergeFilterWarpsC = 8;  // hub size class boundary (== kMergeFilterWarps)
 
 __device__ __forceinline__ void mark_first(uint64_t* first, uint32_t v, uint32_t tag, uint32_t pos) {
   atomicMax(reinterpret_cast<unsigned long long*>(first + v),
@@ -57,6 +58,8 @@ struct SampleArgs {
   HubArena hub;
   uint32_t* hub_count;
   uint32_t* seg_count;
+  uint32_t* big_count;    // hubs with > kMergeFilterWarps segments (k_hub_merge)
+  uint32_t* small_count;  // hubs with 1..kMergeFilterWarps segments (k_hub_merge_warp)
   uint32_t* item_count;
   uint32_t* item_work;
   uint64_t seed;
@@ -235,6 +238,11 @@ __global__ void __launch_bounds__(256) k_classify(SampleArgs a) {
           a.hub.nseg[h] = ok ? nseg : 0u;  // 0: streamed as one whole-row item instead
         }
         if (ok) {
+          // per size class work lists of the two merge kernels
+          if (nseg > kMergeFilterWarpsC)
+            a.hub.big[atomicAdd(a.big_count, 1u)] = h;
+          else
+            a.hub.small[atomicAdd(a.small_count, 1u)] = h;
           for (uint32_t i = 0; i < nseg; ++i) a.hub.seg_hub[s0 + i] = h;
           n_items = nseg;
         } else {
@@ -814,9 +822,195 @@ __global__ void k_item_keys(const uint4* items, const uint32_t* item_count, uint
 template <int WM>
 __global__ void __launch_bounds__(256) k_hub_merge_warp(SampleArgs a);
 
-constexpr int kMergeFilterWarps = 8;
+constexpr int kMergeFilterWarps = kMergeFilterWarpsC;
 constexpr int kMergeThreads = (kMergeFilterWarps + 1) * 32;
-constexpr size_t kMergeSmem = 2ull * kMergeFilterWarps * kRecCap * (8 + 4);
+constexpr size_t kMergeSmemWin = 2ull * kMergeFilterWarps * kRecCap * (8 + 4);
+
+// Big hubs (more than kMergeFilterWarps segments), block per hub, without a
+// serial window chain: (A) L_s = max tau over segments < s and the record
+// prefix over segments (warp scans), (B) every thread filters records of the
+// flattened (segment, record) list against L_s -- a global insertion in
+// segment s must beat the running minimum, which is >= L_s -- into a keep
+// bitmap (independent loads, no warp collectives), then ranks the kept ones
+// by popcounts and writes them in (segment, record) order to shared memory,
+// (C) warp 0 replays the few survivors exactly. Falls back to the windowed
+// k_hub_merge path (same block) when a hub has more segments or survivors
+// than the shared-memory plan holds.
+constexpr int kM2Warps = kMergeFilterWarps + 1;  // the k_hub_merge block
+constexpr int kM2Threads = kM2Warps * 32;
+constexpr uint32_t kM2MaxSegs = 1024;
+constexpr uint32_t kM2MaxSurv = 3072;
+constexpr uint32_t kM2Words = kRecCap / 32;  // keep-bitmap words per segment
+constexpr size_t kM2Smem = kM2MaxSegs * (8 + 4 + 4 + 4 + 4 * kM2Words) + kM2MaxSurv * (8 + 4);
+
+template <int WM>
+__device__ bool hub_merge_parallel(const SampleArgs& a, uint32_t h, uint8_t* smem) {
+  using P = typename PolOf<WM>::P;
+  using K = typename P::K;
+  K* s_L = reinterpret_cast<K*>(smem);                                   // [segs] prefix max tau
+  uint32_t* s_lok = reinterpret_cast<uint32_t*>(smem + kM2MaxSegs * 8);  // [segs]
+  uint32_t* s_pre = s_lok + kM2MaxSegs;                                  // [segs] record prefix
+  uint32_t* s_off = s_pre + kM2MaxSegs;                                  // [segs] survivor prefix
+  uint32_t* s_bits = s_off + kM2MaxSegs;                                 // [segs][kM2Words]
+  K* s_key = reinterpret_cast<K*>(s_bits + kM2MaxSegs * kM2Words);        // [kM2MaxSurv]
+  uint32_t* s_pos = reinterpret_cast<uint32_t*>(s_key + kM2MaxSurv);      // [kM2MaxSurv]
+  __shared__ uint32_t s_nrec, s_total;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t ns = a.hub.nseg[h], s0 = a.hub.seg0[h], k = a.hub.row[h];
+  const uint32_t m = a.f;
+  if (ns > kM2MaxSegs) return false;
+  P pol = PolOf<WM>::make(a);
+  for (uint32_t i = threadIdx.x; i < ns * kM2Words; i += blockDim.x) s_bits[i] = 0;
+  if (warp == 0) {
+    // (A) exclusive prefix max of tau (segments with tau_ok) + record prefix
+    K run{};
+    int rok = 0;
+    uint32_t rrun = 0;
+    for (uint32_t c0 = 0; c0 < ns; c0 += 32) {
+      const uint32_t s = c0 + lane;
+      int ok = 0;
+      K tv{};
+      uint32_t rc = 0;
+      if (s < ns) {
+        ok = a.hub.tau_ok[s0 + s];
+        tv = key_from_bits<K>(a.hub.tau[s0 + s]);
+        rc = a.hub.rec_cnt[s0 + s];
+        if (s == 0) rc = rc > m ? rc - m : 0u;  // segment 0's fill records seed the reservoir
+      }
+      K iv = tv;
+      int iok = ok;
+      uint32_t inc = rc;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const K ov = __shfl_up_sync(kFull, iv, off);
+        const int oo = __shfl_up_sync(kFull, iok, off);
+        const uint32_t oc = __shfl_up_sync(kFull, inc, off);
+        if (lane >= off) {
+          if (oo && (!iok || ov > iv)) {
+            iv = ov;
+            iok = 1;
+          }
+          inc += oc;
+        }
+      }
+      K ev = __shfl_up_sync(kFull, iv, 1);
+      int eok = __shfl_up_sync(kFull, iok, 1);
+      if (lane == 0) eok = 0;
+      if (rok && (!eok || run > ev)) {
+        ev = run;
+        eok = 1;
+      }
+      if (s < ns) {
+        s_L[s] = ev;
+        s_lok[s] = eok;
+        s_pre[s] = rrun + inc - rc;
+      }
+      const K lv = __shfl_sync(kFull, iv, 31);
+      const int lo = __shfl_sync(kFull, iok, 31);
+      if (lo && (!rok || lv > run)) {
+        run = lv;
+        rok = 1;
+      }
+      rrun += __shfl_sync(kFull, inc, 31);
+    }
+    if (lane == 0) s_nrec = rrun;
+  }
+  __syncthreads();
+  const uint32_t nrec = s_nrec;
+  // segment of flattened record r: last s with s_pre[s] <= r
+  auto seg_of = [&](uint32_t r) {
+    uint32_t lo = 0, hi = ns;  // s_pre[lo] <= r < s_pre[hi]
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (s_pre[mid] <= r) lo = mid; else hi = mid;
+    }
+    return lo;
+  };
+  // (B1) keep bitmap
+  for (uint32_t r = threadIdx.x; r < nrec; r += blockDim.x) {
+    const uint32_t s = seg_of(r);
+    const uint32_t i = r - s_pre[s] + (s == 0 ? m : 0u);
+    const K kv = key_from_bits<K>(a.hub.rec_key[static_cast<uint64_t>(s0 + s) * kRecCap + i]);
+    if (!s_lok[s] || pol.keep(kv, s_L[s])) atomicOr(&s_bits[s * kM2Words + (i >> 5)], 1u << (i & 31));
+  }
+  __syncthreads();
+  if (warp == 0) {  // survivors per segment -> exclusive offsets
+    uint32_t run = 0;
+    for (uint32_t c0 = 0; c0 < ns; c0 += 32) {
+      const uint32_t s = c0 + lane;
+      uint32_t v = 0;
+      if (s < ns)
+        for (uint32_t w = 0; w < kM2Words; ++w) v += __popc(s_bits[s * kM2Words + w]);
+      uint32_t inc = v;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, inc, off);
+        if (lane >= off) inc += y;
+      }
+      if (s < ns) s_off[s] = run + inc - v;
+      run += __shfl_sync(kFull, inc, 31);
+    }
+    if (lane == 0) s_total = run;
+  }
+  __syncthreads();
+  if (s_total > kM2MaxSurv) return false;  // uniform: read after the barrier
+  // (B2) kept records to their (segment, record)-ordered rank
+  for (uint32_t r = threadIdx.x; r < nrec; r += blockDim.x) {
+    const uint32_t s = seg_of(r);
+    const uint32_t i = r - s_pre[s] + (s == 0 ? m : 0u);
+    const uint32_t* bw = s_bits + s * kM2Words;
+    if (!((bw[i >> 5] >> (i & 31)) & 1u)) continue;
+    uint32_t rank = s_off[s] + __popc(bw[i >> 5] & ((1u << (i & 31)) - 1u));
+    for (uint32_t w = 0; w < (i >> 5); ++w) rank += __popc(bw[w]);
+    const uint64_t rb = static_cast<uint64_t>(s0 + s) * kRecCap + i;
+    s_key[rank] = key_from_bits<K>(a.hub.rec_key[rb]);
+    s_pos[rank] = a.hub.rec_id[rb];
+  }
+  __syncthreads();
+  // (C) exact replay of the survivors by warp 0
+  if (warp == 0) {
+    const uint32_t dst = a.front[k];
+    const uint64_t beg = a.ro[dst];
+    const uint32_t* nb = a.col + beg;
+    const uint64_t rb0 = static_cast<uint64_t>(s0) * kRecCap;
+    rsv::WState<K> st;
+    st.my_key = lane < static_cast<int>(m) ? key_from_bits<K>(a.hub.rec_key[rb0 + lane]) : pol.inf();
+    st.my_id = lane < static_cast<int>(m) ? a.hub.rec_id[rb0 + lane] : 0u;
+    pol.argmin(st.thr, st.mp, st.my_key, lane);
+    const uint32_t n = s_total;
+    for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const bool valid = i < n;
+      const K kk = valid ? s_key[i] : K{};
+      const uint32_t v = valid ? s_pos[i] : 0u;
+      unsigned mask = __ballot_sync(kFull, valid && pol.cheap_gt(kk, st.thr));
+      while (mask) {
+        const int src = __ffs(mask) - 1;
+        const K kv = __shfl_sync(kFull, kk, src);
+        const uint32_t iv = __shfl_sync(kFull, v, src);
+        if (pol.gt(kv, st.thr)) {
+          if (lane == st.mp) {
+            st.my_key = kv;
+            st.my_id = iv;
+          }
+          pol.argmin(st.thr, st.mp, st.my_key, lane);
+          mask &= __ballot_sync(kFull, valid && pol.cheap_gt(kk, st.thr));
+        }
+        mask &= ~((2u << src) - 1u);
+      }
+    }
+    const uint64_t row0 = static_cast<uint64_t>(k) * m;
+    if (lane < static_cast<int>(m)) {
+      const uint32_t id = __ldg(nb + st.my_id);  // records hold row positions
+      a.S[row0 + lane] = id;
+      mark_first(a.first, id, a.tag, static_cast<uint32_t>(row0 + lane));
+    }
+    if (lane == 0) a.cnt[k] = m;
+  }
+  return true;
+}
+
+constexpr size_t kMergeSmem = kMergeSmemWin > kM2Smem ? kMergeSmemWin : kM2Smem;
 
 // Block per hub: warp 0 replays window w-1 while warps 1..8 filter window w.
 template <int WM>
@@ -831,9 +1025,10 @@ __global__ void __launch_bounds__(kMergeThreads) k_hub_merge(SampleArgs a) {
   __shared__ int s_lok[2];
   __shared__ uint32_t s_hub[4];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t nhub = min(*a.hub_count, a.hub.hub_cap);
+  const uint32_t nbig = min(*a.big_count, a.hub.hub_cap);
   const uint32_t m = a.f;
-  for (uint32_t h = blockIdx.x; h < nhub; h += gridDim.x) {
+  for (uint32_t hb = blockIdx.x; hb < nbig; hb += gridDim.x) {
+    const uint32_t h = a.hub.big[hb];
     if (threadIdx.x == 0) {
       s_hub[0] = a.hub.nseg[h];
       s_hub[1] = a.hub.seg0[h];
@@ -879,6 +1074,9 @@ __global__ void __launch_bounds__(kMergeThreads) k_hub_merge(SampleArgs a) {
       __syncthreads();
       continue;
     }
+    const bool par = hub_merge_parallel<WM>(a, h, smem_raw);  // uniform across the block
+    __syncthreads();
+    if (par) continue;
     P pol = PolOf<WM>::make(a);
     rsv::WState<K> st;
     if (warp == 0) {  // global fill = records 0..m-1 of segment 0 (positions 0..m-1)
@@ -1019,11 +1217,12 @@ __global__ void __launch_bounds__(256) k_hub_merge_warp(SampleArgs a) {
   using P = typename PolOf<WM>::P;
   using K = typename P::K;
   const int lane = threadIdx.x & 31;
-  const uint32_t nhub = min(*a.hub_count, a.hub.hub_cap);
+  const uint32_t nsmall = min(*a.small_count, a.hub.hub_cap);
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   const uint32_t m = a.f;
-  for (uint32_t h = gw; h < nhub; h += nw) {
+  for (uint32_t hs = gw; hs < nsmall; hs += nw) {
+    const uint32_t h = a.hub.small[hs];
     const uint32_t ns = a.hub.nseg[h];
     if (ns == 0 || ns > kMergeFilterWarps) continue;
     const uint32_t s0 = a.hub.seg0[h], k = a.hub.row[h];
@@ -1517,6 +1716,8 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
     sa.hub = s.hub;
     sa.hub_count = &ctr->hubs[l];
     sa.seg_count = &ctr->segs[l];
+    sa.big_count = &ctr->hub_big[l];
+    sa.small_count = &ctr->hub_small[l];
     sa.item_count = &ctr->items[l];
     sa.item_work = &ctr->iwork[l];
     sa.seed = rng_seed;

@@ -29,6 +29,8 @@ struct HubArena {
   uint32_t* row = nullptr;       // [hub_cap] frontier row of hub h
   uint32_t* seg0 = nullptr;      // [hub_cap] first segment
   uint32_t* nseg = nullptr;      // [hub_cap] #segments (0: handled in-row)
+  uint32_t* big = nullptr;       // [hub_cap] hubs with > 8 segments
+  uint32_t* small = nullptr;     // [hub_cap] hubs with 1..8 segments
   uint32_t* seg_hub = nullptr;   // [seg_cap] owning hub
   uint32_t* rec_cnt = nullptr;   // [seg_cap]
   uint64_t* tau = nullptr;       // [seg_cap] m-th largest key of the segment (policy key bits)

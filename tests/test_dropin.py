@@ -32,7 +32,7 @@ def run(preload=None):
     env = dict(os.environ)
     if preload:
         env["LD_PRELOAD"] = preload
-    r = subprocess.run([CHECK, str(N)], capture_output=True, text=True, env=env, timeout=600)
+    r = subprocess.run([CHECK, str(N)], capture_output=True, text=True, env=env, timeout=120)
     assert r.returncode == 0, r.stderr[-2000:]
     return r.stdout.strip().splitlines()
 

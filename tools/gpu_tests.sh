@@ -1,5 +1,5 @@
 # GPU parity suite on the box; log under gpurun_out/
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -x -q ${PYTEST_ARGS:-} > gpurun_out/pytest_gpu.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -x -q --timeout 300 ${PYTEST_ARGS:-} > gpurun_out/pytest_gpu.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 tail -30 gpurun_out/pytest_gpu.log

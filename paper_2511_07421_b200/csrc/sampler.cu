@@ -59,7 +59,7 @@ struct SampleArgs {
   uint32_t* hub_count;
   uint32_t* seg_count;
   uint32_t* big_count;    // hubs with > kMergeFilterWarps segments (k_hub_merge)
-  uint32_t* small_count;  // hubs with 1..kMergeFilterWarps segments (k_hub_merge_warp)
+  uint32_t* small_count;  // hubs with 1..kMergeFilterWarps segments (merge_small_hub)
   uint32_t* item_count;
   uint32_t* item_work;
   uint64_t seed;
@@ -808,9 +808,9 @@ __global__ void k_item_keys(const uint4* items, const uint32_t* item_count, uint
   const uint32_t n = min(*item_count, cap);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) {
     uint32_t len = 0;
-    if (i < n) {
+    if (i < n) {  // 255 length buckets of 16 positions: one radix pass
       const uint4 it = items[i];
-      len = min(it.z - it.y, 4095u) + 1;
+      len = min((it.z - it.y) >> 4, 254u) + 1;
     }
     keys[i] = len;
     vals[i] = i;
@@ -820,7 +820,7 @@ __global__ void k_item_keys(const uint4* items, const uint32_t* item_count, uint
 // Warp per hub with few segments (<= kMergeFilterWarps): replay the records in
 // segment order, dropping those that cannot beat max_{s'<s} tau_{s'}.
 template <int WM>
-__global__ void __launch_bounds__(256) k_hub_merge_warp(SampleArgs a);
+__device__ void merge_small_hub(const SampleArgs& a, uint32_t h, int lane);
 
 constexpr int kMergeFilterWarps = kMergeFilterWarpsC;
 constexpr int kMergeThreads = (kMergeFilterWarps + 1) * 32;
@@ -1038,7 +1038,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_hub_merge(SampleArgs a) {
     }
     __syncthreads();
     const uint32_t ns = s_hub[0];
-    if (ns <= kMergeFilterWarps) {  // 0: streamed whole; small: k_hub_merge_warp
+    if (ns <= kMergeFilterWarps) {  // 0: streamed whole; small: merge_small_hub
       __syncthreads();
       continue;
     }
@@ -1210,21 +1210,28 @@ __global__ void __launch_bounds__(kMergeThreads) k_hub_merge(SampleArgs a) {
     }
     __syncthreads();
   }
+  // small hubs (1..kMergeFilterWarps segments): warp per hub, claimed
+  // dynamically so warps of blocks without (or done with) big hubs take them
+  const uint32_t nsmall = min(*a.small_count, a.hub.hub_cap);
+  for (;;) {
+    uint32_t hs = 0;
+    if (lane == 0) hs = atomicAdd(a.work, 1u);
+    hs = __shfl_sync(kFull, hs, 0);
+    if (hs >= nsmall) break;
+    merge_small_hub<WM>(a, a.hub.small[hs], lane);
+  }
 }
 
+// Warp merge of one hub with 1..kMergeFilterWarps segments: replay the
+// records in segment order, dropping those that cannot beat max_{s'<s} tau_{s'}.
 template <int WM>
-__global__ void __launch_bounds__(256) k_hub_merge_warp(SampleArgs a) {
+__device__ void merge_small_hub(const SampleArgs& a, uint32_t h, int lane) {
   using P = typename PolOf<WM>::P;
   using K = typename P::K;
-  const int lane = threadIdx.x & 31;
-  const uint32_t nsmall = min(*a.small_count, a.hub.hub_cap);
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   const uint32_t m = a.f;
-  for (uint32_t hs = gw; hs < nsmall; hs += nw) {
-    const uint32_t h = a.hub.small[hs];
+  {
     const uint32_t ns = a.hub.nseg[h];
-    if (ns == 0 || ns > kMergeFilterWarps) continue;
+    if (ns == 0 || ns > kMergeFilterWarps) return;
     const uint32_t s0 = a.hub.seg0[h], k = a.hub.row[h];
     const uint32_t dst = a.front[k];
     const uint64_t beg = a.ro[dst], deg = a.ro[dst + 1] - beg;
@@ -1250,7 +1257,7 @@ __global__ void __launch_bounds__(256) k_hub_merge_warp(SampleArgs a) {
       }
     } else if (__ballot_sync(kFull, rc_l > kRecCap)) {  // records overflowed: whole-row replay
       row_by_warp<WM>(a, nb, deg, key, k, lane);
-      continue;
+      return;
     } else {
       P pol = PolOf<WM>::make(a);
       rsv::WState<K> st;
@@ -1630,7 +1637,7 @@ void launch_layer_kernels(const SampleArgs& sa, int sm_count, cudaStream_t st) {
       size_t tmp = hb.sort_tmp_bytes;
       A3G_CUDA(cub::DeviceRadixSort::SortPairsDescending(hb.sort_tmp, tmp, hb.sort_keys[0], hb.sort_keys[1],
                                                          hb.sort_vals[0], hb.sort_vals[1],
-                                                         static_cast<int>(hb.item_cap), 0, 13, st));
+                                                         static_cast<int>(hb.item_cap), 0, 8, st));
       constexpr int W = WM == 2 ? 0 : WM;
       const int grid = sm_count * 8;
       if (sa.f <= 8)
@@ -1644,8 +1651,6 @@ void launch_layer_kernels(const SampleArgs& sa, int sm_count, cudaStream_t st) {
       k_stream<WM><<<sm_count * 3, kStreamWarps * 32, kStreamSmem, st>>>(sa);
       A3G_LAUNCH_CHECK("k_stream");
     }
-    k_hub_merge_warp<WM><<<sm_count * 2, 256, 0, st>>>(sa);
-    A3G_LAUNCH_CHECK("k_hub_merge_warp");
     k_hub_merge<WM><<<sm_count * 2, kMergeThreads, kMergeSmem, st>>>(sa);
     A3G_LAUNCH_CHECK("k_hub_merge");
   }
@@ -1803,7 +1808,7 @@ size_t item_sort_temp_bytes(uint32_t n) {
                                                      static_cast<const uint32_t*>(nullptr),
                                                      static_cast<uint32_t*>(nullptr),
                                                      static_cast<const uint32_t*>(nullptr),
-                                                     static_cast<uint32_t*>(nullptr), static_cast<int>(n), 0, 13));
+                                                     static_cast<uint32_t*>(nullptr), static_cast<int>(n), 0, 8));
   return bytes;
 }
 }  // namespace a3g

@@ -250,7 +250,8 @@ struct OuterArgs {
   float* dlogits;
   float* loss_s;
   float* dagg;     // [cap_seeds x H] per-edge dh1 contribution of seed s
-  uint32_t* keys;  // [cap_seeds x (f0 + 1)] dh1 row of each scatter entry (kInv: none)
+  uint32_t* keys;  // [cap_seeds x (f0 + 1)] dh1 row of each scatter entry (none: `none`)
+  uint32_t none;   // padding key, > every row index (the sort needs bit_width(none) bits)
   uint32_t* vals;  // seed of each scatter entry
   uint32_t cap_seeds;
   int has_layer0;
@@ -313,34 +314,34 @@ __global__ void __launch_bounds__(256) k_outer(OuterArgs a) {
     // entries in edge order, then the self-fallback entry (trainer.cpp:182-198)
     const uint64_t e0 = static_cast<uint64_t>(s) * a.f0;
     for (uint32_t t = lane; t < a.f0; t += 32) {
-      a.keys[e0 + t] = t < c0 ? srcs[t] : kInv;
+      a.keys[e0 + t] = t < c0 ? srcs[t] : a.none;
       a.vals[e0 + t] = s;
     }
     if (lane == 0) {
       const uint64_t fb = static_cast<uint64_t>(a.cap_seeds) * a.f0 + s;
-      a.keys[fb] = c0 == 0 ? s : kInv;
+      a.keys[fb] = c0 == 0 ? s : a.none;
       a.vals[fb] = s;
     }
   }
   // pad the unused tail of the entry arrays (rows ns .. cap_seeds)
   const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
   for (uint64_t i = static_cast<uint64_t>(ns) * a.f0 + gt; i < static_cast<uint64_t>(a.cap_seeds) * a.f0; i += nt)
-    a.keys[i] = kInv;
+    a.keys[i] = a.none;
   for (uint64_t i = static_cast<uint64_t>(a.cap_seeds) * a.f0 + ns + gt;
        i < static_cast<uint64_t>(a.cap_seeds) * (a.f0 + 1); i += nt)
-    a.keys[i] = kInv;
+    a.keys[i] = a.none;
 }
 
 // dh1[r] = sum of the contributions of the sorted entries with key r, in
 // order (edges in edge order, then the fallback): deterministic, no atomics.
 __global__ void __launch_bounds__(256) k_dh1_gather(const uint32_t* keys, const uint32_t* vals, uint64_t n_entries,
-                                                    const float* dagg, uint32_t H, float* dh1) {
+                                                    uint32_t none, const float* dagg, uint32_t H, float* dh1) {
   const int lane = threadIdx.x & 31;
   const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t i = gw; i < n_entries; i += nw) {
     const uint32_t r = keys[i];
-    if (r == kInv) break;  // sorted: the padding is last
+    if (r == none) break;  // sorted: the padding is last
     if (i > 0 && keys[i - 1] == r) continue;  // not the head of its run
     float acc = 0.f;
     for (uint64_t j = i; j < n_entries && keys[j] == r; ++j)
@@ -544,6 +545,9 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
   oa.keys = t.d_keys[0];
   oa.vals = t.d_vals[0];
   oa.cap_seeds = t.max_seeds;
+  oa.none = static_cast<uint32_t>(t.cap_inner);
+  int sort_bits = 1;
+  while (sort_bits < 32 && (t.cap_inner >> sort_bits) != 0) ++sort_bits;
   if (oa.f0 == 0) oa.f0 = 1;  // no layer: fallback entries only (keys of the edge part are all kInv)
   k_outer<<<std::max(1, static_cast<int>((t.max_seeds + 7) / 8)), 256, 0, st>>>(oa);
   A3G_LAUNCH_CHECK("k_outer");
@@ -551,8 +555,9 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
   {
     size_t tmp = t.sort_tmp_bytes;
     A3G_CUDA(cub::DeviceRadixSort::SortPairs(t.d_sort_tmp, tmp, t.d_keys[0], t.d_keys[1], t.d_vals[0], t.d_vals[1],
-                                             static_cast<int>(t.n_entries), 0, 32, st));
-    k_dh1_gather<<<t.sm_count * 2, 256, 0, st>>>(t.d_keys[1], t.d_vals[1], t.n_entries, t.d_dagg, t.H, t.d_dh1);
+                                             static_cast<int>(t.n_entries), 0, sort_bits, st));
+    k_dh1_gather<<<t.sm_count * 2, 256, 0, st>>>(t.d_keys[1], t.d_vals[1], t.n_entries, oa.none, t.d_dagg, t.H,
+                                                 t.d_dh1);
     A3G_LAUNCH_CHECK("k_dh1_gather");
   }
   // ---- dW1 = agg_inner^T . (dh1 * [h1 > 0]) on tcgen05, partials per row split

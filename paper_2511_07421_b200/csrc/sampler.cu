@@ -8,19 +8,26 @@
 // (sampler.cpp:113-131).
 //
 // Per layer:
-//   k_sample_rows   warp per frontier row (dynamic chunks of rows). deg <= m:
-//                   copy; m < deg <= kSeg: in-warp exact replay
-//                   (reservoir.cuh); deg > kSeg ("hubs", up to n-1
-//                   neighbours): registered for splitting.
-//   k_hub_segments  warp per kSeg-long segment of a hub row: local replay from
-//                   an empty reservoir, emitting every local insertion
-//                   ("record") and the segment's exact m-th largest key tau_s.
-//                   Every global insertion is a local record of its segment.
-//   k_hub_merge     block per hub: 8 filter warps drop the records of segment
-//                   s whose key cannot beat max_{s'<s} tau_{s'} (a lower bound
-//                   of the running minimum) while a replay warp applies the
-//                   survivors of the previous window in order -- the
-//                   sequential slot history, reproduced exactly.
+//   k_classify      frontier rows -> work items: deg <= m rows are copied
+//                   (fill only, sampler.cpp:30-33); m < deg <= kSeg rows are one
+//                   item; deg > kSeg rows ("hubs", up to n-1 neighbours) are
+//                   split into kSeg-long segment items + a merge entry in the
+//                   small (<= 8 segments) or big hub work list.
+//   k_item_keys + one-pass radix sort: items ordered by length (descending).
+//   k_stream_grp    integer-key policies (all weights 1 or all gamma, and
+//                   Algorithm R): lane groups of next_pow2(m) lanes, one item
+//                   per group, keys hashed from positions only; candidates
+//                   replayed in order per group (exact slot history).
+//   k_stream        bitmap-weighted keys (partial cache, gamma > 1): warp per
+//                   item over TMA-staged neighbour-id pieces (fp64 keys).
+//   segments        replay locally from an empty reservoir, emitting every
+//                   local insertion ("record", row position + key) and the
+//                   segment's exact m-th largest key tau_s: every global
+//                   insertion is a local record of its segment.
+//   k_hub_merge     big hubs: block per hub, parallel filter of all records
+//                   against L_s = max_{s'<s} tau_{s'} (a lower bound of the
+//                   running minimum), then an exact replay of the survivors;
+//                   small hubs: warp per hub, claimed dynamically.
 //   k_fin_count / k_fin_emit: first-seen dedup + relabel (tagged atomicMax of
 //                   the first position, tile partials, ballot scans).
 // Counts stay on the device: no host sync inside a batch.

@@ -625,18 +625,18 @@ __global__ void __launch_bounds__(256) k_stream_int(SampleArgs a) {
 // (PolGammaAll; PolUnit keys are exact integers).
 template <int G, typename P>
 __device__ __forceinline__ void grp_argmin(const P& pol, uint64_t my, uint32_t gl, uint64_t& thr, uint32_t& mp) {
-  uint64_t k = my;
-  uint32_t i = gl;
+  // fast path: butterfly on the packed (top 32 key bits, slot) -- one 64-bit
+  // min per step; exact whenever no other slot shares the minimum's top bits
+  // (or, for K-ties, the next value): keys differing only below bit 21 are the
+  // sole ambiguity, and every K-tie window (<= 64 (gamma + 1) << 2^21) lies there
+  const uint32_t my32 = static_cast<uint32_t>(my >> 21);
+  uint64_t pk = (static_cast<uint64_t>(my32) << 32) | gl;
 #pragma unroll
-  for (int off = G / 2; off > 0; off >>= 1) {
-    const uint64_t ok = __shfl_xor_sync(kFull, k, off, G);
-    const uint32_t oi = __shfl_xor_sync(kFull, i, off, G);
-    if (ok < k || (ok == k && oi < i)) {
-      k = ok;
-      i = oi;
-    }
-  }
-  if (P::kNearTies && __any_sync(kFull, my != ~0ull && my != k && my - k <= pol.tie)) {
+  for (int off = G / 2; off > 0; off >>= 1) pk = min(pk, __shfl_xor_sync(kFull, pk, off, G));
+  const uint32_t m32 = static_cast<uint32_t>(pk >> 32);
+  uint32_t i = static_cast<uint32_t>(pk);
+  uint64_t k = __shfl_sync(kFull, my, static_cast<int>(i), G);
+  if (__any_sync(kFull, gl != i && my != ~0ull && my32 - m32 <= 1u)) {
     // exact pass: first slot whose K equals the minimum's K
     uint64_t kk = my;
     uint32_t ii = gl;
@@ -767,7 +767,7 @@ __global__ void __launch_bounds__(256) k_stream_grp(SampleArgs a, const uint32_t
           const int src = mask ? __ffs(mask) - 1 : lane;
           const uint64_t kv = __shfl_sync(kFull, kk, src);
           const bool ins = mask != 0 && pol.gt(kv, thr);
-          const uint32_t pos = jb + b + u * G + (src % G);
+          const uint32_t pos = jb + b + u * G + (static_cast<uint32_t>(src) % G);
           if (ins && gl == mp) {
             my_key = kv;
             my_pos = pos;

@@ -662,6 +662,8 @@ a3g_status a3g_trainer_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds, co
       t.d_sort_tmp = dalloc<uint8_t>(t.sort_tmp_bytes);
       t.nparts = static_cast<uint32_t>(t.sm_count);
       t.tc_splits = std::max<uint32_t>(1, static_cast<uint32_t>(t.sm_count) / ((t.F + 127) / 128));
+      t.h1_split_cap = std::min<uint32_t>(8, (t.F + 63) / 64);
+      t.d_hpart = dalloc<float>(static_cast<size_t>(t.h1_split_cap) * t.cap_inner * H);
       t.d_part = dalloc<float>(static_cast<size_t>(std::max(t.nparts, t.tc_splits)) * t.F * H);
       t.d_agg_bytes = dalloc<unsigned long long>(1);
       A3G_CUDA(cudaMemset(t.d_agg_bytes, 0, 8));
@@ -717,6 +719,7 @@ void a3g_trainer_destroy(a3g_trainer* tr) {
   }
   if (t.d_sort_tmp) cudaFree(t.d_sort_tmp);
   dfree(t.d_part);
+  dfree(t.d_hpart);
   dfree(t.d_agg_bytes);
   dfree(t.d_losses);
   dfree(t.d_stats);

@@ -21,13 +21,16 @@
 // with tcgen05.ld (warp w owns lanes 32w..32w+31).
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include "ptx.cuh"
 #include "trainer.cuh"
 
 namespace a3g {
 namespace {
 
-constexpr int kTcThreads = 128;
+constexpr int kTcThreads = 256;  // 8 warps: conversion throughput; warps 0-3 own the TMEM lanes
+constexpr int kPerThr = 2048 / kTcThreads;  // float4 of a 128 x 64 (or 64 x 128) block per thread
 constexpr uint32_t kCore = 128;  // bytes per core matrix (8 rows x 16 B)
 
 // ---------------------------------------------------------------- PTX ------
@@ -137,6 +140,9 @@ struct TcArgs {
   float* part;           // k_dw1_tc: nsplit x F x H partial dW1
   uint32_t k_pad;        // k_h1_tc: F rounded up to 64
   uint32_t rows_per_split;
+  uint32_t kb_per_split; // k_h1_tc: K blocks per split (gridDim.y splits)
+  float* hpart;          // k_h1_tc with > 1 split: [split][rows][H] pre-ReLU partials
+  uint32_t part_rows;    // row capacity of hpart
 };
 
 // cp.async (LDGSTS) 16 B global -> shared; src_size 0 zero-fills (the source
@@ -183,7 +189,7 @@ __global__ void __launch_bounds__(kTcThreads) k_h1_tc(const __grid_constant__ Tc
   auto issue = [&](uint32_t kb) {
     float* dst = stg + (kb & 1) * (kStgBytes / 4);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < kPerThr; ++j) {
       const uint32_t i = tid + j * kTcThreads, rr = i >> 4, c = (i & 15) * 4;
       const uint32_t row = r0 + rr, col = kb * 64 + c;
       const bool ok = row < n && col < a.pitch;
@@ -191,25 +197,29 @@ __global__ void __launch_bounds__(kTcThreads) k_h1_tc(const __grid_constant__ Tc
     }
     cp_async_commit();
   };
-  issue(0);
+  // split-K: this CTA's K blocks [kb0, kb0 + nkb); local index t drives the
+  // double buffer and the mbarrier phases
+  const uint32_t kb0 = blockIdx.y * a.kb_per_split;
+  const uint32_t nkb = min(a.k_pad / 64 - kb0, a.kb_per_split);
+  issue(kb0);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
   const uint32_t idesc = idesc_bf16(a.HN, false, false);
-  const uint32_t nkb = a.k_pad / 64;
-  for (uint32_t kb = 0; kb < nkb; ++kb) {
-    if (kb + 1 < nkb) {
+  for (uint32_t t = 0; t < nkb; ++t) {
+    const uint32_t kb = kb0 + t;
+    if (t + 1 < nkb) {
       issue(kb + 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
-    __syncthreads();                                  // block kb staged by every thread
-    if (kb >= 1) ptx::mbar_wait(&bar, (kb - 1) & 1);  // MMAs of kb-1 done reading the terms
+    __syncthreads();                                // block t staged by every thread
+    if (t >= 1) ptx::mbar_wait(&bar, (t - 1) & 1);  // MMAs of t-1 done reading the terms
     const float* src = stg + (kb & 1) * (kStgBytes / 4);
 #pragma unroll 4
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < kPerThr; ++j) {
       const uint32_t i = tid + j * kTcThreads, rr = i >> 4, c = (i & 15) * 4;
       put4(apart, kPartBytes, rr, c, kCore, 16 * kCore, *reinterpret_cast<const float4*>(src + rr * 64 + c));
     }
@@ -232,7 +242,7 @@ __global__ void __launch_bounds__(kTcThreads) k_h1_tc(const __grid_constant__ Tc
           aa[i] = ptx::smem_u32(apart + i * kPartBytes) + s * 2 * 16 * kCore;
           bb[i] = ptx::smem_u32(bpart + i * b_part) + s * 2 * b_cs;
         }
-        mma_step6(tmem, aa, bb, 16 * kCore, kCore, b_cs, kCore, idesc, (kb | s) == 0);
+        mma_step6(tmem, aa, bb, 16 * kCore, kCore, b_cs, kCore, idesc, (t | s) == 0);
       }
       mma_commit(&bar);
     }
@@ -241,13 +251,15 @@ __global__ void __launch_bounds__(kTcThreads) k_h1_tc(const __grid_constant__ Tc
   ptx::mbar_wait(&bar, (nkb - 1) & 1);
   tc_fence_after();
   const uint32_t row = r0 + warp * 32 + lane;
-  for (uint32_t c0 = 0; c0 < a.HN; c0 += 16) {
+  const bool split = gridDim.y > 1;
+  float* out = split ? a.hpart + (static_cast<uint64_t>(blockIdx.y) * a.part_rows) * a.H : a.h1;
+  for (uint32_t c0 = 0; warp < 4 && c0 < a.HN; c0 += 16) {
     float v[16];
     tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
     if (row < n)
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        if (c0 + j < a.H) a.h1[static_cast<uint64_t>(row) * a.H + c0 + j] = fmaxf(v[j], 0.f);
+        if (c0 + j < a.H) out[static_cast<uint64_t>(row) * a.H + c0 + j] = split ? v[j] : fmaxf(v[j], 0.f);
   }
   tc_fence_before();
   __syncthreads();
@@ -295,7 +307,7 @@ __global__ void __launch_bounds__(kTcThreads) k_dw1_tc(const __grid_constant__ T
     const uint32_t kr0 = rb + kb * 64;
     float* dst = stg + (kb & 1) * (kStgBytes / 4);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < kPerThr; ++j) {
       const uint32_t i = tid + j * kTcThreads, rr = i >> 5, c = (i & 31) * 4;
       const uint32_t row = kr0 + rr, f = f0 + c;
       const bool ok = row < re && f < a.pitch;
@@ -331,7 +343,7 @@ __global__ void __launch_bounds__(kTcThreads) k_dw1_tc(const __grid_constant__ T
     if (kb >= 1) ptx::mbar_wait(&bar, (kb - 1) & 1);
     const float* src = stg + (kb & 1) * (kStgBytes / 4);
 #pragma unroll 4
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < kPerThr; ++j) {
       const uint32_t i = tid + j * kTcThreads, rr = i >> 5, c = (i & 31) * 4;
       put4(apart, kPartBytes, rr, c, 16 * kCore, kCore, *reinterpret_cast<const float4*>(src + rr * 128 + c));
     }
@@ -369,7 +381,7 @@ __global__ void __launch_bounds__(kTcThreads) k_dw1_tc(const __grid_constant__ T
   ptx::mbar_wait(&bar, (nkb - 1) & 1);
   tc_fence_after();
   const uint32_t f = f0 + warp * 32 + lane;
-  for (uint32_t c0 = 0; c0 < a.HN; c0 += 16) {
+  for (uint32_t c0 = 0; warp < 4 && c0 < a.HN; c0 += 16) {
     float v[16];
     tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
     if (f < a.F)
@@ -380,6 +392,19 @@ __global__ void __launch_bounds__(kTcThreads) k_dw1_tc(const __grid_constant__ T
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc(tmem, 32);
+}
+
+// h1 = ReLU(sum of the split-K partials), in split order (deterministic).
+__global__ void k_h1_reduce(const float* hpart, uint32_t nsplit, uint32_t part_rows, const uint32_t* n_inner,
+                            uint32_t H, float* h1) {
+  const uint64_t total = static_cast<uint64_t>(*n_inner) * H;
+  const uint64_t stride = static_cast<uint64_t>(part_rows) * H;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    float v = 0.f;
+    for (uint32_t k = 0; k < nsplit; ++k) v += hpart[k * stride + i];
+    h1[i] = fmaxf(v, 0.f);
+  }
 }
 
 }  // namespace
@@ -404,11 +429,23 @@ void launch_h1_tc(const TrainerState& t, const float* agg, const uint32_t* n_inn
   a.w1 = t.d_w1;
   a.h1 = h1;
   a.k_pad = (t.F + 63) / 64 * 64;
+  // split K so the grid covers ~4 CTAs per SM (the row tiles alone are < 1 wave)
+  const uint32_t tiles = static_cast<uint32_t>((t.cap_inner + 127) / 128);
+  const uint32_t nkb = a.k_pad / 64;
+  uint32_t ksplit = std::min<uint32_t>(std::min<uint32_t>(nkb, t.h1_split_cap),
+                                       std::max<uint32_t>(1, (4u * t.sm_count + tiles - 1) / tiles));
+  a.kb_per_split = (nkb + ksplit - 1) / ksplit;
+  ksplit = (nkb + a.kb_per_split - 1) / a.kb_per_split;
+  a.hpart = t.d_hpart;
+  a.part_rows = static_cast<uint32_t>(t.cap_inner);
   const size_t smem = tc_h1_smem(t.F, t.H);
   A3G_CUDA(cudaFuncSetAttribute(k_h1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  const uint32_t grid = static_cast<uint32_t>((t.cap_inner + 127) / 128);
-  k_h1_tc<<<grid, kTcThreads, smem, st>>>(a);
+  k_h1_tc<<<dim3(tiles, ksplit), kTcThreads, smem, st>>>(a);
   A3G_LAUNCH_CHECK("k_h1_tc");
+  if (ksplit > 1) {
+    k_h1_reduce<<<t.sm_count * 2, 256, 0, st>>>(t.d_hpart, ksplit, a.part_rows, n_inner, t.H, h1);
+    A3G_LAUNCH_CHECK("k_h1_reduce");
+  }
 }
 
 void launch_dw1_tc(const TrainerState& t, const float* agg, const uint32_t* n_inner, const float* h1,

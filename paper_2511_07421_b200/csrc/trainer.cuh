@@ -50,6 +50,8 @@ struct TrainerState {
   a3g_comm* comm = nullptr;
   int sm_count = 148;
   uint32_t tc_splits = 1;   // row splits of the dW1 tcgen05 GEMM (partials in d_part)
+  float* d_hpart = nullptr; // split-K partials of the h1 GEMM [h1_split_cap][cap_inner][H]
+  uint32_t h1_split_cap = 1;
 };
 
 // Compute part of one step on s_comp for the batch in arena `smp`

@@ -38,7 +38,13 @@ CONFIGS = {
     "c3": (2_450_000, 9, 100, [15, 10, 5], 4096, 0.2,
            "ogbn-products-shaped synthetic 2.45M nodes / 65M edges, 100-d f32, fanout [15,10,5], batch 4096/GPU, "
            "20% cache"),
+    # papers-scale: topology from the host generator at feat_dim 1, the 128-d
+    # features synthesized on the device in bf16 (a3g_graph_synthesize_features)
+    "c5": (111_000_000, 5, 128, [15, 10, 5], 8192, 0.2,
+           "ogbn-papers100M-shaped synthetic 111M nodes / 1.6B edges, 128-d bf16 (device-synthesized), "
+           "fanout [15,10,5], batch 8192/GPU, 20% cache bias, whole table in HBM"),
 }
+SYNTH = {"c5"}  # configs whose features are synthesized on the device (bf16)
 HIDDEN, CLASSES, LR, BASE_SEED = 16, 4, 0.2, 1
 
 
@@ -121,7 +127,7 @@ class ClockSampler:
 def make_graph(cfg_name):
     from paper_2511_07421_b200 import graph as G
     n, m, F, fan, B, frac, _ = CONFIGS[cfg_name]
-    return G.generate_power_law(n, m, 2.5, F, BASE_SEED)
+    return G.generate_power_law(n, m, 2.5, 1 if cfg_name in SYNTH else F, BASE_SEED)
 
 
 def cpu_reference_run(g, cfg_name, gamma, units, producers, tmpdir="/tmp"):
@@ -183,8 +189,11 @@ def run_ours(args):
     t0 = time.time()
     g = make_graph(args.config)
     gen_s = time.time() - t0
-    cache = CA.build_static_cache(g, CA.CacheConfig(int(frac * n) * F * 4 // 1, 1), device=local)
-    tr = T.Trainer(g, cache, T.ModelSpec(F, HIDDEN, CLASSES, learning_rate=LR), fan, max_seeds=B, device=local)
+    synth = args.config in SYNTH
+    Fh = 1 if synth else F  # host feat_dim (the cache's node_cost, cache.cpp:20, scales the same set)
+    cache = CA.build_static_cache(g, CA.CacheConfig(int(frac * n) * Fh * 4, 1), device=local)
+    tr = T.Trainer(g, cache, T.ModelSpec(F, HIDDEN, CLASSES, learning_rate=LR), fan, max_seeds=B, device=local,
+                   feat_dtype=1 if synth else 0, synth_seed=BASE_SEED if synth else None)
     comm = None
     if world > 1:
         import torch.distributed as dist
@@ -245,12 +254,13 @@ def run_ours(args):
     out = {
         "metric": "trained seed nodes/sec", "value": value, "unit": "seeds/s", "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": dev_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic (generate_power_law, bit-identical to the reference generator)",
+        "dtype": "bf16" if args.config in SYNTH else "f32", "data": "synthetic (generate_power_law, bit-identical to the reference generator)",
         "config": {"workload": args.config, "description": desc, "global_batch": world * B, "batch_per_gpu": B,
                    "fanouts": fan, "gamma": args.gamma, "model": "2-layer mean-GCN (reference trainer), H=16, C=4",
                    "hidden": HIDDEN, "classes": CLASSES, "parallelism": f"dp{world}",
                    "l2": "inputs larger than L2 (CSR %.0f MB + features %.0f MB)" % (
-                       g.num_edges * 4 / 1e6, n * F * 4 / 1e6), "graph_gen_s": round(gen_s, 1)},
+                       g.num_edges * 4 / 1e6, n * F * (2 if args.config in SYNTH else 4) / 1e6),
+                   "graph_gen_s": round(gen_s, 1)},
         "roofline": {"kernel": "k_agg1 (fused gather + mean aggregation + W1 update)", "bound": "hbm",
                      "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "bytes_per_launch": agg_bytes,
@@ -260,7 +270,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "loss_first_last": [float(losses[0]), float(losses_e2e[-1])],
     }
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline and world == 1 and args.config not in SYNTH:
         r = cpu_reference_run(g, args.config, args.gamma, args.cpu_units, 0)
         if r:
             out["cpu_baseline"] = {"value": r["seeds_per_s"], "unit": "seeds/s", "cores": 1, "kind": "reference",

@@ -104,6 +104,12 @@ a3g_status a3g_graph_create(int device, uint64_t num_nodes, uint64_t num_edges, 
                             const float* features, int feat_dtype, const uint32_t* labels,
                             a3g_graph** out);
 void a3g_graph_destroy(a3g_graph* g);
+/* Papers-scale inputs (BASELINE config 5): fill the device feature table of a
+ * graph created without features, with the power-law generator's features
+ * (generators.cpp:12-24: Gaussian noise of substream 0xfea7 + one-hot label)
+ * synthesized on the device at feat_dim, stored as feat_dtype. The topology,
+ * labels and masks come from a3g_host_graph_power_law at feat_dim 1. */
+a3g_status a3g_graph_synthesize_features(a3g_graph* g, uint32_t feat_dim, int feat_dtype, uint64_t seed);
 
 /* --------------------------------------------------------------- store --- */
 /* Places the feature rows of `g` by `policy` (A3G_STORE_*) from host f32

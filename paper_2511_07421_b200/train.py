@@ -103,11 +103,14 @@ class Trainer:
     """Device-resident 2-layer mean-GCN trainer (trainer.hpp:24-60, 63-83)."""
 
     def __init__(self, g: Graph, cache: CacheState, spec: ModelSpec, fanouts, max_seeds: int,
-                 model_seed: int = 1, device: int = 0, feat_dtype: int = 0, placement=None):
+                 model_seed: int = 1, device: int = 0, feat_dtype: int = 0, placement=None, synth_seed=None):
         """placement: None (whole feature table in HBM) or dict(policy=STORE_*,
         rank=0, nranks=1) -- feature rows placed by the tiered store from the
-        cache's device_map (graph.Store)."""
-        if spec.feat_dim != g.feat_dim:
+        cache's device_map (graph.Store). synth_seed: papers-scale inputs --
+        the host graph carries topology/labels only (feat_dim 1) and the
+        spec.feat_dim features are synthesized on the device
+        (a3g_graph_synthesize_features, the generator's formula)."""
+        if synth_seed is None and spec.feat_dim != g.feat_dim:
             raise ParameterError("trainer: spec.feat_dim != graph feat_dim")
         self.g, self.cache, self.spec = g, cache, spec
         self.fanouts = [int(x) for x in fanouts]
@@ -115,7 +118,17 @@ class Trainer:
             raise ParameterError("sample_khop: fanout must be >= 1")
         f = np.asarray(self.fanouts, dtype=np.uint32)
         self.store = None
-        if placement is None:
+        if synth_seed is not None:
+            dg = DeviceGraph(g, device, feat_dtype, upload_features=False)
+            check(lib().a3g_graph_synthesize_features(dg.h, spec.feat_dim, feat_dtype, int(synth_seed)))
+            from .cache import _DeviceCache
+            hc = vp()
+            dm = np.ascontiguousarray(cache.device_map, dtype=np.int32)
+            check(lib().a3g_cache_from_map(dg.h, ptr(dm, i32p), cache.num_devices, C.byref(hc)))
+            dc = _DeviceCache(hc)
+            ch = dc.h
+            keep = [dc, dg]
+        elif placement is None:
             dg = g.device(device, feat_dtype)
             ch = cache.device(g, device, feat_dtype)
             keep = [dg]

@@ -201,3 +201,32 @@ def test_nccl_gradient_sync_world1(c1):
     assert rel_err(b1, a1) < 1e-6 and rel_err(b2, a2) < 1e-6
     b.set_comm(None)
     del comm
+
+
+@pytest.mark.parametrize("feat_dtype", [0, 1])
+def test_device_feature_synthesis_matches_generator(feat_dtype):
+    """Papers-scale inputs: features synthesized on the device from the
+    generator's streams (generators.cpp:12-24) equal the host generator's
+    (bf16: after the same RNE rounding), up to rare 1-ulp libm differences."""
+    import ctypes as C
+    from paper_2511_07421_b200._lib import check, f32p, lib, ptr, u32p, vp
+    n, F = 20000, 24
+    full = G.generate_power_law(n, 3, 2.5, F, 7)
+    topo = G.generate_power_law(n, 3, 2.5, 1, 7)
+    assert np.array_equal(full.col_indices, topo.col_indices) and np.array_equal(full.labels, topo.labels)
+    dg = G.DeviceGraph(topo, 0, feat_dtype, upload_features=False)
+    check(lib().a3g_graph_synthesize_features(dg.h, F, feat_dtype, 7))
+    hc = vp()
+    check(lib().a3g_cache_from_map(dg.h, None, 1, C.byref(hc)))
+    ids = np.arange(n, dtype=np.uint32)
+    out = np.empty((n, F), np.float32)
+    h, m = C.c_uint64(), C.c_uint64()
+    check(lib().a3g_gather_rows(dg.h, hc, ptr(ids, u32p), n, ptr(out, f32p), C.byref(h), C.byref(m)))
+    lib().a3g_cache_destroy(hc)
+    want = full.features
+    if feat_dtype == 1:
+        u = want.view(np.uint32).astype(np.uint64)
+        want = (((u + 0x7fff + ((u >> 16) & 1)) >> 16) << 16).astype(np.uint32).view(np.float32)
+    diff = out != want
+    assert diff.mean() < 1e-5, diff.sum()
+    np.testing.assert_allclose(out, want, rtol=1e-2 if feat_dtype else 1e-6, atol=1e-6)

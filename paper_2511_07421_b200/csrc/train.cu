@@ -92,15 +92,20 @@ __device__ __forceinline__ void ldgsts_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <typename T, int NCH, int WARPS, int S>
+template <typename T, int NCH, int WARPS, int S, int LPR>
 __global__ void __launch_bounds__(WARPS * 32, 1) k_agg1(const __grid_constant__ AggArgs a) {
+  // LPR lanes per source row: short rows (<= 16 chunks) are copied RPI at a
+  // time by lane groups; each group sums its own rows, the groups' partial
+  // sums are added at the end of an inner row (fixed order: deterministic)
   using Ch = Chunk<T>;
   constexpr int EPC = Ch::EPC;
+  constexpr int RPI = 32 / LPR;
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t g = lane / LPR, gl = lane % LPR;
   const uint32_t rb = a.view.row_bytes;
-  const uint32_t ring = ptx::smem_u32(smem) + static_cast<uint32_t>(warp) * S * rb;
-  const uint8_t* ring_p = smem + static_cast<size_t>(warp) * S * rb;
+  const uint32_t ring = ptx::smem_u32(smem) + static_cast<uint32_t>(warp) * S * RPI * rb;
+  const uint8_t* ring_p = smem + static_cast<size_t>(warp) * S * RPI * rb;
   const uint32_t n_inner = *a.n_inner;
   const uint32_t chunks = a.pitch / EPC;  // 16-byte chunks per row
   const uint32_t gw = blockIdx.x * WARPS + warp, nw = gridDim.x * WARPS;
@@ -108,12 +113,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_agg1(const __grid_constant__ 
   unsigned long long nbytes = 0;
   // producer: row j, source t; lanes hold the (layer row, count) of rows
   // 32*batch + lane and the current row's source ids; lane s holds the
-  // (row, count, last) record of ring slot s for the consumer
+  // (row, count|last, groups) record of ring slot s for the consumer
   uint32_t pj = 0, pt = 0, pc = 0, batch = ~0u, src_lane = 0;
   int32_t meta_k = -1, pk = -1;
   uint32_t meta_c = 0;
   bool row_ready = false;
-  uint32_t slot_row = 0, slot_c = 0;
+  uint32_t slot_row = 0, slot_c = 0, slot_n = 0;
   uint32_t issued = 0, consumed = 0;
   float acc[NCH][EPC];
 #pragma unroll
@@ -141,22 +146,28 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_agg1(const __grid_constant__ 
         nbytes += pc ? static_cast<unsigned long long>(pc) * 4 + 8 : static_cast<unsigned long long>(a.F) * sizeof(T) + 4;
         row_ready = true;
       }
-      uint32_t v = __shfl_sync(kFull, src_lane, pt & 31);
+      const uint32_t total = pc ? pc : 1u;           // sources of this row (fallback: own row)
+      const uint32_t ngrp = min(static_cast<uint32_t>(RPI), total - pt);
+      const uint32_t t = pt + g;
+      uint32_t v = __shfl_sync(kFull, src_lane, t & 31);
       if (pc == 0) v = __ldg(a.unique + r);  // self-fallback: own features (trainer.cpp:102-107)
-      else if (pt >= 32) v = __ldg(a.S1 + static_cast<uint64_t>(pk) * a.f1 + pt);  // fanout > 32
+      else if (t >= 32 && t < pc) v = __ldg(a.S1 + static_cast<uint64_t>(pk) * a.f1 + t);  // fanout > 32
       const uint32_t slot = issued % S;
-      const bool last = pt + 1 >= (pc ? pc : 1u);
-      const uint8_t* src = row_ptr(a.view, v);
-      const uint32_t dst = ring + slot * rb;
+      const bool last = pt + ngrp >= total;
+      if (g < ngrp) {
+        const uint8_t* src = row_ptr(a.view, v);
+        const uint32_t dst = ring + (slot * RPI + g) * rb;
 #pragma unroll
-      for (int i = 0; i < NCH; ++i) {
-        const uint32_t q = lane + 32 * i;
-        if (q < chunks) ldgsts16(dst + q * 16, src + q * 16);
+        for (int i = 0; i < NCH; ++i) {
+          const uint32_t q = gl + LPR * i;
+          if (q < chunks) ldgsts16(dst + q * 16, src + q * 16);
+        }
       }
       ldgsts_commit();
       if (lane == static_cast<int>(slot)) {
         slot_row = r;
         slot_c = pc | (last ? 0x80000000u : 0u);
+        slot_n = ngrp;
       }
       ++issued;
       if (last) {
@@ -164,33 +175,44 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_agg1(const __grid_constant__ 
         pt = 0;
         row_ready = false;
       } else {
-        ++pt;
+        pt += ngrp;
       }
     }
     if (consumed == issued) break;
-    // ---- consumer: the oldest source row (this lane's chunks of it)
+    // ---- consumer: the oldest slot (this lane's chunks of its group's row)
     if (issued - consumed == S)
       ldgsts_wait<S - 1>();
     else
       ldgsts_wait<0>();
     const uint32_t slot = consumed % S;
-    const uint4* row = reinterpret_cast<const uint4*>(ring_p + static_cast<size_t>(slot) * rb);
+    const uint32_t sn = __shfl_sync(kFull, slot_n, slot);
+    if (g < sn) {
+      const uint4* row = reinterpret_cast<const uint4*>(ring_p + static_cast<size_t>(slot * RPI + g) * rb);
 #pragma unroll
-    for (int i = 0; i < NCH; ++i) {
-      const uint32_t q = lane + 32 * i;
-      if (q < chunks) Ch::add(acc[i], row[q]);
+      for (int i = 0; i < NCH; ++i) {
+        const uint32_t q = gl + LPR * i;
+        if (q < chunks) Ch::add(acc[i], row[q]);
+      }
     }
     const uint32_t srow = __shfl_sync(kFull, slot_row, slot);
     const uint32_t sc = __shfl_sync(kFull, slot_c, slot);
     ++consumed;
     if (sc & 0x80000000u) {
+      if (RPI > 1) {
+#pragma unroll
+        for (int off = LPR; off < 32; off <<= 1)
+#pragma unroll
+          for (int i = 0; i < NCH; ++i)
+#pragma unroll
+            for (int e = 0; e < EPC; ++e) acc[i][e] += __shfl_xor_sync(kFull, acc[i][e], off);
+      }
       const uint32_t c = sc & 0x7fffffffu;
       const float scale = c ? 1.f / static_cast<float>(c) : 1.f;
       float4* out = reinterpret_cast<float4*>(a.agg_inner + static_cast<uint64_t>(srow) * a.pitch);
 #pragma unroll
       for (int i = 0; i < NCH; ++i) {
-        const uint32_t q = lane + 32 * i;
-        if (q < chunks) {
+        const uint32_t q = gl + LPR * i;
+        if (g == 0 && q < chunks) {
 #pragma unroll
           for (int e = 0; e < EPC; e += 4)
             out[q * (EPC / 4) + e / 4] = make_float4(acc[i][e] * scale, acc[i][e + 1] * scale,
@@ -425,50 +447,55 @@ __global__ void k_sgd(float* w1, float* w2, float* gw, uint32_t FH, uint32_t HC,
   if (blockIdx.x == 0 && threadIdx.x == 0 && loss_slot) *loss_slot = static_cast<double>(gw[FH + HC + 1]) / n;
 }
 
-template <typename T, int N, int W, int S>
+template <typename T, int N, int W, int S, int LPR>
 void launch_agg_cfg(TrainerState& t, const AggArgs& aa, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(W) * S * aa.view.row_bytes;
+  const size_t smem = static_cast<size_t>(W) * S * (32 / LPR) * aa.view.row_bytes;
   if (smem > 227 * 1024) raise(A3G_ERR_PARAMETER, "feature row too wide for k_agg1's shared-memory ring");
   const int grid = t.sm_count * (smem * 2 <= 227 * 1024 && W <= 32 ? 2 : 1);
-  A3G_CUDA(cudaFuncSetAttribute(k_agg1<T, N, W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  A3G_CUDA(cudaFuncSetAttribute(k_agg1<T, N, W, S, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
-  k_agg1<T, N, W, S><<<grid, W * 32, smem, st>>>(aa);
+  k_agg1<T, N, W, S, LPR><<<grid, W * 32, smem, st>>>(aa);
 }
 
 // 24 warps per CTA (more warps beat a deeper ring: r01 sweep 8x8 63 us,
 // 16x4 53 us, 24x3 51 us on C2); ring depth from the row size.
-template <typename T, int N>
+template <typename T, int N, int LPR>
 void launch_agg_n(TrainerState& t, const AggArgs& aa, cudaStream_t st) {
-  const uint64_t per_slot = 24ull * aa.view.row_bytes;
+  const uint64_t per_slot = 24ull * (32 / LPR) * aa.view.row_bytes;
   if (per_slot * 8 <= 176 * 1024)
-    launch_agg_cfg<T, N, 24, 8>(t, aa, st);
+    launch_agg_cfg<T, N, 24, 8, LPR>(t, aa, st);
   else if (per_slot * 6 <= 176 * 1024)
-    launch_agg_cfg<T, N, 24, 6>(t, aa, st);
+    launch_agg_cfg<T, N, 24, 6, LPR>(t, aa, st);
   else if (per_slot * 4 <= 176 * 1024)
-    launch_agg_cfg<T, N, 24, 4>(t, aa, st);
+    launch_agg_cfg<T, N, 24, 4, LPR>(t, aa, st);
   else
-    launch_agg_cfg<T, N, 24, 3>(t, aa, st);
+    launch_agg_cfg<T, N, 24, 3, LPR>(t, aa, st);
 }
 
+// rows of <= 16 chunks (16 B) go 4 rows per warp step (LPR 8): short rows
+// are issue-bound, not bandwidth-bound
 template <typename T>
-void launch_agg(TrainerState& t, AggArgs aa, int nch, cudaStream_t st) {
-#define A3G_AGG_CASE(N)                  \
-  case N:                                \
-    launch_agg_n<T, N>(t, aa, st);       \
-    break;
-  switch (nch) {
-    A3G_AGG_CASE(1)
-    A3G_AGG_CASE(2)
-    A3G_AGG_CASE(3)
-    A3G_AGG_CASE(4)
-    A3G_AGG_CASE(5)
-    A3G_AGG_CASE(6)
-    A3G_AGG_CASE(8)
-    A3G_AGG_CASE(16)
-    default:
-      raise(A3G_ERR_PARAMETER, "feature row too wide for k_agg1");
+void launch_agg(TrainerState& t, AggArgs aa, uint32_t chunks, cudaStream_t st) {
+  if (chunks <= 8) {
+    launch_agg_n<T, 1, 8>(t, aa, st);
+  } else if (chunks <= 16) {
+    launch_agg_n<T, 2, 8>(t, aa, st);
+  } else {
+    switch ((chunks + 31) / 32) {
+      case 1: launch_agg_n<T, 1, 32>(t, aa, st); break;
+      case 2: launch_agg_n<T, 2, 32>(t, aa, st); break;
+      case 3: launch_agg_n<T, 3, 32>(t, aa, st); break;
+      case 4: launch_agg_n<T, 4, 32>(t, aa, st); break;
+      case 5: launch_agg_n<T, 5, 32>(t, aa, st); break;
+      case 6: launch_agg_n<T, 6, 32>(t, aa, st); break;
+      case 7: case 8: launch_agg_n<T, 8, 32>(t, aa, st); break;
+      case 9: case 10: case 11: case 12: case 13: case 14: case 15: case 16:
+        launch_agg_n<T, 16, 32>(t, aa, st);
+        break;
+      default:
+        raise(A3G_ERR_PARAMETER, "feature row too wide for k_agg1");
+    }
   }
-#undef A3G_AGG_CASE
   A3G_LAUNCH_CHECK("k_agg1");
 }
 
@@ -511,13 +538,10 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
     A3G_CUDA(cudaEventCreate(&e1));
     A3G_CUDA(cudaEventRecord(e0, st));
   }
-  if (g->feat_dtype == A3G_FEAT_BF16) {
-    const int nch = static_cast<int>((g->pitch / 8 + 31) / 32);
-    launch_agg<uint16_t>(t, aa, nch == 7 ? 8 : (nch > 8 && nch <= 16 ? 16 : nch), st);
-  } else {
-    const int nch = static_cast<int>((g->pitch / 4 + 31) / 32);
-    launch_agg<float>(t, aa, nch == 7 ? 8 : (nch > 8 && nch <= 16 ? 16 : nch), st);
-  }
+  if (g->feat_dtype == A3G_FEAT_BF16)
+    launch_agg<uint16_t>(t, aa, g->pitch / 8, st);
+  else
+    launch_agg<float>(t, aa, g->pitch / 4, st);
   if (record_timing) {
     A3G_CUDA(cudaEventRecord(e1, st));
     t.ev_agg.push_back(e0);

@@ -623,13 +623,14 @@ __global__ void __launch_bounds__(256) k_stream_int(SampleArgs a) {
 // are K-monotone, so only another slot within the policy's tie window of the
 // minimum can share its K value -- then (rare) the exact K-order decides
 // (PolGammaAll; PolUnit keys are exact integers).
-template <int G, typename P>
+template <int G, typename P, int SHIFT = 21>
 __device__ __forceinline__ void grp_argmin(const P& pol, uint64_t my, uint32_t gl, uint64_t& thr, uint32_t& mp) {
   // fast path: butterfly on the packed (top 32 key bits, slot) -- one 64-bit
   // min per step; exact whenever no other slot shares the minimum's top bits
   // (or, for K-ties, the next value): keys differing only below bit 21 are the
   // sole ambiguity, and every K-tie window (<= 64 (gamma + 1) << 2^21) lies there
-  const uint32_t my32 = static_cast<uint32_t>(my >> 21);
+  // SHIFT: 21 for 53-bit integer keys, 32 for fp64 bit patterns (exponent on top)
+  const uint32_t my32 = static_cast<uint32_t>(my >> SHIFT);
   uint64_t pk = (static_cast<uint64_t>(my32) << 32) | gl;
 #pragma unroll
   for (int off = G / 2; off > 0; off >>= 1) pk = min(pk, __shfl_xor_sync(kFull, pk, off, G));
@@ -797,6 +798,143 @@ __global__ void __launch_bounds__(256) k_stream_grp(SampleArgs a, const uint32_t
       if (gl == 0) {
         a.hub.rec_cnt[im.w] = rcnt;
         a.hub.tau[im.w] = thr;
+        a.hub.tau_ok[im.w] = (p1 - p0 >= m) ? 1u : 0u;
+      }
+    } else if (gl < m) {
+      const uint32_t id = __ldg(nb + my_pos);
+      a.S[row0 + gl] = id;
+      mark_first(a.first, id, a.tag, static_cast<uint32_t>(row0 + gl));
+      if (gl == 0) a.cnt[im.x] = m;
+    }
+  }
+}
+
+// Bitmap-weighted items (partial cache, gamma > 1: w = gamma if cached else
+// 1, assign_weights sampler.cpp:60-68) by lane groups, as k_stream_grp but
+// with fp64 keys: each position needs its neighbour id (the cached bit), and a
+// cached neighbour's key pow(u, 1/gamma) is evaluated only when
+// u >= thr^gamma (1 - 1e-6) -- below that no <= 2-ulp pow can beat the
+// minimum (reservoir.cuh PolMixed). Keys are >= 0, so their IEEE bits order
+// like the values: the argmin is the packed top-32-bit butterfly with an
+// exact 64-bit fallback on (near-)equal top bits.
+template <int G>
+__global__ void __launch_bounds__(256) k_stream_grp_mixed(SampleArgs a, const uint32_t* order) {
+  constexpr int NG = 32 / G;
+  constexpr int U = 32 / G;
+  constexpr uint64_t kStepG = static_cast<uint64_t>(G) * kPhi;
+  const int lane = threadIdx.x & 31;
+  const uint32_t gl = lane % G, grp = lane / G;
+  const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << (grp * G));
+  const uint32_t nitems = min(*a.item_count, a.hub.item_cap);
+  const uint32_t m = a.f;
+  const double ig = a.inv_gamma, gamma = a.gamma;
+  const uint32_t* bits = a.bits;
+  auto cached = [&](uint32_t v) { return (__ldg(bits + (v >> 5)) >> (v & 31)) & 1u; };
+  const rsv::PolUnit ipol{};  // bit-pattern argmin (keys >= 0)
+  for (;;) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(a.item_work, static_cast<uint32_t>(NG));
+    base = __shfl_sync(kFull, base, 0);
+    if (base >= nitems) break;
+    const uint32_t ii = base + grp;
+    const bool live = ii < nitems;
+    uint4 im = make_uint4(0, 0, 0, kInv);
+    uint32_t dst = 0;
+    uint64_t beg = 0;
+    if (live) {
+      im = a.hub.items[__ldg(order + ii)];
+      dst = __ldg(a.front + im.x);
+      beg = __ldg(a.ro + dst);
+    }
+    const uint32_t* nb = a.col + beg;
+    const uint64_t key = hash2(a.seed, hash2(a.layer, dst));
+    const bool seg = im.w != kInv;
+    const uint64_t row0 = static_cast<uint64_t>(im.x) * m;
+    const uint32_t p0 = im.y, p1 = im.z;
+    const uint32_t nf = live ? min(m, p1 - p0) : 0u;
+    uint64_t my_key = __double_as_longlong(INFINITY);  // key bits
+    uint32_t my_pos = 0;
+    uint32_t* rid = a.hub.rec_id + static_cast<uint64_t>(seg ? im.w : 0) * kRecCap;
+    uint64_t* rkey = a.hub.rec_key + static_cast<uint64_t>(seg ? im.w : 0) * kRecCap;
+    if (gl < nf) {
+      const uint32_t j = p0 + gl;
+      const double u = unit_of(draw(key, static_cast<uint64_t>(j) + 1));
+      const double k = cached(__ldg(nb + j)) ? pow(u, ig) : u;
+      my_key = __double_as_longlong(k);
+      my_pos = j;
+      if (seg) {
+        rid[gl] = j;
+        rkey[gl] = my_key;
+      }
+    }
+    uint64_t thrb;
+    uint32_t mp;
+    grp_argmin<G, rsv::PolUnit, 32>(ipol, my_key, gl, thrb, mp);
+    double thr = __longlong_as_double(thrb);
+    double lo = rsv::gamma_lo(thr, gamma);
+    uint32_t rcnt = nf;
+    const uint32_t jb = p0 + nf;
+    uint32_t len = live && p1 > jb ? p1 - jb : 0u;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) len = max(len, __shfl_xor_sync(kFull, len, off));
+    uint64_t ctr = key + (static_cast<uint64_t>(jb) + gl + 1) * kPhi;
+    for (uint32_t b = 0; b < len; b += 32, ctr += 32 * kPhi) {
+      double kk[U];
+      bool c[U];
+      bool anyc = false;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t j = jb + b + u * G + gl;
+        const bool valid = j < p1;
+        const uint32_t v = valid ? __ldg(nb + j) : 0u;
+        const double uu = unit_of(mix64(ctr + u * kStepG));
+        const bool cw = valid && cached(v);
+        kk[u] = uu;
+        c[u] = valid && (cw ? uu >= lo : uu > thr);
+        if (c[u] && cw) {
+          kk[u] = pow(uu, ig);
+          c[u] = kk[u] > thr;
+        }
+        anyc |= c[u];
+      }
+      if (!__any_sync(kFull, anyc)) continue;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        unsigned mask = __ballot_sync(kFull, c[u] && kk[u] > thr) & gmask;
+        while (__any_sync(kFull, mask != 0)) {
+          const int src = mask ? __ffs(mask) - 1 : lane;
+          const double kv = __shfl_sync(kFull, kk[u], src);
+          const bool ins = mask != 0 && kv > thr;
+          const uint32_t pos = jb + b + u * G + (static_cast<uint32_t>(src) % G);
+          if (ins && gl == mp) {
+            my_key = __double_as_longlong(kv);
+            my_pos = pos;
+          }
+          if (ins && seg && lane == src) {
+            if (rcnt < kRecCap) {
+              rid[rcnt] = pos;
+              rkey[rcnt] = __double_as_longlong(kv);
+            }
+          }
+          if (ins) ++rcnt;
+          uint64_t nthr;
+          uint32_t nmp;
+          grp_argmin<G, rsv::PolUnit, 32>(ipol, my_key, gl, nthr, nmp);
+          if (ins) {
+            thr = __longlong_as_double(nthr);
+            mp = nmp;
+          }
+          if (mask) mask &= ~((2u << src) - 1u);
+          mask &= __ballot_sync(kFull, c[u] && kk[u] > thr) & gmask;
+        }
+      }
+      lo = rsv::gamma_lo(thr, gamma);
+    }
+    if (!live) continue;
+    if (seg) {
+      if (gl == 0) {
+        a.hub.rec_cnt[im.w] = rcnt;
+        a.hub.tau[im.w] = __double_as_longlong(thr);
         a.hub.tau_ok[im.w] = (p1 - p0 >= m) ? 1u : 0u;
       }
     } else if (gl < m) {
@@ -1635,8 +1773,9 @@ void launch_layer_kernels(const SampleArgs& sa, int sm_count, cudaStream_t st) {
                                     static_cast<int>(kMergeSmem)));
       attr_set = true;
     }
-    if (WM != 2 || sa.kind == A3G_SAMPLER_UNIFORM) {
-      // integer keys: thread per item over the length-sorted items
+    {
+      // lane groups over the length-sorted items: integer keys (or Algorithm
+      // R) in k_stream_grp, bitmap weights (fp64 keys) in k_stream_grp_mixed
       const HubArena& hb = sa.hub;
       k_item_keys<<<sm_count * 2, 256, 0, st>>>(hb.items, sa.item_count, hb.item_cap, hb.sort_keys[0],
                                                 hb.sort_vals[0]);
@@ -1647,16 +1786,23 @@ void launch_layer_kernels(const SampleArgs& sa, int sm_count, cudaStream_t st) {
                                                          static_cast<int>(hb.item_cap), 0, 8, st));
       constexpr int W = WM == 2 ? 0 : WM;
       const int grid = sm_count * 8;
-      if (sa.f <= 8)
-        k_stream_grp<W, 8><<<grid, 256, 0, st>>>(sa, hb.sort_vals[1]);
-      else if (sa.f <= 16)
-        k_stream_grp<W, 16><<<grid, 256, 0, st>>>(sa, hb.sort_vals[1]);
-      else
-        k_stream_grp<W, 32><<<grid, 256, 0, st>>>(sa, hb.sort_vals[1]);
-      A3G_LAUNCH_CHECK("k_stream_grp");
-    } else {
-      k_stream<WM><<<sm_count * 3, kStreamWarps * 32, kStreamSmem, st>>>(sa);
-      A3G_LAUNCH_CHECK("k_stream");
+      if (WM == 2 && sa.kind != A3G_SAMPLER_UNIFORM) {
+        if (sa.f <= 8)
+          k_stream_grp_mixed<8><<<grid, 256, 0, st>>>(sa, hb.sort_vals[1]);
+        else if (sa.f <= 16)
+          k_stream_grp_mixed<16><<<grid, 256, 0, st>>>(sa, hb.sort_vals[1]);
+        else
+          k_stream_grp_mixed<32><<<grid, 256, 0, st>>>(sa, hb.sort_vals[1]);
+        A3G_LAUNCH_CHECK("k_stream_grp_mixed");
+      } else {
+        if (sa.f <= 8)
+          k_stream_grp<W, 8><<<grid, 256, 0, st>>>(sa, hb.sort_vals[1]);
+        else if (sa.f <= 16)
+          k_stream_grp<W, 16><<<grid, 256, 0, st>>>(sa, hb.sort_vals[1]);
+        else
+          k_stream_grp<W, 32><<<grid, 256, 0, st>>>(sa, hb.sort_vals[1]);
+        A3G_LAUNCH_CHECK("k_stream_grp");
+      }
     }
     k_hub_merge<WM><<<sm_count * 2, kMergeThreads, kMergeSmem, st>>>(sa);
     A3G_LAUNCH_CHECK("k_hub_merge");

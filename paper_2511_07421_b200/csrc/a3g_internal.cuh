@@ -91,6 +91,7 @@ struct BatchCounters {
   uint32_t iwork[kMaxLayers];       // stream items claimed per layer
   uint32_t hub_big[kMaxLayers];     // hubs with > 8 segments (block merge)
   uint32_t hub_small[kMaxLayers];   // hubs with 1..8 segments (warp merge)
+  uint32_t icls[kMaxLayers][8];     // stream items per length class (k_item_class)
   uint32_t n_seeds;                 // seeds given (incl. duplicates)
   uint32_t hits, misses;            // retrieve_features accounting
   uint32_t pad;

@@ -120,12 +120,7 @@ void sampler_alloc(SamplerState& s, a3g_graph* g, a3g_cache* c, uint32_t max_see
   hb.slot_last = dalloc<uint32_t>(static_cast<size_t>(hb.seg_cap) * 32);
   hb.item_cap = hb.hub_cap + hb.seg_cap;
   hb.items = dalloc<uint4>(hb.item_cap);
-  for (int i = 0; i < 2; ++i) {
-    hb.sort_keys[i] = dalloc<uint32_t>(hb.item_cap);
-    hb.sort_vals[i] = dalloc<uint32_t>(hb.item_cap);
-  }
-  hb.sort_tmp_bytes = item_sort_temp_bytes(hb.item_cap);
-  hb.sort_tmp = dalloc<uint8_t>(hb.sort_tmp_bytes);
+  hb.sort_keys[0] = dalloc<uint32_t>(8ull * hb.item_cap);
   s.d_ctr = dalloc<BatchCounters>(1);
   A3G_CUDA(cudaMallocHost(&s.h_ctr, sizeof(BatchCounters)));
   A3G_CUDA(cudaMallocHost(&s.h_seeds, max_seeds * sizeof(uint32_t)));
@@ -162,12 +157,7 @@ void sampler_free(SamplerState& s) {
   dfree(s.hub.rec_key);
   dfree(s.hub.slot_last);
   dfree(s.hub.items);
-  for (int i = 0; i < 2; ++i) {
-    dfree(s.hub.sort_keys[i]);
-    dfree(s.hub.sort_vals[i]);
-  }
-  if (s.hub.sort_tmp) cudaFree(s.hub.sort_tmp);
-  s.hub.sort_tmp = nullptr;
+  dfree(s.hub.sort_keys[0]);
   dfree(s.d_ctr);
   if (s.h_ctr) cudaFreeHost(s.h_ctr);
   if (s.h_seeds) cudaFreeHost(s.h_seeds);

@@ -13,7 +13,7 @@
 //                   item; deg > kSeg rows ("hubs", up to n-1 neighbours) are
 //                   split into kSeg-long segment items + a merge entry in the
 //                   small (<= 8 segments) or big hub work list.
-//   k_item_keys + one-pass radix sort: items ordered by length (descending).
+//   k_item_class    items bucketed by length class (longest claimed first).
 //   k_stream_grp    integer-key policies (all weights 1 or all gamma, and
 //                   Algorithm R): lane groups of next_pow2(m) lanes, one item
 //                   per group, keys hashed from positions only; candidates
@@ -66,6 +66,7 @@ struct SampleArgs {
   uint32_t* hub_count;
   uint32_t* seg_count;
   uint32_t* big_count;    // hubs with > kMergeFilterWarps segments (k_hub_merge)
+  uint32_t* cls_count;    // [8] stream items per length class (k_item_class)
   uint32_t* small_count;  // hubs with 1..kMergeFilterWarps segments (merge_small_hub)
   uint32_t* item_count;
   uint32_t* item_work;
@@ -605,6 +606,48 @@ __global__ void __launch_bounds__(256) k_stream_int(SampleArgs a) {
   }
 }
 
+// Length classes of the layer's items (class k: lengths in [2^(k+5), 2^(k+6)),
+// 0 below 64, 7 from 4096): per-class index lists built with warp-aggregated
+// atomics. The lane-group stream kernels claim items longest class first, so
+// a warp's groups carry items within 2x of each other's length.
+constexpr int kClasses = 8;
+
+__device__ __forceinline__ uint32_t len_class(uint32_t len) {
+  const int l2 = 31 - __clz(max(len, 1u));
+  return static_cast<uint32_t>(min(max(l2 - 5, 0), kClasses - 1));
+}
+
+__global__ void k_item_class(const uint4* items, const uint32_t* item_count, uint32_t cap, uint32_t* lists,
+                             uint32_t* cls_count) {
+  const uint32_t n = min(*item_count, cap);
+  const int lane = threadIdx.x & 31;
+  for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < n; i0 += gridDim.x * blockDim.x) {
+    const uint32_t i = i0 + threadIdx.x;
+    const bool ok = i < n;
+    const unsigned act = __ballot_sync(kFull, ok);
+    if (!ok) continue;
+    const uint4 it = items[i];
+    const uint32_t c = len_class(it.z - it.y);
+    const unsigned peers = __match_any_sync(act, c);
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(cls_count + c, __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    lists[static_cast<uint64_t>(c) * cap + base + __popc(peers & ((1u << lane) - 1u))] = i;
+  }
+}
+
+// Item of claim index ii: classes walked from the longest down.
+__device__ __forceinline__ uint32_t item_of(const uint32_t* lists, const uint32_t* cls_count, uint32_t cap,
+                                            uint32_t ii) {
+  for (int c = kClasses - 1; c > 0; --c) {
+    const uint32_t n = cls_count[c];
+    if (ii < n) return lists[static_cast<uint64_t>(c) * cap + ii];
+    ii -= n;
+  }
+  return lists[ii];
+}
+
 // ----------------------------------------------------------- stream (group) -
 // Integer-key items (PolUnit / PolGammaAll weights, Algorithm R) processed by
 // lane groups of G = next_pow2(m) lanes: a warp carries 32/G items at once,
@@ -658,7 +701,7 @@ __device__ __forceinline__ void grp_argmin(const P& pol, uint64_t my, uint32_t g
 }
 
 template <int WM, int G>
-__global__ void __launch_bounds__(256) k_stream_grp(SampleArgs a, const uint32_t* order) {
+__global__ void __launch_bounds__(256) k_stream_grp(SampleArgs a, const uint32_t* lists, const uint32_t* cls_count) {
   using P = typename PolOf<WM>::P;
   constexpr int NG = 32 / G;
   constexpr uint64_t kStepG = static_cast<uint64_t>(G) * kPhi;
@@ -679,7 +722,7 @@ __global__ void __launch_bounds__(256) k_stream_grp(SampleArgs a, const uint32_t
     uint32_t dst = 0;
     uint64_t beg = 0;
     if (live) {
-      im = a.hub.items[__ldg(order + ii)];
+      im = a.hub.items[item_of(lists, cls_count, a.hub.item_cap, ii)];
       dst = __ldg(a.front + im.x);
       beg = __ldg(a.ro + dst);
     }
@@ -818,7 +861,8 @@ __global__ void __launch_bounds__(256) k_stream_grp(SampleArgs a, const uint32_t
 // like the values: the argmin is the packed top-32-bit butterfly with an
 // exact 64-bit fallback on (near-)equal top bits.
 template <int G>
-__global__ void __launch_bounds__(256) k_stream_grp_mixed(SampleArgs a, const uint32_t* order) {
+__global__ void __launch_bounds__(256) k_stream_grp_mixed(SampleArgs a, const uint32_t* lists,
+                                                          const uint32_t* cls_count) {
   constexpr int NG = 32 / G;
   constexpr int U = 32 / G;
   constexpr uint64_t kStepG = static_cast<uint64_t>(G) * kPhi;
@@ -842,7 +886,7 @@ __global__ void __launch_bounds__(256) k_stream_grp_mixed(SampleArgs a, const ui
     uint32_t dst = 0;
     uint64_t beg = 0;
     if (live) {
-      im = a.hub.items[__ldg(order + ii)];
+      im = a.hub.items[item_of(lists, cls_count, a.hub.item_cap, ii)];
       dst = __ldg(a.front + im.x);
       beg = __ldg(a.ro + dst);
     }
@@ -943,22 +987,6 @@ __global__ void __launch_bounds__(256) k_stream_grp_mixed(SampleArgs a, const ui
       mark_first(a.first, id, a.tag, static_cast<uint32_t>(row0 + gl));
       if (gl == 0) a.cnt[im.x] = m;
     }
-  }
-}
-
-// Sort keys of the layer's items (length, clamped; 0 = no item) for the
-// descending radix sort that feeds k_stream_thr.
-__global__ void k_item_keys(const uint4* items, const uint32_t* item_count, uint32_t cap, uint32_t* keys,
-                            uint32_t* vals) {
-  const uint32_t n = min(*item_count, cap);
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) {
-    uint32_t len = 0;
-    if (i < n) {  // 255 length buckets of 16 positions: one radix pass
-      const uint4 it = items[i];
-      len = min((it.z - it.y) >> 4, 254u) + 1;
-    }
-    keys[i] = len;
-    vals[i] = i;
   }
 }
 
@@ -1777,30 +1805,27 @@ void launch_layer_kernels(const SampleArgs& sa, int sm_count, cudaStream_t st) {
       // lane groups over the length-sorted items: integer keys (or Algorithm
       // R) in k_stream_grp, bitmap weights (fp64 keys) in k_stream_grp_mixed
       const HubArena& hb = sa.hub;
-      k_item_keys<<<sm_count * 2, 256, 0, st>>>(hb.items, sa.item_count, hb.item_cap, hb.sort_keys[0],
-                                                hb.sort_vals[0]);
-      A3G_LAUNCH_CHECK("k_item_keys");
-      size_t tmp = hb.sort_tmp_bytes;
-      A3G_CUDA(cub::DeviceRadixSort::SortPairsDescending(hb.sort_tmp, tmp, hb.sort_keys[0], hb.sort_keys[1],
-                                                         hb.sort_vals[0], hb.sort_vals[1],
-                                                         static_cast<int>(hb.item_cap), 0, 8, st));
+      k_item_class<<<sm_count * 2, 256, 0, st>>>(hb.items, sa.item_count, hb.item_cap, hb.sort_keys[0],
+                                                 sa.cls_count);
+      A3G_LAUNCH_CHECK("k_item_class");
+      const uint32_t* lists = hb.sort_keys[0];
       constexpr int W = WM == 2 ? 0 : WM;
       const int grid = sm_count * 8;
       if (WM == 2 && sa.kind != A3G_SAMPLER_UNIFORM) {
         if (sa.f <= 8)
-          k_stream_grp_mixed<8><<<grid, 256, 0, st>>>(sa, hb.sort_vals[1]);
+          k_stream_grp_mixed<8><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         else if (sa.f <= 16)
-          k_stream_grp_mixed<16><<<grid, 256, 0, st>>>(sa, hb.sort_vals[1]);
+          k_stream_grp_mixed<16><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         else
-          k_stream_grp_mixed<32><<<grid, 256, 0, st>>>(sa, hb.sort_vals[1]);
+          k_stream_grp_mixed<32><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         A3G_LAUNCH_CHECK("k_stream_grp_mixed");
       } else {
         if (sa.f <= 8)
-          k_stream_grp<W, 8><<<grid, 256, 0, st>>>(sa, hb.sort_vals[1]);
+          k_stream_grp<W, 8><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         else if (sa.f <= 16)
-          k_stream_grp<W, 16><<<grid, 256, 0, st>>>(sa, hb.sort_vals[1]);
+          k_stream_grp<W, 16><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         else
-          k_stream_grp<W, 32><<<grid, 256, 0, st>>>(sa, hb.sort_vals[1]);
+          k_stream_grp<W, 32><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         A3G_LAUNCH_CHECK("k_stream_grp");
       }
     }
@@ -1875,6 +1900,7 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
     sa.hub_count = &ctr->hubs[l];
     sa.seg_count = &ctr->segs[l];
     sa.big_count = &ctr->hub_big[l];
+    sa.cls_count = ctr->icls[l];
     sa.small_count = &ctr->hub_small[l];
     sa.item_count = &ctr->items[l];
     sa.item_work = &ctr->iwork[l];
@@ -1954,14 +1980,3 @@ void launch_reservoir_list(const uint32_t* d_nb, const double* d_w, uint64_t deg
 
 }  // namespace a3g
 
-namespace a3g {
-size_t item_sort_temp_bytes(uint32_t n) {
-  size_t bytes = 0;
-  A3G_CUDA(cub::DeviceRadixSort::SortPairsDescending(static_cast<void*>(nullptr), bytes,
-                                                     static_cast<const uint32_t*>(nullptr),
-                                                     static_cast<uint32_t*>(nullptr),
-                                                     static_cast<const uint32_t*>(nullptr),
-                                                     static_cast<uint32_t*>(nullptr), static_cast<int>(n), 0, 8));
-  return bytes;
-}
-}  // namespace a3g

@@ -40,14 +40,8 @@ struct HubArena {
   uint32_t* slot_last = nullptr; // [seg_cap * 32] uniform kind: last position per slot
   uint32_t item_cap = 0;
   uint4* items = nullptr;        // [item_cap] stream work: (row, begin, end, segment | kInv)
-  uint32_t* sort_keys[2] = {nullptr, nullptr};  // item lengths (descending sort for k_stream_thr)
-  uint32_t* sort_vals[2] = {nullptr, nullptr};  // item indices
-  void* sort_tmp = nullptr;
-  size_t sort_tmp_bytes = 0;
+  uint32_t* sort_keys[2] = {nullptr, nullptr};  // [0]: per-length-class item lists (8 x item_cap)
 };
-
-// CUB temp storage of the item-length sort.
-size_t item_sort_temp_bytes(uint32_t n);
 
 struct SamplerState {
   HubArena hub;

@@ -99,13 +99,14 @@ void sampler_alloc(SamplerState& s, a3g_graph* g, a3g_cache* c, uint32_t max_see
   A3G_CUDA(cudaMemset(s.d_gidx, 0, n * sizeof(uint64_t)));
   s.d_blk = dalloc<uint4>(s.blk_cap);
   // hub-splitting arena: every frontier row could be a hub; the segment pool
-  // covers sum(deg)/kSeg of a layer's hubs up to 64K segments (rows beyond
+  // covers sum(deg)/seg of a layer's hubs up to 64K segments (rows beyond
   // capacity fall back to the in-row warp replay, still exact).
   uint64_t max_rows = 0;
   for (uint32_t l = 0; l < L; ++l) max_rows = std::max<uint64_t>(max_rows, s.layer[l].cap_rows);
   HubArena& hb = s.hub;
   hb.hub_cap = static_cast<uint32_t>(std::max<uint64_t>(1, max_rows));
-  hb.seg_cap = static_cast<uint32_t>(std::min<uint64_t>(65536, std::max<uint64_t>(1, g->m / kSeg + max_rows)));
+  s.seg = g->n && g->m / g->n >= 128 ? 2 * kSegMin : kSegMin;
+  hb.seg_cap = static_cast<uint32_t>(std::min<uint64_t>(65536, std::max<uint64_t>(1, g->m / s.seg + max_rows)));
   hb.row = dalloc<uint32_t>(hb.hub_cap);
   hb.seg0 = dalloc<uint32_t>(hb.hub_cap);
   hb.nseg = dalloc<uint32_t>(hb.hub_cap);

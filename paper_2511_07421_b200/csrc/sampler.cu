@@ -9,17 +9,18 @@
 //
 // Per layer:
 //   k_classify      frontier rows -> work items: deg <= m rows are copied
-//                   (fill only, sampler.cpp:30-33); m < deg <= kSeg rows are one
-//                   item; deg > kSeg rows ("hubs", up to n-1 neighbours) are
-//                   split into kSeg-long segment items + a merge entry in the
+//                   (fill only, sampler.cpp:30-33); m < deg <= seg rows are one
+//                   item; deg > seg rows ("hubs", up to n-1 neighbours) are
+//                   split into seg-long segment items + a merge entry in the
 //                   small (<= 8 segments) or big hub work list.
 //   k_item_class    items bucketed by length class (longest claimed first).
 //   k_stream_grp    integer-key policies (all weights 1 or all gamma, and
 //                   Algorithm R): lane groups of next_pow2(m) lanes, one item
 //                   per group, keys hashed from positions only; candidates
 //                   replayed in order per group (exact slot history).
-//   k_stream        bitmap-weighted keys (partial cache, gamma > 1): warp per
-//                   item over TMA-staged neighbour-id pieces (fp64 keys).
+//   k_stream_grp_mixed  bitmap-weighted keys (partial cache, gamma > 1): the
+//                   same lane groups with fp64 keys (the neighbour id of every
+//                   position decides its weight).
 //   segments        replay locally from an empty reservoir, emitting every
 //                   local insertion ("record", row position + key) and the
 //                   segment's exact m-th largest key tau_s: every global
@@ -74,6 +75,7 @@ struct SampleArgs {
   double gamma, inv_gamma;
   uint64_t tie;
   uint32_t f, layer, tag;
+  uint32_t seg;  // hub segment length (SamplerState::seg)
   int kind;   // A3G_SAMPLER_*
   int wmode;  // 0: all weights 1; 1: all gamma; 2: bitmap
 };
@@ -193,8 +195,8 @@ __device__ __forceinline__ K key_from_bits(uint64_t b) {
 //   deg == 0           no edges, no draws (sampler.cpp:116)
 //   deg <= m           fill only: output = neighbour list (sampler.cpp:30-33)
 //   m > 32 < deg       thread-serial exact replay (rare wide fanouts)
-//   m < deg <= kSeg    one stream item (whole row)
-//   deg > kSeg         hub: ceil(deg/kSeg) segment items + a merge entry
+//   m < deg <= seg     one stream item (whole row)
+//   deg > seg          hub: ceil(deg/seg) segment items + a merge entry
 // Items are appended with one warp-aggregated atomic.
 template <int WM>
 __global__ void __launch_bounds__(256) k_classify(SampleArgs a) {
@@ -235,8 +237,8 @@ __global__ void __launch_bounds__(256) k_classify(SampleArgs a) {
         serial_row(a, a.col + beg, deg, hash2(a.seed, hash2(a.layer, dst)), a.S + row0, a.scratch + row0);
         for (uint32_t t = 0; t < m; ++t) mark_first(a.first, a.S[row0 + t], a.tag, static_cast<uint32_t>(row0 + t));
         a.cnt[k] = m;
-      } else if (deg > kSeg) {
-        nseg = static_cast<uint32_t>((deg + kSeg - 1) / kSeg);
+      } else if (deg > a.seg) {
+        nseg = static_cast<uint32_t>((deg + a.seg - 1) / a.seg);
         h = atomicAdd(a.hub_count, 1u);
         s0 = atomicAdd(a.seg_count, nseg);
         const bool ok = h < a.hub.hub_cap && s0 + static_cast<uint64_t>(nseg) <= a.hub.seg_cap;
@@ -275,333 +277,12 @@ __global__ void __launch_bounds__(256) k_classify(SampleArgs a) {
     uint32_t o = base + incl - n_items;
     if (h != kInv) {
       for (uint32_t i = 0; i < nseg; ++i, ++o) {
-        const uint32_t sb = i * kSeg;
-        const uint32_t se = static_cast<uint32_t>(deg < sb + static_cast<uint64_t>(kSeg) ? deg : sb + kSeg);
+        const uint32_t sb = i * a.seg;
+        const uint32_t se = static_cast<uint32_t>(deg < sb + static_cast<uint64_t>(a.seg) ? deg : sb + a.seg);
         if (o < a.hub.item_cap) a.hub.items[o] = make_uint4(k, sb, se, s0 + i);
       }
     } else if (n_items == 1) {
       if (o < a.hub.item_cap) a.hub.items[o] = make_uint4(k, 0, static_cast<uint32_t>(deg), kInv);
-    }
-  }
-}
-
-// ---------------------------------------------------------------- stream ---
-// Warp-level streaming of items through a shared-memory ring fed by TMA 1-D
-// bulk copies (cp.async.bulk + mbarrier): piece q+kStages is in flight while
-// piece q is replayed, so every warp keeps kStages-1 pieces of neighbour ids
-// in flight instead of stalling on each 32-key chunk.
-constexpr uint32_t kPiece = 512;                 // neighbour ids per piece
-constexpr uint32_t kStages = 4;                  // ring depth per warp
-constexpr uint32_t kPieceBuf = kPiece + 8;       // + 16-byte alignment slack
-constexpr uint32_t kItemsPerClaim = 8;
-constexpr int kStreamWarps = 8;
-constexpr size_t kStreamSmem = static_cast<size_t>(kStreamWarps) * kStages * (kPieceBuf * 4 + 8);
-
-struct PieceMeta {
-  uint32_t it;     // item slot within the claim (lane holding its meta)
-  uint32_t p0, p1; // row positions of the piece
-};
-
-// Piece q of a claim: the item holding it (lanes hold per-item np / exclusive
-// piece prefix / [ia, ib)) and its row positions. Warp-uniform.
-__device__ __forceinline__ PieceMeta piece_meta(uint32_t q, uint32_t np, uint32_t pref_ex, uint32_t ia,
-                                                uint32_t ib) {
-  const unsigned bm = __ballot_sync(kFull, np > 0 && pref_ex <= q);
-  PieceMeta pm;
-  pm.it = 31 - __clz(bm);
-  const uint32_t a0 = __shfl_sync(kFull, ia, pm.it), a1 = __shfl_sync(kFull, ib, pm.it);
-  const uint32_t px = __shfl_sync(kFull, pref_ex, pm.it);
-  pm.p0 = a0 + (q - px) * kPiece;
-  pm.p1 = min(a1, pm.p0 + kPiece);
-  return pm;
-}
-
-// Lane 0 arms stage `st` and issues the TMA bulk copy of piece pm (16-byte
-// aligned window of col[beg + p0, beg + p1)).
-__device__ __forceinline__ void issue_piece(const PieceMeta& pm, uint64_t b0, const uint32_t* col, uint32_t* ring,
-                                            uint64_t* bar, uint32_t st, int lane) {
-  if (lane == 0) {
-    const uint64_t g0 = (b0 + pm.p0) & ~3ull, g1 = (b0 + pm.p1 + 3) & ~3ull;
-    const uint32_t bytes = static_cast<uint32_t>(g1 - g0) * 4;
-    ptx::mbar_arrive_expect_tx(bar + st, bytes);
-    ptx::bulk_g2s(ring + st * kPieceBuf, col + g0, bytes, bar + st);
-  }
-}
-
-template <int WM>
-__global__ void __launch_bounds__(kStreamWarps * 32) k_stream(SampleArgs a) {
-  using P = typename PolOf<WM>::P;
-  using K = typename P::K;
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* ring = reinterpret_cast<uint32_t*>(smem_raw) + static_cast<size_t>(warp) * kStages * kPieceBuf;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + static_cast<size_t>(kStreamWarps) * kStages * kPieceBuf * 4) +
-                  warp * kStages;
-  if (lane == 0) {
-    for (uint32_t s = 0; s < kStages; ++s) ptx::mbar_init(bar + s, 1);
-    ptx::fence_mbar_init();
-  }
-  __syncwarp();
-  const uint32_t nitems = min(*a.item_count, a.hub.item_cap);
-  const uint32_t m = a.f;
-  // claim size: spread small layers over all warps, amortise the atomic on big ones
-  const uint32_t nwarps_total = gridDim.x * kStreamWarps;
-  const uint32_t claim = max(1u, min(kItemsPerClaim, nitems / (4 * nwarps_total)));
-  uint32_t Q = 0;  // pieces consumed by this warp so far (ring position / parity)
-  for (;;) {
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(a.item_work, claim);
-    base = __shfl_sync(kFull, base, 0);
-    if (base >= nitems) break;
-    // lane i < claim holds item i's meta
-    uint4 itm = make_uint4(0, 0, 0, kInv);
-    uint64_t beg = 0, key = 0;
-    uint32_t np = 0;
-    if (lane < static_cast<int>(claim) && base + lane < nitems) {
-      itm = a.hub.items[base + lane];
-      const uint32_t dst = __ldg(a.front + itm.x);
-      beg = __ldg(a.ro + dst);
-      key = hash2(a.seed, hash2(a.layer, dst));
-      np = (itm.z - itm.y + kPiece - 1) / kPiece;
-    }
-    uint32_t pref = np;  // inclusive scan of pieces
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, pref, off);
-      if (lane >= off) pref += y;
-    }
-    const uint32_t NP = __shfl_sync(kFull, pref, 31);
-    const uint32_t pref_ex = pref - np;
-    for (uint32_t q = 0; q < min(NP, kStages); ++q) {
-      const PieceMeta pm = piece_meta(q, np, pref_ex, itm.y, itm.z);
-      issue_piece(pm, __shfl_sync(kFull, beg, pm.it), a.col, ring, bar, (Q + q) % kStages, lane);
-    }
-    rsv::WState<K> wst;
-    P pol = PolOf<WM>::make(a);
-    uint32_t rcnt = 0, ulast = kInv, uid = 0;
-    for (uint32_t q = 0; q < NP; ++q) {
-      const PieceMeta pm = piece_meta(q, np, pref_ex, itm.y, itm.z);
-      const uint4 im = make_uint4(__shfl_sync(kFull, itm.x, pm.it), __shfl_sync(kFull, itm.y, pm.it),
-                                  __shfl_sync(kFull, itm.z, pm.it), __shfl_sync(kFull, itm.w, pm.it));
-      const uint64_t b0 = __shfl_sync(kFull, beg, pm.it);
-      const uint64_t ky = __shfl_sync(kFull, key, pm.it);
-      const uint32_t st = (Q + q) % kStages;
-      ptx::mbar_wait(bar + st, ((Q + q) / kStages) & 1u);
-      // nb[j] == col[beg + j] for j in [p0, p1)
-      const uint32_t* nb = ring + st * kPieceBuf - static_cast<int64_t>(((b0 + pm.p0) & ~3ull) - b0);
-      const bool seg = im.w != kInv;
-      const bool first_piece = pm.p0 == im.y, last_piece = pm.p1 == im.z;
-      uint32_t* rid = nullptr;
-      uint64_t* rkey = nullptr;
-      if (seg) {
-        rid = a.hub.rec_id + static_cast<uint64_t>(im.w) * kRecCap;
-        rkey = a.hub.rec_key + static_cast<uint64_t>(im.w) * kRecCap;
-      }
-      if (a.kind == A3G_SAMPLER_UNIFORM) {
-        if (!seg) {
-          if (first_piece) uid = lane < static_cast<int>(m) ? nb[lane] : 0u;
-          const uint64_t jb = pm.p0 > m ? pm.p0 : static_cast<uint64_t>(m);
-          if (jb < pm.p1) rsv::uniform_range(nb, jb, pm.p1, m, ky, lane, 0, uid);
-        } else {
-          if (first_piece) ulast = kInv;
-          const uint64_t jb = pm.p0 > m ? pm.p0 : static_cast<uint64_t>(m);
-          for (uint64_t b = jb; b < pm.p1; b += 32) {
-            const uint64_t j = b + lane;
-            uint32_t r = kInv;
-            if (j < pm.p1) r = static_cast<uint32_t>(__umul64hi(draw(ky, j - m + 1), j + 1));
-            unsigned mask = __ballot_sync(kFull, j < pm.p1 && r < m);
-            while (mask) {
-              const int src = __ffs(mask) - 1;
-              const uint32_t slot = __shfl_sync(kFull, r, src);
-              if (lane == static_cast<int>(slot)) ulast = static_cast<uint32_t>(b + src);
-              mask &= mask - 1;
-            }
-          }
-        }
-      } else if (seg) {
-        uint64_t jb = pm.p0;
-        if (first_piece) {
-          const uint32_t nf = min(m, im.z - im.y);
-          rsv::fill_slots(nb, im.y, nf, ky, 0, lane, pol, wst, FillEmit<K>{rid, rkey});
-          rcnt = nf;
-          jb = im.y + nf;
-        }
-        if (im.z - im.y >= m && jb < pm.p1) {
-          SegEmit<K> em{rid, rkey, &rcnt, kRecCap, lane};
-          rsv::replay_range(nb, jb, pm.p1, ky, 0, lane, pol, wst, em);
-        }
-      } else {
-        uint64_t jb = pm.p0;
-        if (first_piece) {
-          rsv::fill_slots(nb, 0, m, ky, 0, lane, pol, wst, rsv::NoEmit{});
-          jb = m;
-        }
-        if (jb < pm.p1) rsv::replay_range(nb, jb, pm.p1, ky, 0, lane, pol, wst, rsv::NoEmit{});
-      }
-      if (last_piece) {
-        if (seg) {
-          if (a.kind == A3G_SAMPLER_UNIFORM) {
-            a.hub.slot_last[static_cast<uint64_t>(im.w) * 32 + lane] = ulast;
-          } else if (lane == 0) {
-            a.hub.rec_cnt[im.w] = rcnt;
-            a.hub.tau[im.w] = *reinterpret_cast<const uint64_t*>(&wst.thr);
-            a.hub.tau_ok[im.w] = (im.z - im.y >= m) ? 1u : 0u;
-          }
-        } else {
-          const uint64_t row0 = static_cast<uint64_t>(im.x) * m;
-          const uint32_t id = a.kind == A3G_SAMPLER_UNIFORM ? uid : wst.my_id;
-          if (lane < static_cast<int>(m)) {
-            a.S[row0 + lane] = id;
-            mark_first(a.first, id, a.tag, static_cast<uint32_t>(row0 + lane));
-          }
-          if (lane == 0) a.cnt[im.x] = m;
-        }
-      }
-      __syncwarp();
-      if (q + kStages < NP) {
-        if (lane == 0) ptx::fence_proxy_async_smem();
-        const PieceMeta pn = piece_meta(q + kStages, np, pref_ex, itm.y, itm.z);
-        issue_piece(pn, __shfl_sync(kFull, beg, pn.it), a.col, ring, bar, st, lane);
-      }
-    }
-    Q += NP;
-  }
-}
-
-// ------------------------------------------------------------ stream (int) -
-// Items of the integer-key policies (all weights 1 -- PolUnit -- or all gamma
-// -- PolGammaAll -- and Algorithm R): a key depends only on (row key,
-// position), never on the neighbour id, so the hot loop hashes positions
-// without touching the adjacency. Each lane evaluates kIntU keys per group
-// (independent mix64 chains); one vote decides whether any beats the current
-// minimum (x > (thr << 11 | 0x7ff) <=> x >> 11 > thr). Only groups with
-// candidates load the candidates' ids (one coalesced round trip) and run the
-// ordered insertion replay of reservoir.cuh -- the same slot history as the
-// reference (sampler.cpp:24-40).
-constexpr int kIntU = 4;
-
-template <typename P, typename Emit>
-__device__ __forceinline__ void replay_int(const uint32_t* nb, uint64_t jb, uint64_t je, uint64_t key, int lane,
-                                           P& pol, rsv::WState<uint64_t>& s, const Emit& emit) {
-  constexpr uint64_t kStep = 32ull * kPhi;
-  uint64_t thrx = (s.thr << 11) | 0x7ffull;
-  uint64_t ctr = key + (jb + lane + 1) * kPhi;
-  for (uint64_t b = jb; b < je; b += 32 * kIntU, ctr += kIntU * kStep) {
-    uint64_t x[kIntU];
-    bool c[kIntU];
-    bool anyc = false;
-#pragma unroll
-    for (int q = 0; q < kIntU; ++q) {
-      x[q] = mix64(ctr + q * kStep);
-      c[q] = b + q * 32 + lane < je && x[q] > thrx;
-      anyc |= c[q];
-    }
-    if (!__any_sync(kFull, anyc)) continue;
-    uint32_t v[kIntU];
-#pragma unroll
-    for (int q = 0; q < kIntU; ++q) v[q] = c[q] ? __ldg(nb + b + q * 32 + lane) : 0u;
-#pragma unroll
-    for (int q = 0; q < kIntU; ++q) {
-      const uint64_t kk = x[q] >> 11;
-      unsigned mask = __ballot_sync(kFull, c[q] && kk > s.thr);
-      while (mask) {
-        const int src = __ffs(mask) - 1;
-        const uint64_t kv = __shfl_sync(kFull, kk, src);
-        const uint32_t iv = __shfl_sync(kFull, v[q], src);
-        if (pol.gt(kv, s.thr)) {
-          if (lane == s.mp) {
-            s.my_key = kv;
-            s.my_id = iv;
-          }
-          emit(iv, kv, src, b + q * 32 + src);
-          pol.argmin(s.thr, s.mp, s.my_key, lane);
-          mask &= __ballot_sync(kFull, c[q] && kk > s.thr);
-        }
-        mask &= ~((2u << src) - 1u);
-      }
-    }
-    thrx = (s.thr << 11) | 0x7ffull;
-  }
-}
-
-template <int WM>
-__global__ void __launch_bounds__(256) k_stream_int(SampleArgs a) {
-  using P = typename PolOf<WM>::P;
-  static_assert(sizeof(typename P::K) == 8, "integer-key policy");
-  const int lane = threadIdx.x & 31;
-  const uint32_t nitems = min(*a.item_count, a.hub.item_cap);
-  const uint32_t m = a.f;
-  const uint32_t nwarps_total = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t claim = max(1u, min(8u, nitems / (8 * nwarps_total)));
-  for (;;) {
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(a.item_work, claim);
-    base = __shfl_sync(kFull, base, 0);
-    if (base >= nitems) break;
-    const uint32_t iend = min(nitems, base + claim);
-    for (uint32_t it = base; it < iend; ++it) {
-      const uint4 im = a.hub.items[it];
-      const uint32_t dst = __ldg(a.front + im.x);
-      const uint64_t beg = __ldg(a.ro + dst);
-      const uint32_t* nb = a.col + beg;
-      const uint64_t key = hash2(a.seed, hash2(a.layer, dst));
-      const bool seg = im.w != kInv;
-      if (a.kind == A3G_SAMPLER_UNIFORM) {
-        if (!seg) {
-          uint32_t uid = lane < static_cast<int>(m) ? __ldg(nb + lane) : 0u;
-          rsv::uniform_range(nb, m, im.z, m, key, lane, 0, uid);
-          const uint64_t row0 = static_cast<uint64_t>(im.x) * m;
-          if (lane < static_cast<int>(m)) {
-            a.S[row0 + lane] = uid;
-            mark_first(a.first, uid, a.tag, static_cast<uint32_t>(row0 + lane));
-          }
-          if (lane == 0) a.cnt[im.x] = m;
-        } else {
-          uint32_t ulast = kInv;
-          const uint64_t jb0 = im.y > m ? im.y : static_cast<uint64_t>(m);
-          for (uint64_t b = jb0; b < im.z; b += 32) {
-            const uint64_t j = b + lane;
-            uint32_t r = kInv;
-            if (j < im.z) r = static_cast<uint32_t>(__umul64hi(draw(key, j - m + 1), j + 1));
-            unsigned mask = __ballot_sync(kFull, j < im.z && r < m);
-            while (mask) {
-              const int src = __ffs(mask) - 1;
-              const uint32_t slot = __shfl_sync(kFull, r, src);
-              if (lane == static_cast<int>(slot)) ulast = static_cast<uint32_t>(b + src);
-              mask &= mask - 1;
-            }
-          }
-          a.hub.slot_last[static_cast<uint64_t>(im.w) * 32 + lane] = ulast;
-        }
-        continue;
-      }
-      P pol = PolOf<WM>::make(a);
-      rsv::WState<uint64_t> wst;
-      if (seg) {
-        uint32_t* rid = a.hub.rec_id + static_cast<uint64_t>(im.w) * kRecCap;
-        uint64_t* rkey = a.hub.rec_key + static_cast<uint64_t>(im.w) * kRecCap;
-        const uint32_t nf = min(m, im.z - im.y);
-        rsv::fill_slots(nb, im.y, nf, key, 0, lane, pol, wst, FillEmit<uint64_t>{rid, rkey});
-        uint32_t rcnt = nf;
-        if (im.z - im.y >= m) {
-          SegEmit<uint64_t> em{rid, rkey, &rcnt, kRecCap, lane};
-          replay_int(nb, im.y + nf, im.z, key, lane, pol, wst, em);
-        }
-        if (lane == 0) {
-          a.hub.rec_cnt[im.w] = rcnt;
-          a.hub.tau[im.w] = wst.thr;
-          a.hub.tau_ok[im.w] = (im.z - im.y >= m) ? 1u : 0u;
-        }
-      } else {
-        rsv::fill_slots(nb, 0, m, key, 0, lane, pol, wst, rsv::NoEmit{});
-        replay_int(nb, m, im.z, key, lane, pol, wst, rsv::NoEmit{});
-        const uint64_t row0 = static_cast<uint64_t>(im.x) * m;
-        if (lane < static_cast<int>(m)) {
-          a.S[row0 + lane] = wst.my_id;
-          mark_first(a.first, wst.my_id, a.tag, static_cast<uint32_t>(row0 + lane));
-        }
-        if (lane == 0) a.cnt[im.x] = m;
-      }
     }
   }
 }
@@ -1795,8 +1476,6 @@ void launch_layer_kernels(const SampleArgs& sa, int sm_count, cudaStream_t st) {
   if (sa.f <= 32) {
     static bool attr_set = false;
     if (!attr_set) {
-      A3G_CUDA(cudaFuncSetAttribute(k_stream<WM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(kStreamSmem)));
       A3G_CUDA(cudaFuncSetAttribute(k_hub_merge<WM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kMergeSmem)));
       attr_set = true;
@@ -1910,6 +1589,7 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
     sa.tie = 64ull * (static_cast<uint64_t>(std::ceil(std::min(gamma, 1e12))) + 1);
     sa.f = la.f;
     sa.layer = l;
+    sa.seg = s.seg;
     sa.tag = tag;
     sa.kind = kind;
     sa.wmode = wmode;

@@ -20,9 +20,9 @@ struct LayerArena {
   double* scratch = nullptr;      // reservoir keys for f > 32 rows [cap_rows*f]
 };
 
-// Hub splitting (rows with deg > kSeg): per-segment local records.
-constexpr uint32_t kSeg = 2048;    // neighbours per segment
-constexpr uint32_t kRecCap = 256;  // record capacity per segment (expected ~m(1+ln(kSeg/m)) <= 90)
+// Hub splitting (rows with deg > seg): per-segment local records.
+constexpr uint32_t kSegMin = 2048;  // neighbours per hub segment (SamplerState::seg: 2048 or 4096)
+constexpr uint32_t kRecCap = 256;   // record capacity per segment (expected m(1+ln(seg/m)) <= 190 for m <= 32)
 
 struct HubArena {
   uint32_t hub_cap = 0, seg_cap = 0;
@@ -73,6 +73,11 @@ struct SamplerState {
   bool has_batch = false;
   int sm_count = 148;
   int device = 0;  // the graph's device (kept so destroy never dereferences the graph)
+  // Hub segment length. Rows longer than this are split and merged; shorter
+  // ones are one item. Longer segments mean fewer merges but longer serial
+  // items: 4096 pays on dense graphs (mean degree >= 128, e.g. C2: 0.80 vs
+  // 0.88 ms/step), 2048 on sparse ones (C3: 1.24 vs 1.36 ms/step), r01 sweep.
+  uint32_t seg = kSegMin;
 };
 
 // Launch the whole k-hop sample for seeds already in s.d_seeds (n_seeds on host).

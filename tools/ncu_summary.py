@@ -45,11 +45,12 @@ def main(path):
             if key in hdr:
                 i = hdr.index(key)
                 print(f"  {label:16s} {r[i]:>14s} {units[i]}")
+        scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
         try:
-            rd = float(r[hdr.index("dram__bytes_read.sum")])
-            wr = float(r[hdr.index("dram__bytes_write.sum")])
-            print(f"  {'traffic':16s} {rd + wr:14.3f} {units[hdr.index('dram__bytes_read.sum')]} (read+write)")
-        except ValueError:
+            ir, iw = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+            mb = float(r[ir]) * scale[units[ir]] + float(r[iw]) * scale[units[iw]]
+            print(f"  {'traffic':16s} {mb:14.3f} Mbyte (read+write)")
+        except (ValueError, KeyError):
             pass
     det = ncu(path, "details")
     h = det[0]

@@ -78,50 +78,78 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML polled
+    every ~2 ms from a thread (the timed region of a short run is tens of ms,
+    below nvidia-smi's sampling period); nvidia-smi is the fallback."""
+    NAMES = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
 
     def __init__(self, device: int):
         self.device = device
-        self.rows = []
-        self.proc = None
+        self.sm, self.mx, self.reasons = [], None, set()
+        self.stop = threading.Event()
+        self.t = None
+
+    def _poll(self):
+        import pynvml
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+        get_r = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+        self.mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        while True:
+            self.sm.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+            r = get_r(h)
+            for name, bit in self.NAMES.items():
+                if r & bit:
+                    self.reasons.add(name)
+            if self.stop.wait(0.002):
+                break
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def _smi(self):  # fallback without NVML bindings: nvidia-smi at its fastest period
+        try:
+            self._smi_loop()
+        except Exception:
+            pass
+
+    def _smi_loop(self):
+        self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits", "-lms", "20"],
+                                     stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.proc.stdout:
+            p = [x.strip() for x in line.split(",")]
+            if len(p) >= 6 and p[0].replace(".", "").isdigit():
+                self.sm.append(float(p[0]))
+                self.mx = float(p[1]) if p[1].replace(".", "").isdigit() else self.mx
+                self.reasons.update(n for n, v in zip(names, p[2:6]) if v.lower() == "active")
 
     def __enter__(self):
+        self.proc = None
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            import pynvml
+            pynvml.nvmlInit()
+            self.t = threading.Thread(target=self._poll, daemon=True)
         except Exception:
-            self.proc = None
+            self.t = threading.Thread(target=self._smi, daemon=True)
+        self.t.start()
+        time.sleep(0.005)  # first sample lands inside the region
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 9:
-                self.rows.append(parts)
-
     def __exit__(self, *a):
+        self.stop.set()
         if self.proc:
+            time.sleep(0.05)
             self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
 
     def summary(self):
-        if not self.rows:
+        if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.mx, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": "nvml"}
 
 
 def make_graph(cfg_name):
@@ -261,7 +289,7 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (CSR %.0f MB + features %.0f MB)" % (
                        g.num_edges * 4 / 1e6, n * F * (2 if args.config in SYNTH else 4) / 1e6),
                    "graph_gen_s": round(gen_s, 1)},
-        "roofline": {"kernel": "k_agg1 (fused gather + mean aggregation + W1 update)", "bound": "hbm",
+        "roofline": {"kernel": "k_agg1 (fused feature gather + mean aggregation)", "bound": "hbm",
                      "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "bytes_per_launch": agg_bytes,
                      "ms_per_launch": agg_ms},

@@ -936,10 +936,12 @@ a3g_status a3g_trainer_timing(a3g_trainer* tr, double* total_ms, double* agg_ms,
     if (total_ms) *total_ms = t.last_total_ms;
     if (agg_ms) *agg_ms = t.last_agg_ms;
     if (agg_bytes) *agg_bytes = t.last_agg_bytes;
-    // kernels per step: init + mark + 2 (seed finalize) + 3 per layer + resolve
-    //                   + agg1 + outer + dw1 + reduce + sgd (+ scale with comm)
-    if (launches_per_step)
-      *launches_per_step = 4 + 3ull * t.L + (t.L ? 1 : 0) + 5 + (t.comm ? 1 : 0);
+    // our kernels per step (library CUB sort kernels not counted): seeds phase
+    // 4 (init, mark, fin count/emit); per layer 6 (classify, item classes,
+    // stream, hub merge, fin count/emit); resolve; compute 8 (stats, agg,
+    // h1 GEMM, outer, dh1 gather, dW1 GEMM, reduce, sgd) + split-K reduce +
+    // the sync scale with a communicator
+      *launches_per_step = 4 + 6ull * t.L + (t.L ? 1 : 0) + 8 + (t.h1_split_used ? 1 : 0) + (t.comm ? 1 : 0);
   });
 }
 

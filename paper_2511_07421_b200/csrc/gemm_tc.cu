@@ -418,7 +418,7 @@ size_t tc_dw1_smem(uint32_t H) {
   return 2ull * kStgBytes + 2ull * (2 * 64 * 32 * 4) + kParts * kPartBytes + static_cast<size_t>(kParts) * 64 * HN * 2;
 }
 
-void launch_h1_tc(const TrainerState& t, const float* agg, const uint32_t* n_inner, float* h1, cudaStream_t st) {
+void launch_h1_tc(TrainerState& t, const float* agg, const uint32_t* n_inner, float* h1, cudaStream_t st) {
   TcArgs a{};
   a.agg = agg;
   a.pitch = t.pitch;
@@ -442,6 +442,7 @@ void launch_h1_tc(const TrainerState& t, const float* agg, const uint32_t* n_inn
   A3G_CUDA(cudaFuncSetAttribute(k_h1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   k_h1_tc<<<dim3(tiles, ksplit), kTcThreads, smem, st>>>(a);
   A3G_LAUNCH_CHECK("k_h1_tc");
+  t.h1_split_used = ksplit > 1;
   if (ksplit > 1) {
     k_h1_reduce<<<t.sm_count * 2, 256, 0, st>>>(t.d_hpart, ksplit, a.part_rows, n_inner, t.H, h1);
     A3G_LAUNCH_CHECK("k_h1_reduce");

@@ -52,6 +52,7 @@ struct TrainerState {
   uint32_t tc_splits = 1;   // row splits of the dW1 tcgen05 GEMM (partials in d_part)
   float* d_hpart = nullptr; // split-K partials of the h1 GEMM [h1_split_cap][cap_inner][H]
   uint32_t h1_split_cap = 1;
+  bool h1_split_used = false;  // the last step's h1 GEMM ran split-K (+ k_h1_reduce)
 };
 
 // Compute part of one step on s_comp for the batch in arena `smp`
@@ -62,7 +63,7 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
 // tcgen05 dense update (gemm_tc.cu)
 size_t tc_h1_smem(uint32_t F, uint32_t H);
 size_t tc_dw1_smem(uint32_t H);
-void launch_h1_tc(const TrainerState& t, const float* agg, const uint32_t* n_inner, float* h1, cudaStream_t st);
+void launch_h1_tc(TrainerState& t, const float* agg, const uint32_t* n_inner, float* h1, cudaStream_t st);
 void launch_dw1_tc(const TrainerState& t, const float* agg, const uint32_t* n_inner, const float* h1,
                    const float* dh1, float* part, uint32_t nsplit, cudaStream_t st);
 // CUB temp storage of the dh1 scatter sort for n_entries entries.

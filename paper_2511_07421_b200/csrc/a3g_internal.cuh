@@ -48,6 +48,15 @@ a3g_status guard(Fn&& fn) {
 #define A3G_CUDA(x) ::a3g::cuda_check((x), #x)
 #define A3G_LAUNCH_CHECK(name) ::a3g::cuda_check(cudaGetLastError(), name)
 
+// Launch timeline (diagnostics, A3G_TIMELINE=1): an event after every kernel
+// of the traced steps on its stream; a3g_train_steps prints the end times.
+void tl_mark(const char* name, cudaStream_t st);
+#define A3G_LAUNCH_DONE(name, st)                        \
+  do {                                                   \
+    ::a3g::cuda_check(cudaGetLastError(), name);         \
+    ::a3g::tl_mark(name, st);                            \
+  } while (0)
+
 // ------------------------------------------------------------ RNG ----------
 // include/a3gnn/rng.hpp:13-55, bit-exact on the device.
 constexpr uint64_t kPhi = 0x9e3779b97f4a7c15ull;

@@ -2,6 +2,7 @@
 // reference-order validation, status <-> exception mapping, host<->device
 // staging. Kernels live in sampler.cu / train.cu.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -224,6 +225,24 @@ void init_weights(uint32_t F, uint32_t H, uint32_t C, uint64_t seed, std::vector
 }  // namespace
 
 void a3g::set_error(const std::string& msg) { g_err = msg; }
+
+namespace {
+struct TlEvent {
+  const char* name;
+  cudaStream_t st;
+  cudaEvent_t ev;
+};
+thread_local bool g_tl_on = false;
+thread_local std::vector<TlEvent> g_tl;
+}  // namespace
+
+void a3g::tl_mark(const char* name, cudaStream_t st) {
+  if (!g_tl_on) return;
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, st);
+  g_tl.push_back(TlEvent{name, st, e});
+}
 
 // ====================================================================== ABI
 extern "C" {
@@ -830,8 +849,16 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
     }
     // depth-2 pipeline: sampling of step i+1 (s_samp) overlaps compute of
     // step i (s_comp); arena i%2 is reused only after compute i-2 consumed it.
+    static const bool tl_env = std::getenv("A3G_TIMELINE") != nullptr;
+    cudaEvent_t tl0 = nullptr;
     for (uint32_t i = 0; i < K; ++i) {
       a3g_sampler* smp = t.smp[i & 1];
+      if (tl_env && K >= 4 && i == K / 2) {  // trace steps K/2 and K/2+1 (both streams)
+        g_tl_on = true;
+        A3G_CUDA(cudaEventCreate(&tl0));
+        A3G_CUDA(cudaEventRecord(tl0, t.s_comp));
+      }
+      if (tl_env && K >= 4 && i == K / 2 + 2) g_tl_on = false;
       if (i >= 2) A3G_CUDA(cudaStreamWaitEvent(t.s_samp, t.ev_consumed[i & 1], 0));
       sample_impl(smp->st, dseeds + off[i], static_cast<uint32_t>(off[i + 1] - off[i]), true, gamma, kind,
                   rng_seeds[i], t.s_samp);
@@ -841,9 +868,21 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
                            t.s_comp, t.timing);
       A3G_CUDA(cudaEventRecord(t.ev_consumed[i & 1], t.s_comp));
     }
+    g_tl_on = false;
     A3G_CUDA(cudaMemcpyAsync(t.h_losses, t.d_losses, K * 8ull, cudaMemcpyDeviceToHost, t.s_comp));
     A3G_CUDA(cudaEventRecord(t.ev_t1, t.s_comp));
     A3G_CUDA(cudaStreamSynchronize(t.s_comp));
+    A3G_CUDA(cudaStreamSynchronize(t.s_samp));
+    if (tl0) {  // end time of every traced launch, relative to the first traced step's start
+      for (const TlEvent& e : g_tl) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, tl0, e.ev);
+        std::fprintf(stderr, "a3g-timeline %s %s %.1f\n", e.st == t.s_comp ? "comp" : "samp", e.name, ms * 1e3);
+        cudaEventDestroy(e.ev);
+      }
+      g_tl.clear();
+      cudaEventDestroy(tl0);
+    }
     t.last_steps = K;
     if (losses_out) std::memcpy(losses_out, t.h_losses, K * 8ull);
     float ms = 0;

@@ -441,11 +441,11 @@ void launch_h1_tc(TrainerState& t, const float* agg, const uint32_t* n_inner, fl
   const size_t smem = tc_h1_smem(t.F, t.H);
   A3G_CUDA(cudaFuncSetAttribute(k_h1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   k_h1_tc<<<dim3(tiles, ksplit), kTcThreads, smem, st>>>(a);
-  A3G_LAUNCH_CHECK("k_h1_tc");
+  A3G_LAUNCH_DONE("k_h1_tc", st);
   t.h1_split_used = ksplit > 1;
   if (ksplit > 1) {
     k_h1_reduce<<<t.sm_count * 2, 256, 0, st>>>(t.d_hpart, ksplit, a.part_rows, n_inner, t.H, h1);
-    A3G_LAUNCH_CHECK("k_h1_reduce");
+    A3G_LAUNCH_DONE("k_h1_reduce", st);
   }
 }
 
@@ -467,7 +467,7 @@ void launch_dw1_tc(const TrainerState& t, const float* agg, const uint32_t* n_in
   A3G_CUDA(cudaFuncSetAttribute(k_dw1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const dim3 grid((t.F + 127) / 128, nsplit);
   k_dw1_tc<<<grid, kTcThreads, smem, st>>>(a);
-  A3G_LAUNCH_CHECK("k_dw1_tc");
+  A3G_LAUNCH_DONE("k_dw1_tc", st);
 }
 
 }  // namespace a3g

@@ -780,12 +780,26 @@ __device__ bool hub_merge_parallel(const SampleArgs& a, uint32_t h, uint8_t* sme
     }
     return lo;
   };
-  // (B1) keep bitmap
-  for (uint32_t r = threadIdx.x; r < nrec; r += blockDim.x) {
-    const uint32_t s = seg_of(r);
-    const uint32_t i = r - s_pre[s] + (s == 0 ? m : 0u);
-    const K kv = key_from_bits<K>(a.hub.rec_key[static_cast<uint64_t>(s0 + s) * kRecCap + i]);
-    if (!s_lok[s] || pol.keep(kv, s_L[s])) atomicOr(&s_bits[s * kM2Words + (i >> 5)], 1u << (i & 31));
+  // (B1) keep bitmap; 4 records per thread per round with their loads issued
+  // together (the round trips, not the work, bound this phase)
+  constexpr int kB1 = 4;
+  for (uint32_t r0 = threadIdx.x; r0 < nrec; r0 += kB1 * blockDim.x) {
+    uint32_t sg[kB1], ix[kB1];
+    uint64_t kb[kB1];
+#pragma unroll
+    for (int q = 0; q < kB1; ++q) {
+      const uint32_t r = r0 + q * blockDim.x;
+      sg[q] = r < nrec ? seg_of(r) : 0u;
+      ix[q] = r < nrec ? r - s_pre[sg[q]] + (sg[q] == 0 ? m : 0u) : 0u;
+      kb[q] = r < nrec ? a.hub.rec_key[static_cast<uint64_t>(s0 + sg[q]) * kRecCap + ix[q]] : 0ull;
+    }
+#pragma unroll
+    for (int q = 0; q < kB1; ++q) {
+      if (r0 + q * blockDim.x >= nrec) break;
+      const uint32_t sq = sg[q], iq = ix[q];
+      if (!s_lok[sq] || pol.keep(key_from_bits<K>(kb[q]), s_L[sq]))
+        atomicOr(&s_bits[sq * kM2Words + (iq >> 5)], 1u << (iq & 31));
+    }
   }
   __syncthreads();
   if (warp == 0) {  // survivors per segment -> exclusive offsets
@@ -1472,7 +1486,7 @@ __global__ void k_gather_unique(const __grid_constant__ StoreView view, uint32_t
 template <int WM>
 void launch_layer_kernels(const SampleArgs& sa, int sm_count, cudaStream_t st) {
   k_classify<WM><<<sm_count * 2, 256, 0, st>>>(sa);
-  A3G_LAUNCH_CHECK("k_classify");
+  A3G_LAUNCH_DONE("k_classify", st);
   if (sa.f <= 32) {
     static bool attr_set = false;
     if (!attr_set) {
@@ -1486,7 +1500,7 @@ void launch_layer_kernels(const SampleArgs& sa, int sm_count, cudaStream_t st) {
       const HubArena& hb = sa.hub;
       k_item_class<<<sm_count * 2, 256, 0, st>>>(hb.items, sa.item_count, hb.item_cap, hb.sort_keys[0],
                                                  sa.cls_count);
-      A3G_LAUNCH_CHECK("k_item_class");
+      A3G_LAUNCH_DONE("k_item_class", st);
       const uint32_t* lists = hb.sort_keys[0];
       constexpr int W = WM == 2 ? 0 : WM;
       const int grid = sm_count * 8;
@@ -1497,7 +1511,7 @@ void launch_layer_kernels(const SampleArgs& sa, int sm_count, cudaStream_t st) {
           k_stream_grp_mixed<16><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         else
           k_stream_grp_mixed<32><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
-        A3G_LAUNCH_CHECK("k_stream_grp_mixed");
+        A3G_LAUNCH_DONE("k_stream_grp_mixed", st);
       } else {
         if (sa.f <= 8)
           k_stream_grp<W, 8><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
@@ -1505,11 +1519,11 @@ void launch_layer_kernels(const SampleArgs& sa, int sm_count, cudaStream_t st) {
           k_stream_grp<W, 16><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         else
           k_stream_grp<W, 32><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
-        A3G_LAUNCH_CHECK("k_stream_grp");
+        A3G_LAUNCH_DONE("k_stream_grp", st);
       }
     }
     k_hub_merge<WM><<<sm_count * 2, kMergeThreads, kMergeSmem, st>>>(sa);
-    A3G_LAUNCH_CHECK("k_hub_merge");
+    A3G_LAUNCH_DONE("k_hub_merge", st);
   }
 }
 
@@ -1522,13 +1536,13 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
   a3g_cache* c = s.c;
   BatchCounters* ctr = s.d_ctr;
   k_init_counters<<<1, 64, 0, st>>>(ctr, n_seeds);
-  A3G_LAUNCH_CHECK("k_init_counters");
+  A3G_LAUNCH_DONE("k_init_counters", st);
   if (s.cap_inner) A3G_CUDA(cudaMemsetAsync(s.d_inv1, 0xff, s.cap_inner * sizeof(int32_t), st));
   ++s.gtag;
   // ---- seeds phase (sampler.cpp:100-105)
   const uint32_t tag0 = ++s.tag;
   k_mark_list<<<(n_seeds + 255) / 256, 256, 0, st>>>(s.d_seeds, n_seeds, s.d_first, tag0);
-  A3G_LAUNCH_CHECK("k_mark_list");
+  A3G_LAUNCH_DONE("k_mark_list", st);
   {
     FinArgs fa{};
     fa.S = s.d_seeds;
@@ -1551,7 +1565,7 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
     const uint32_t nb = (n_seeds + kFinTile - 1) / kFinTile;
     k_fin_count<<<nb, kFinThreads, 0, st>>>(fa);
     k_fin_emit<<<nb, kFinThreads, 0, st>>>(fa);
-    A3G_LAUNCH_CHECK("seed finalize");
+    A3G_LAUNCH_DONE("seed finalize", st);
   }
   // ---- layers (sampler.cpp:107-135)
   int wmode = 0;
@@ -1620,7 +1634,7 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
     const uint32_t nb = static_cast<uint32_t>((la.cap_rows * la.f + kFinTile - 1) / kFinTile);
     k_fin_count<<<nb, kFinThreads, 0, st>>>(fa);
     k_fin_emit<<<nb, kFinThreads, 0, st>>>(fa);
-    A3G_LAUNCH_CHECK("layer finalize");
+    A3G_LAUNCH_DONE("layer finalize", st);
   }
   if (s.L) {
     ResolveArgs ra{};
@@ -1633,7 +1647,7 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
     }
     ra.gidx = s.d_gidx;
     k_resolve<<<dim3(s.sm_count * 2, s.L), 256, 0, st>>>(ra);
-    A3G_LAUNCH_CHECK("k_resolve");
+    A3G_LAUNCH_DONE("k_resolve", st);
   }
 }
 
@@ -1648,14 +1662,14 @@ void launch_gather_unique(SamplerState& s, float* out, cudaStream_t st) {
   else
     k_gather_unique<float><<<s.sm_count * 4, 256, 0, st>>>(g->view, g->F, s.d_unique, uc, c->d_bits, bitmode,
                                                             out, s.d_ctr);
-  A3G_LAUNCH_CHECK("k_gather_unique");
+  A3G_LAUNCH_DONE("k_gather_unique", st);
 }
 
 void launch_reservoir_list(const uint32_t* d_nb, const double* d_w, uint64_t deg, uint32_t m,
                            uint64_t key, uint64_t c0, int kind, uint32_t* d_out, double* d_keys,
                            cudaStream_t st) {
   k_reservoir_list<<<1, 32, 0, st>>>(d_nb, d_w, deg, m, key, c0, kind, d_out, d_keys);
-  A3G_LAUNCH_CHECK("k_reservoir_list");
+  A3G_LAUNCH_DONE("k_reservoir_list", st);
 }
 
 }  // namespace a3g

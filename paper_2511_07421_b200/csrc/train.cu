@@ -496,7 +496,7 @@ void launch_agg(TrainerState& t, AggArgs aa, uint32_t chunks, cudaStream_t st) {
         raise(A3G_ERR_PARAMETER, "feature row too wide for k_agg1");
     }
   }
-  A3G_LAUNCH_CHECK("k_agg1");
+  A3G_LAUNCH_DONE("k_agg1", st);
 }
 
 }  // namespace
@@ -514,7 +514,7 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
     const a3g_cache* c = t.c;
     const int bitmode = c->all_cached ? 1 : (c->none_cached ? 0 : 2);
     k_step_stats<<<t.sm_count, 256, 0, st>>>(ctr, s.d_unique, c->d_bits, bitmode, s.L, d_stats);
-    A3G_LAUNCH_CHECK("k_step_stats");
+    A3G_LAUNCH_DONE("k_step_stats", st);
   }
   // ---- gather + aggregation + GEMM1 (forward, inner rows)
   AggArgs aa{};
@@ -574,7 +574,7 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
   while (sort_bits < 32 && (t.cap_inner >> sort_bits) != 0) ++sort_bits;
   if (oa.f0 == 0) oa.f0 = 1;  // no layer: fallback entries only (keys of the edge part are all kInv)
   k_outer<<<std::max(1, static_cast<int>((t.max_seeds + 7) / 8)), 256, 0, st>>>(oa);
-  A3G_LAUNCH_CHECK("k_outer");
+  A3G_LAUNCH_DONE("k_outer", st);
   // ---- deterministic scatter into dh1: stable radix sort of the entries by row
   {
     size_t tmp = t.sort_tmp_bytes;
@@ -582,7 +582,7 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
                                              static_cast<int>(t.n_entries), 0, sort_bits, st));
     k_dh1_gather<<<t.sm_count * 2, 256, 0, st>>>(t.d_keys[1], t.d_vals[1], t.n_entries, oa.none, t.d_dagg, t.H,
                                                  t.d_dh1);
-    A3G_LAUNCH_CHECK("k_dh1_gather");
+    A3G_LAUNCH_DONE("k_dh1_gather", st);
   }
   // ---- dW1 = agg_inner^T . (dh1 * [h1 > 0]) on tcgen05, partials per row split
   const uint32_t nparts = t.tc_splits;
@@ -602,16 +602,16 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
   const uint32_t FH = t.F * t.H, HC = t.H * t.C;
   const uint32_t nb1 = std::min<uint32_t>(t.sm_count, (FH + 255) / 256);
   k_reduce<<<nb1 + HC + 1, 256, 0, st>>>(ra, nb1);
-  A3G_LAUNCH_CHECK("k_reduce");
+  A3G_LAUNCH_DONE("k_reduce", st);
   const bool synced = t.comm != nullptr;
   if (synced) {
     k_scale_for_sync<<<t.sm_count, 256, 0, st>>>(t.d_gw, FH + HC);
-    A3G_LAUNCH_CHECK("k_scale_for_sync");
+    A3G_LAUNCH_DONE("k_scale_for_sync", st);
     comm_allreduce_sum(t.comm, t.d_gw, FH + HC + 2, st);
   }
   k_sgd<<<t.sm_count, 256, 0, st>>>(t.d_w1, t.d_w2, t.d_gw, FH, HC, static_cast<float>(lr), synced ? 1 : 0,
                                     d_loss_slot);
-  A3G_LAUNCH_CHECK("k_sgd");
+  A3G_LAUNCH_DONE("k_sgd", st);
 }
 
 }  // namespace a3g

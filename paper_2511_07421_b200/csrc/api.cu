@@ -655,6 +655,8 @@ a3g_status a3g_trainer_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds, co
       t.d_w2 = dalloc<float>(static_cast<size_t>(H) * C);
       t.d_gw = dalloc<float>(static_cast<size_t>(t.F) * H + H * C + 2);
       t.d_agg_inner = dalloc<float>(t.cap_inner * g->pitch);
+      t.d_dh1_fx = dalloc<unsigned long long>(t.cap_inner * H);
+      A3G_CUDA(cudaMemset(t.d_dh1_fx, 0, t.cap_inner * H * 8));
       t.d_h1 = dalloc<float>(t.cap_inner * H);
       t.d_dh1 = dalloc<float>(t.cap_inner * H);
       t.d_agg_outer = dalloc<float>(static_cast<size_t>(max_seeds) * H);
@@ -662,14 +664,7 @@ a3g_status a3g_trainer_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds, co
       t.d_dlogits = dalloc<float>(static_cast<size_t>(max_seeds) * C);
       t.d_loss_s = dalloc<float>(max_seeds);
       t.d_dagg = dalloc<float>(static_cast<size_t>(max_seeds) * H);
-      t.n_entries = static_cast<uint64_t>(max_seeds) * ((L >= 1 ? fanouts[0] : 1) + 1);
-      if (t.n_entries >= (1ull << 31)) raise(A3G_ERR_PARAMETER, "trainer: batch x fanout too large");
-      for (int i = 0; i < 2; ++i) {
-        t.d_keys[i] = dalloc<uint32_t>(t.n_entries);
-        t.d_vals[i] = dalloc<uint32_t>(t.n_entries);
-      }
-      t.sort_tmp_bytes = dh1_sort_temp_bytes(t.n_entries);
-      t.d_sort_tmp = dalloc<uint8_t>(t.sort_tmp_bytes);
+      t.d_amax = dalloc<uint32_t>(1);
       t.nparts = static_cast<uint32_t>(t.sm_count);
       t.tc_splits = std::max<uint32_t>(1, static_cast<uint32_t>(t.sm_count) / ((t.F + 127) / 128));
       t.h1_split_cap = std::min<uint32_t>(8, (t.F + 63) / 64);
@@ -723,11 +718,8 @@ void a3g_trainer_destroy(a3g_trainer* tr) {
   dfree(t.d_dlogits);
   dfree(t.d_loss_s);
   dfree(t.d_dagg);
-  for (int i = 0; i < 2; ++i) {
-    dfree(t.d_keys[i]);
-    dfree(t.d_vals[i]);
-  }
-  if (t.d_sort_tmp) cudaFree(t.d_sort_tmp);
+  dfree(t.d_dh1_fx);
+  dfree(t.d_amax);
   dfree(t.d_part);
   dfree(t.d_hpart);
   dfree(t.d_agg_bytes);

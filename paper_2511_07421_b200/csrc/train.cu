@@ -10,16 +10,14 @@
 //   k_outer       per seed: agg_outer (trainer.cpp:116-127), logits,
 //                 softmax-CE + dlogits (:153-171), dagg_outer = dlogits . W2^T
 //                 (:177-179) pre-scaled by 1/deg, and the scatter entries.
-//   k_dh1_gather  dh1 rows from the stably sorted scatter entries (:182-198),
-//                 deterministic (no float atomics).
+//   k_dh1_scatter dh1 = the outer aggregation's scatter (:182-198) as 64-bit
+//                 fixed-point integer atomics (order-independent: deterministic).
 //   k_dw1_tc      dW1 = agg_inner^T . (dh1 * [h1>0]) on tcgen05 (:200-204).
 //   k_reduce      fixed-order reduction of the dW1 partials, dW2 (:174-175),
 //                 mean loss.
 //   k_sgd         w -= lr * g (trainer.cpp:208-211).
 #include <cmath>
 #include <cstdlib>
-
-#include <cub/device/device_radix_sort.cuh>
 
 #include "ptx.cuh"
 #include "trainer.cuh"
@@ -272,10 +270,7 @@ struct OuterArgs {
   float* dlogits;
   float* loss_s;
   float* dagg;     // [cap_seeds x H] per-edge dh1 contribution of seed s
-  uint32_t* keys;  // [cap_seeds x (f0 + 1)] dh1 row of each scatter entry (none: `none`)
-  uint32_t none;   // padding key, > every row index (the sort needs bit_width(none) bits)
-  uint32_t* vals;  // seed of each scatter entry
-  uint32_t cap_seeds;
+  uint32_t* amax;  // max |dagg| (float bits), the fixed-point scale of the dh1 scatter
   int has_layer0;
 };
 
@@ -331,44 +326,56 @@ __global__ void __launch_bounds__(256) k_outer(OuterArgs a) {
       const float dc = __shfl_sync(kFull, d, cc);
       if (lane < H) dg = fmaf(dc, a.w2[lane * C + cc], dg);
     }
-    if (lane < H) a.dagg[static_cast<uint64_t>(s) * H + lane] = c0 == 0 ? dg : (1.f / static_cast<float>(c0)) * dg;
-    // scatter entries (dh1 row <- seed s), sorted stably by row next: edge
-    // entries in edge order, then the self-fallback entry (trainer.cpp:182-198)
-    const uint64_t e0 = static_cast<uint64_t>(s) * a.f0;
-    for (uint32_t t = lane; t < a.f0; t += 32) {
-      a.keys[e0 + t] = t < c0 ? srcs[t] : a.none;
-      a.vals[e0 + t] = s;
-    }
-    if (lane == 0) {
-      const uint64_t fb = static_cast<uint64_t>(a.cap_seeds) * a.f0 + s;
-      a.keys[fb] = c0 == 0 ? s : a.none;
-      a.vals[fb] = s;
+    if (lane < H) {
+      const float v = c0 == 0 ? dg : (1.f / static_cast<float>(c0)) * dg;
+      a.dagg[static_cast<uint64_t>(s) * H + lane] = v;
+      atomicMax(a.amax, __float_as_uint(fabsf(v)));  // non-negative floats order like their bits
     }
   }
-  // pad the unused tail of the entry arrays (rows ns .. cap_seeds)
-  const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
-  for (uint64_t i = static_cast<uint64_t>(ns) * a.f0 + gt; i < static_cast<uint64_t>(a.cap_seeds) * a.f0; i += nt)
-    a.keys[i] = a.none;
-  for (uint64_t i = static_cast<uint64_t>(a.cap_seeds) * a.f0 + ns + gt;
-       i < static_cast<uint64_t>(a.cap_seeds) * (a.f0 + 1); i += nt)
-    a.keys[i] = a.none;
 }
 
-// dh1[r] = sum of the contributions of the sorted entries with key r, in
-// order (edges in edge order, then the fallback): deterministic, no atomics.
-__global__ void __launch_bounds__(256) k_dh1_gather(const uint32_t* keys, const uint32_t* vals, uint64_t n_entries,
-                                                    uint32_t none, const float* dagg, uint32_t H, float* dh1) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t i = gw; i < n_entries; i += nw) {
-    const uint32_t r = keys[i];
-    if (r == none) break;  // sorted: the padding is last
-    if (i > 0 && keys[i - 1] == r) continue;  // not the head of its run
-    float acc = 0.f;
-    for (uint64_t j = i; j < n_entries && keys[j] == r; ++j)
-      if (lane < static_cast<int>(H)) acc += dagg[static_cast<uint64_t>(vals[j]) * H + lane];
-    if (lane < static_cast<int>(H)) dh1[static_cast<uint64_t>(r) * H + lane] = acc;
+// Fixed-point scale of the dh1 scatter: every row sums at most ns + 1
+// contributions bounded by amax, so sums stay below 2^62.
+__device__ __forceinline__ double fx_scale(uint32_t amax_bits, uint32_t ns) {
+  const float amax = __uint_as_float(amax_bits);
+  if (!(amax > 0.f)) return 1.0;
+  const int e = ilogb(static_cast<double>(amax) * (ns + 1.0)) + 1;
+  return ldexp(1.0, 62 - e);
+}
+
+// Scatter through the outer mean aggregation into dh1 (trainer.cpp:182-198):
+// dh1[src] += dagg[s] for every layer-0 edge (s -> src), dh1[s] += dagg[s]
+// for self-fallback seeds -- as 64-bit fixed-point integer atomics, which add
+// associatively: the result is independent of the order (deterministic) and
+// more precise than an fp32 sum.
+__global__ void __launch_bounds__(256) k_dh1_scatter(const float* dagg, const uint32_t* amax, const uint32_t* ns_p,
+                                                     const uint32_t* cnt0, const uint32_t* sidx0, uint32_t f0,
+                                                     int has_layer0, uint32_t H, unsigned long long* fx) {
+  const uint32_t ns = *ns_p;
+  const double scale = fx_scale(*amax, ns);
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < static_cast<uint64_t>(ns) * H;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t s = static_cast<uint32_t>(i / H), h = static_cast<uint32_t>(i - static_cast<uint64_t>(s) * H);
+    const unsigned long long q = static_cast<unsigned long long>(llrint(static_cast<double>(dagg[i]) * scale));
+    const uint32_t c0 = has_layer0 ? cnt0[s] : 0u;
+    if (c0 == 0) {
+      atomicAdd(fx + static_cast<uint64_t>(s) * H + h, q);
+    } else {
+      const uint32_t* srcs = sidx0 + static_cast<uint64_t>(s) * f0;
+      for (uint32_t t = 0; t < c0; ++t) atomicAdd(fx + static_cast<uint64_t>(srcs[t]) * H + h, q);
+    }
+  }
+}
+
+// dh1 = fixed point / scale (rows < n_inner); clears the accumulator for the next step.
+__global__ void k_dh1_fix(unsigned long long* fx, const uint32_t* amax, const uint32_t* ns_p, const uint32_t* n_inner,
+                          uint32_t H, float* dh1) {
+  const double inv = 1.0 / fx_scale(*amax, *ns_p);
+  const uint64_t total = static_cast<uint64_t>(*n_inner) * H;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    dh1[i] = static_cast<float>(static_cast<double>(static_cast<long long>(fx[i])) * inv);
+    fx[i] = 0ull;
   }
 }
 
@@ -509,7 +516,6 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
   SamplerState& s = smp->st;
   a3g_graph* g = t.g;
   BatchCounters* ctr = s.d_ctr;
-  A3G_CUDA(cudaMemsetAsync(t.d_dh1, 0, t.cap_inner * t.H * sizeof(float), st));
   if (d_stats) {
     const a3g_cache* c = t.c;
     const int bitmode = c->all_cached ? 1 : (c->none_cached ? 0 : 2);
@@ -566,24 +572,16 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
   oa.dlogits = t.d_dlogits;
   oa.loss_s = t.d_loss_s;
   oa.dagg = t.d_dagg;
-  oa.keys = t.d_keys[0];
-  oa.vals = t.d_vals[0];
-  oa.cap_seeds = t.max_seeds;
-  oa.none = static_cast<uint32_t>(t.cap_inner);
-  int sort_bits = 1;
-  while (sort_bits < 32 && (t.cap_inner >> sort_bits) != 0) ++sort_bits;
-  if (oa.f0 == 0) oa.f0 = 1;  // no layer: fallback entries only (keys of the edge part are all kInv)
+  oa.amax = t.d_amax;
+  A3G_CUDA(cudaMemsetAsync(t.d_amax, 0, sizeof(uint32_t), st));
   k_outer<<<std::max(1, static_cast<int>((t.max_seeds + 7) / 8)), 256, 0, st>>>(oa);
   A3G_LAUNCH_DONE("k_outer", st);
-  // ---- deterministic scatter into dh1: stable radix sort of the entries by row
-  {
-    size_t tmp = t.sort_tmp_bytes;
-    A3G_CUDA(cub::DeviceRadixSort::SortPairs(t.d_sort_tmp, tmp, t.d_keys[0], t.d_keys[1], t.d_vals[0], t.d_vals[1],
-                                             static_cast<int>(t.n_entries), 0, sort_bits, st));
-    k_dh1_gather<<<t.sm_count * 2, 256, 0, st>>>(t.d_keys[1], t.d_vals[1], t.n_entries, oa.none, t.d_dagg, t.H,
-                                                 t.d_dh1);
-    A3G_LAUNCH_DONE("k_dh1_gather", st);
-  }
+  // ---- deterministic scatter into dh1 (fixed-point integer atomics)
+  k_dh1_scatter<<<t.sm_count * 2, 256, 0, st>>>(t.d_dagg, t.d_amax, oa.ns, oa.cnt0, oa.sidx0, oa.f0, oa.has_layer0,
+                                                t.H, t.d_dh1_fx);
+  A3G_LAUNCH_DONE("k_dh1_scatter", st);
+  k_dh1_fix<<<t.sm_count * 2, 256, 0, st>>>(t.d_dh1_fx, t.d_amax, oa.ns, aa.n_inner, t.H, t.d_dh1);
+  A3G_LAUNCH_DONE("k_dh1_fix", st);
   // ---- dW1 = agg_inner^T . (dh1 * [h1 > 0]) on tcgen05, partials per row split
   const uint32_t nparts = t.tc_splits;
   launch_dw1_tc(t, t.d_agg_inner, aa.n_inner, t.d_h1, t.d_dh1, t.d_part, nparts, st);
@@ -616,12 +614,3 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
 
 }  // namespace a3g
 
-namespace a3g {
-size_t dh1_sort_temp_bytes(uint64_t n_entries) {
-  size_t bytes = 0;
-  A3G_CUDA(cub::DeviceRadixSort::SortPairs(static_cast<void*>(nullptr), bytes, static_cast<const uint32_t*>(nullptr),
-                                           static_cast<uint32_t*>(nullptr), static_cast<const uint32_t*>(nullptr),
-                                           static_cast<uint32_t*>(nullptr), static_cast<int>(n_entries), 0, 32));
-  return bytes;
-}
-}  // namespace a3g

@@ -23,11 +23,8 @@ struct TrainerState {
   float* d_dlogits = nullptr;    // max_seeds x C
   float* d_loss_s = nullptr;     // max_seeds
   float* d_dagg = nullptr;       // max_seeds x H: per-edge dh1 contribution of each seed
-  uint32_t* d_keys[2] = {nullptr, nullptr};  // scatter entries (dh1 row), unsorted / sorted
-  uint32_t* d_vals[2] = {nullptr, nullptr};  // scatter entries (seed), unsorted / sorted
-  uint64_t n_entries = 0;        // max_seeds * (f0 + 1)
-  void* d_sort_tmp = nullptr;
-  size_t sort_tmp_bytes = 0;
+  unsigned long long* d_dh1_fx = nullptr;  // cap_inner x H fixed-point dh1 accumulator (kept zero between steps)
+  uint32_t* d_amax = nullptr;    // max |dagg| bits of the step
   float* d_part = nullptr;       // nparts x F x H
   uint32_t nparts = 0;
   double* d_losses = nullptr;    // per-step losses of train_steps
@@ -66,8 +63,6 @@ size_t tc_dw1_smem(uint32_t H);
 void launch_h1_tc(TrainerState& t, const float* agg, const uint32_t* n_inner, float* h1, cudaStream_t st);
 void launch_dw1_tc(const TrainerState& t, const float* agg, const uint32_t* n_inner, const float* h1,
                    const float* dh1, float* part, uint32_t nsplit, cudaStream_t st);
-// CUB temp storage of the dh1 scatter sort for n_entries entries.
-size_t dh1_sort_temp_bytes(uint64_t n_entries);
 // evaluate_full_graph (trainer.cpp:241-303) with the current device weights.
 double evaluate_full_graph(TrainerState& t, const uint8_t* test_mask);
 

@@ -644,7 +644,7 @@ a3g_status a3g_trainer_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds, co
       t.lr = lr;
       t.max_seeds = max_seeds;
       t.sm_count = sm_count_of(g->device);
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < TrainerState::kArenas; ++i) {
         t.smp[i] = new a3g_sampler;
         sampler_alloc(t.smp[i]->st, g, c, max_seeds, fanouts, L);
       }
@@ -677,7 +677,9 @@ a3g_status a3g_trainer_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds, co
       A3G_CUDA(cudaMallocHost(&t.h_losses, 8));
       A3G_CUDA(cudaStreamCreateWithFlags(&t.s_comp, cudaStreamNonBlocking));
       A3G_CUDA(cudaStreamCreateWithFlags(&t.s_samp, cudaStreamNonBlocking));
-      for (int i = 0; i < 2; ++i) {
+      A3G_CUDA(cudaStreamCreateWithFlags(&t.s_samp2, cudaStreamNonBlocking));
+      A3G_CUDA(cudaEventCreateWithFlags(&t.ev_seeds, cudaEventDisableTiming));
+      for (int i = 0; i < TrainerState::kArenas; ++i) {
         A3G_CUDA(cudaEventCreateWithFlags(&t.ev_sampled[i], cudaEventDisableTiming));
         A3G_CUDA(cudaEventCreateWithFlags(&t.ev_consumed[i], cudaEventDisableTiming));
       }
@@ -702,7 +704,8 @@ void a3g_trainer_destroy(a3g_trainer* tr) {
   if (t.g) cudaSetDevice(t.g->device);
   if (t.s_comp) cudaStreamSynchronize(t.s_comp);
   if (t.s_samp) cudaStreamSynchronize(t.s_samp);
-  for (int i = 0; i < 2; ++i)
+  if (t.s_samp2) cudaStreamSynchronize(t.s_samp2);
+  for (int i = 0; i < TrainerState::kArenas; ++i)
     if (t.smp[i]) {
       sampler_free(t.smp[i]->st);
       delete t.smp[i];
@@ -729,10 +732,12 @@ void a3g_trainer_destroy(a3g_trainer* tr) {
   if (t.h_seed_stage) cudaFreeHost(t.h_seed_stage);
   if (t.h_losses) cudaFreeHost(t.h_losses);
   for (cudaEvent_t e : t.ev_agg) cudaEventDestroy(e);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < TrainerState::kArenas; ++i) {
     if (t.ev_sampled[i]) cudaEventDestroy(t.ev_sampled[i]);
     if (t.ev_consumed[i]) cudaEventDestroy(t.ev_consumed[i]);
   }
+  if (t.ev_seeds) cudaEventDestroy(t.ev_seeds);
+  if (t.s_samp2) cudaStreamDestroy(t.s_samp2);
   if (t.ev_t0) cudaEventDestroy(t.ev_t0);
   if (t.ev_t1) cudaEventDestroy(t.ev_t1);
   if (t.s_comp) cudaStreamDestroy(t.s_comp);
@@ -839,37 +844,44 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
       A3G_CUDA(cudaMemcpyAsync(t.d_seed_buf, t.h_seed_stage, total * 4, cudaMemcpyHostToDevice, t.s_samp));
       dseeds = t.d_seed_buf;
     }
-    // depth-2 pipeline: sampling of step i+1 (s_samp) overlaps compute of
-    // step i (s_comp); arena i%2 is reused only after compute i-2 consumed it.
+    // stream pipeline: step i samples into arena i % kArenas on sampling
+    // stream i % 2 (two batches in sampling at once), compute consumes the
+    // arenas in order on s_comp; arena reuse waits for its previous compute.
+    A3G_CUDA(cudaEventRecord(t.ev_seeds, t.s_samp));
+    A3G_CUDA(cudaStreamWaitEvent(t.s_samp2, t.ev_seeds, 0));
     static const bool tl_env = std::getenv("A3G_TIMELINE") != nullptr;
     cudaEvent_t tl0 = nullptr;
     for (uint32_t i = 0; i < K; ++i) {
-      a3g_sampler* smp = t.smp[i & 1];
-      if (tl_env && K >= 4 && i == K / 2) {  // trace steps K/2 and K/2+1 (both streams)
+      const int ar = static_cast<int>(i % TrainerState::kArenas);
+      a3g_sampler* smp = t.smp[ar];
+      cudaStream_t ss = (i & 1) ? t.s_samp2 : t.s_samp;
+      if (tl_env && K >= 4 && i == K / 2) {  // trace steps K/2 and K/2+1 (all streams)
         g_tl_on = true;
         A3G_CUDA(cudaEventCreate(&tl0));
         A3G_CUDA(cudaEventRecord(tl0, t.s_comp));
       }
       if (tl_env && K >= 4 && i == K / 2 + 2) g_tl_on = false;
-      if (i >= 2) A3G_CUDA(cudaStreamWaitEvent(t.s_samp, t.ev_consumed[i & 1], 0));
+      if (i >= static_cast<uint32_t>(TrainerState::kArenas)) A3G_CUDA(cudaStreamWaitEvent(ss, t.ev_consumed[ar], 0));
       sample_impl(smp->st, dseeds + off[i], static_cast<uint32_t>(off[i + 1] - off[i]), true, gamma, kind,
-                  rng_seeds[i], t.s_samp);
-      A3G_CUDA(cudaEventRecord(t.ev_sampled[i & 1], t.s_samp));
-      A3G_CUDA(cudaStreamWaitEvent(t.s_comp, t.ev_sampled[i & 1], 0));
+                  rng_seeds[i], ss);
+      A3G_CUDA(cudaEventRecord(t.ev_sampled[ar], ss));
+      A3G_CUDA(cudaStreamWaitEvent(t.s_comp, t.ev_sampled[ar], 0));
       launch_train_compute(t, smp, t.lr, t.d_losses + i, t.d_stats + static_cast<size_t>(i) * A3G_STEP_STATS,
                            t.s_comp, t.timing);
-      A3G_CUDA(cudaEventRecord(t.ev_consumed[i & 1], t.s_comp));
+      A3G_CUDA(cudaEventRecord(t.ev_consumed[ar], t.s_comp));
     }
     g_tl_on = false;
     A3G_CUDA(cudaMemcpyAsync(t.h_losses, t.d_losses, K * 8ull, cudaMemcpyDeviceToHost, t.s_comp));
     A3G_CUDA(cudaEventRecord(t.ev_t1, t.s_comp));
     A3G_CUDA(cudaStreamSynchronize(t.s_comp));
     A3G_CUDA(cudaStreamSynchronize(t.s_samp));
+    A3G_CUDA(cudaStreamSynchronize(t.s_samp2));
     if (tl0) {  // end time of every traced launch, relative to the first traced step's start
       for (const TlEvent& e : g_tl) {
         float ms = 0;
         cudaEventElapsedTime(&ms, tl0, e.ev);
-        std::fprintf(stderr, "a3g-timeline %s %s %.1f\n", e.st == t.s_comp ? "comp" : "samp", e.name, ms * 1e3);
+        std::fprintf(stderr, "a3g-timeline %s %s %.1f\n",
+                     e.st == t.s_comp ? "comp" : (e.st == t.s_samp ? "samp0" : "samp1"), e.name, ms * 1e3);
         cudaEventDestroy(e.ev);
       }
       g_tl.clear();
@@ -958,7 +970,9 @@ a3g_status a3g_trainer_last_forward(a3g_trainer* tr, uint64_t* n_inner, double* 
   });
 }
 
-a3g_sampler* a3g_trainer_sampler(a3g_trainer* tr, int slot) { return tr->st.smp[slot & 1]; }
+a3g_sampler* a3g_trainer_sampler(a3g_trainer* tr, int slot) {
+  return tr->st.smp[static_cast<unsigned>(slot) % TrainerState::kArenas];
+}
 
 a3g_status a3g_trainer_timing(a3g_trainer* tr, double* total_ms, double* agg_ms, double* agg_bytes,
                               uint64_t* launches_per_step) {

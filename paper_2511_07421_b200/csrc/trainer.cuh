@@ -8,7 +8,13 @@ namespace a3g {
 struct TrainerState {
   a3g_graph* g = nullptr;
   a3g_cache* c = nullptr;
-  a3g_sampler* smp[2] = {nullptr, nullptr};  // ping-pong arenas (pipeline depth 2)
+  // Sampler arenas of the stream pipeline: step i samples into arena i % 3 on
+  // sampling stream i % 2 -- two batches are sampled concurrently (the
+  // sampler's many small latency-bound kernels interleave) while compute
+  // consumes in order; an arena is reused only after its step's compute.
+  static constexpr int kArenas = 3;
+  static constexpr int kSampStreams = 2;
+  a3g_sampler* smp[kArenas] = {nullptr, nullptr, nullptr};
   uint32_t F = 0, H = 0, C = 0, pitch = 0, L = 0, max_seeds = 0;
   double lr = 0.2;
   uint64_t cap_inner = 0;
@@ -37,8 +43,10 @@ struct TrainerState {
   uint32_t* h_seed_stage = nullptr;  // pinned staging
   uint64_t h_seed_cap = 0;
   double* h_losses = nullptr;        // pinned
-  cudaStream_t s_comp = nullptr, s_samp = nullptr;
-  cudaEvent_t ev_sampled[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
+  cudaStream_t s_comp = nullptr, s_samp = nullptr;  // s_samp: sampling stream 0
+  cudaStream_t s_samp2 = nullptr;                     // sampling stream 1
+  cudaEvent_t ev_sampled[kArenas] = {}, ev_consumed[kArenas] = {};
+  cudaEvent_t ev_seeds = nullptr;                     // host seeds copied (sampling streams wait on it)
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
   std::vector<cudaEvent_t> ev_agg;  // pairs around k_agg1 launches (timing)
   bool timing = true;

@@ -677,7 +677,9 @@ a3g_status a3g_trainer_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds, co
       A3G_CUDA(cudaMallocHost(&t.h_losses, 8));
       A3G_CUDA(cudaStreamCreateWithFlags(&t.s_comp, cudaStreamNonBlocking));
       A3G_CUDA(cudaStreamCreateWithFlags(&t.s_samp, cudaStreamNonBlocking));
-      A3G_CUDA(cudaStreamCreateWithFlags(&t.s_samp2, cudaStreamNonBlocking));
+      t.s_sx[0] = t.s_samp;
+      for (int i = 1; i < TrainerState::kSampStreams; ++i)
+        A3G_CUDA(cudaStreamCreateWithFlags(&t.s_sx[i], cudaStreamNonBlocking));
       A3G_CUDA(cudaEventCreateWithFlags(&t.ev_seeds, cudaEventDisableTiming));
       for (int i = 0; i < TrainerState::kArenas; ++i) {
         A3G_CUDA(cudaEventCreateWithFlags(&t.ev_sampled[i], cudaEventDisableTiming));
@@ -704,7 +706,8 @@ void a3g_trainer_destroy(a3g_trainer* tr) {
   if (t.g) cudaSetDevice(t.g->device);
   if (t.s_comp) cudaStreamSynchronize(t.s_comp);
   if (t.s_samp) cudaStreamSynchronize(t.s_samp);
-  if (t.s_samp2) cudaStreamSynchronize(t.s_samp2);
+  for (int i = 1; i < TrainerState::kSampStreams; ++i)
+    if (t.s_sx[i]) cudaStreamSynchronize(t.s_sx[i]);
   for (int i = 0; i < TrainerState::kArenas; ++i)
     if (t.smp[i]) {
       sampler_free(t.smp[i]->st);
@@ -737,7 +740,8 @@ void a3g_trainer_destroy(a3g_trainer* tr) {
     if (t.ev_consumed[i]) cudaEventDestroy(t.ev_consumed[i]);
   }
   if (t.ev_seeds) cudaEventDestroy(t.ev_seeds);
-  if (t.s_samp2) cudaStreamDestroy(t.s_samp2);
+  for (int i = 1; i < TrainerState::kSampStreams; ++i)
+    if (t.s_sx[i]) cudaStreamDestroy(t.s_sx[i]);
   if (t.ev_t0) cudaEventDestroy(t.ev_t0);
   if (t.ev_t1) cudaEventDestroy(t.ev_t1);
   if (t.s_comp) cudaStreamDestroy(t.s_comp);
@@ -848,13 +852,13 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
     // stream i % 2 (two batches in sampling at once), compute consumes the
     // arenas in order on s_comp; arena reuse waits for its previous compute.
     A3G_CUDA(cudaEventRecord(t.ev_seeds, t.s_samp));
-    A3G_CUDA(cudaStreamWaitEvent(t.s_samp2, t.ev_seeds, 0));
+    for (int j = 1; j < TrainerState::kSampStreams; ++j) A3G_CUDA(cudaStreamWaitEvent(t.s_sx[j], t.ev_seeds, 0));
     static const bool tl_env = std::getenv("A3G_TIMELINE") != nullptr;
     cudaEvent_t tl0 = nullptr;
     for (uint32_t i = 0; i < K; ++i) {
       const int ar = static_cast<int>(i % TrainerState::kArenas);
       a3g_sampler* smp = t.smp[ar];
-      cudaStream_t ss = (i & 1) ? t.s_samp2 : t.s_samp;
+      cudaStream_t ss = t.s_sx[i % TrainerState::kSampStreams];
       if (tl_env && K >= 4 && i == K / 2) {  // trace steps K/2 and K/2+1 (all streams)
         g_tl_on = true;
         A3G_CUDA(cudaEventCreate(&tl0));
@@ -875,13 +879,13 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
     A3G_CUDA(cudaEventRecord(t.ev_t1, t.s_comp));
     A3G_CUDA(cudaStreamSynchronize(t.s_comp));
     A3G_CUDA(cudaStreamSynchronize(t.s_samp));
-    A3G_CUDA(cudaStreamSynchronize(t.s_samp2));
+    for (int j = 1; j < TrainerState::kSampStreams; ++j) A3G_CUDA(cudaStreamSynchronize(t.s_sx[j]));
     if (tl0) {  // end time of every traced launch, relative to the first traced step's start
       for (const TlEvent& e : g_tl) {
         float ms = 0;
         cudaEventElapsedTime(&ms, tl0, e.ev);
         std::fprintf(stderr, "a3g-timeline %s %s %.1f\n",
-                     e.st == t.s_comp ? "comp" : (e.st == t.s_samp ? "samp0" : "samp1"), e.name, ms * 1e3);
+                     e.st == t.s_comp ? "comp" : "samp", e.name, ms * 1e3);
         cudaEventDestroy(e.ev);
       }
       g_tl.clear();

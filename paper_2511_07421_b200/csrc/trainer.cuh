@@ -12,9 +12,9 @@ struct TrainerState {
   // sampling stream i % 2 -- two batches are sampled concurrently (the
   // sampler's many small latency-bound kernels interleave) while compute
   // consumes in order; an arena is reused only after its step's compute.
-  static constexpr int kArenas = 3;
-  static constexpr int kSampStreams = 2;
-  a3g_sampler* smp[kArenas] = {nullptr, nullptr, nullptr};
+  static constexpr int kArenas = 5;
+  static constexpr int kSampStreams = 4;
+  a3g_sampler* smp[kArenas] = {};
   uint32_t F = 0, H = 0, C = 0, pitch = 0, L = 0, max_seeds = 0;
   double lr = 0.2;
   uint64_t cap_inner = 0;
@@ -44,7 +44,7 @@ struct TrainerState {
   uint64_t h_seed_cap = 0;
   double* h_losses = nullptr;        // pinned
   cudaStream_t s_comp = nullptr, s_samp = nullptr;  // s_samp: sampling stream 0
-  cudaStream_t s_samp2 = nullptr;                     // sampling stream 1
+  cudaStream_t s_sx[kSampStreams] = {};              // sampling streams (s_sx[0] == s_samp)
   cudaEvent_t ev_sampled[kArenas] = {}, ev_consumed[kArenas] = {};
   cudaEvent_t ev_seeds = nullptr;                     // host seeds copied (sampling streams wait on it)
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;

@@ -113,6 +113,7 @@ _SIGS = {
     "a3g_trainer_set_weights": (C.c_int, [vp, f64p, f64p]),
     "a3g_trainer_get_weights": (C.c_int, [vp, f64p, f64p]),
     "a3g_trainer_set_comm": (C.c_int, [vp, vp]),
+    "a3g_trainer_set_pipeline": (C.c_int, [vp, C.c_int]),
     "a3g_train_step": (C.c_int, [vp, u32p, C.c_uint32, C.c_int, C.c_double, C.c_int, C.c_uint64, C.c_double,
                                  f64p]),
     "a3g_train_steps": (C.c_int, [vp, u32p, C.c_uint32, C.c_uint32, u64p, C.c_double, C.c_int, C.c_int, f64p]),

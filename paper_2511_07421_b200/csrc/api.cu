@@ -773,6 +773,14 @@ a3g_status a3g_trainer_get_weights(a3g_trainer* tr, double* w1, double* w2) {
   });
 }
 
+a3g_status a3g_trainer_set_pipeline(a3g_trainer* tr, int sampling_streams) {
+  return guard([&] {
+    if (sampling_streams < 0 || sampling_streams > TrainerState::kSampStreams)
+      raise(A3G_ERR_PARAMETER, "set_pipeline: sampling streams must be in [0, 4]");
+    tr->st.pipe_streams = sampling_streams;
+  });
+}
+
 a3g_status a3g_trainer_set_comm(a3g_trainer* tr, a3g_comm* comm) {
   return guard([&] { tr->st.comm = comm; });
 }
@@ -855,17 +863,19 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
     for (int j = 1; j < TrainerState::kSampStreams; ++j) A3G_CUDA(cudaStreamWaitEvent(t.s_sx[j], t.ev_seeds, 0));
     static const bool tl_env = std::getenv("A3G_TIMELINE") != nullptr;
     cudaEvent_t tl0 = nullptr;
+    const int nss = t.pipe_streams;  // 0: sequential -- sampling on the compute stream, depth 1
+    const int narenas = nss == 0 ? 1 : nss + 1;
     for (uint32_t i = 0; i < K; ++i) {
-      const int ar = static_cast<int>(i % TrainerState::kArenas);
+      const int ar = static_cast<int>(i % narenas);
       a3g_sampler* smp = t.smp[ar];
-      cudaStream_t ss = t.s_sx[i % TrainerState::kSampStreams];
+      cudaStream_t ss = nss == 0 ? t.s_comp : t.s_sx[i % nss];
       if (tl_env && K >= 4 && i == K / 2) {  // trace steps K/2 and K/2+1 (all streams)
         g_tl_on = true;
         A3G_CUDA(cudaEventCreate(&tl0));
         A3G_CUDA(cudaEventRecord(tl0, t.s_comp));
       }
       if (tl_env && K >= 4 && i == K / 2 + 2) g_tl_on = false;
-      if (i >= static_cast<uint32_t>(TrainerState::kArenas)) A3G_CUDA(cudaStreamWaitEvent(ss, t.ev_consumed[ar], 0));
+      if (i >= static_cast<uint32_t>(narenas)) A3G_CUDA(cudaStreamWaitEvent(ss, t.ev_consumed[ar], 0));
       sample_impl(smp->st, dseeds + off[i], static_cast<uint32_t>(off[i + 1] - off[i]), true, gamma, kind,
                   rng_seeds[i], ss);
       A3G_CUDA(cudaEventRecord(t.ev_sampled[ar], ss));

@@ -45,6 +45,7 @@ struct TrainerState {
   double* h_losses = nullptr;        // pinned
   cudaStream_t s_comp = nullptr, s_samp = nullptr;  // s_samp: sampling stream 0
   cudaStream_t s_sx[kSampStreams] = {};              // sampling streams (s_sx[0] == s_samp)
+  int pipe_streams = kSampStreams;  // a3g_trainer_set_pipeline: 0 = sequential (one stream), 1..kSampStreams
   cudaEvent_t ev_sampled[kArenas] = {}, ev_consumed[kArenas] = {};
   cudaEvent_t ev_seeds = nullptr;                     // host seeds copied (sampling streams wait on it)
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;

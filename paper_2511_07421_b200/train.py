@@ -171,6 +171,10 @@ class Trainer:
         b = np.ascontiguousarray(w2, dtype=np.float64)
         check(lib().a3g_trainer_set_weights(self.h, ptr(a, f64p), ptr(b, f64p)))
 
+    def set_pipeline(self, sampling_streams: int):
+        """0 = sequential (Mode::sequential), 1..4 concurrent sampling streams."""
+        check(lib().a3g_trainer_set_pipeline(self.h, int(sampling_streams)))
+
     def set_comm(self, comm):
         check(lib().a3g_trainer_set_comm(self.h, comm.h if comm is not None else None))
 

@@ -230,3 +230,25 @@ def test_device_feature_synthesis_matches_generator(feat_dtype):
     diff = out != want
     assert diff.mean() < 1e-5, diff.sum()
     np.testing.assert_allclose(out, want, rtol=1e-2 if feat_dtype else 1e-6, atol=1e-6)
+
+
+def test_pipeline_shapes_bit_identical(c1):
+    """Sequential mode and 1..4 concurrent sampling streams only change the
+    schedule (pipeline.hpp:107-109): losses, weights and per-step statistics
+    are bit-identical for every shape, over more steps than arenas."""
+    g = c1
+    spec = T.ModelSpec(g.feat_dim, 16, 4)
+    cache = CA.build_static_cache(g, CA.CacheConfig(int(0.2 * g.num_nodes) * g.feat_dim * 4, 1))
+    ref = None
+    for n in (0, 1, 2, 4):
+        tr = T.Trainer(g, cache, spec, [10, 5], max_seeds=512)
+        tr.set_pipeline(n)
+        got = _steps(tr, g, K=11)
+        if ref is None:
+            ref = got
+        else:
+            assert np.array_equal(got[0], ref[0]), n
+            assert all(np.array_equal(a, b) for a, b in zip(got[1], ref[1])), n
+            assert np.array_equal(got[2], ref[2]), n
+    with pytest.raises(Exception):
+        tr.set_pipeline(5)

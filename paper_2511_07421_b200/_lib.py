@@ -11,7 +11,7 @@ import os
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liba3g_b200.so")
+LIB_PATH = os.environ.get("A3G_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "liba3g_b200.so")
 
 u8p = C.POINTER(C.c_uint8)
 u32p = C.POINTER(C.c_uint32)

@@ -80,6 +80,27 @@ struct SampleArgs {
   int wmode;  // 0: all weights 1; 1: all gamma; 2: bitmap
 };
 
+// Prefilter word of mix64(c) (rng.hpp:13-20) for the hot stream loops: the
+// high word h4 of the second product, before the final z ^= z >> 31, so that
+// x_hi = mix64(c) >> 32 is h4 or h4 ^ 1 and x_hi >= t implies h4 >= t - 1.
+// The second multiply forms only its high word. ~9 alu + ~6 fma instructions
+// per position instead of ~19 alu + 8 fma for the full 64-bit mix64; measured
+// 1.37 vs 1.01 Tpositions/s on a B200 (tools/microbench/hash_pipes.cu).
+__device__ __forceinline__ uint32_t mix64_pre(uint64_t c) {
+  const uint32_t lo = static_cast<uint32_t>(c), hi = static_cast<uint32_t>(c >> 32);
+  const uint32_t l1 = lo ^ __funnelshift_r(lo, hi, 30);
+  const uint32_t h1 = hi ^ (hi >> 30);
+  const uint64_t w = static_cast<uint64_t>(l1) * 0x1ce4e5b9u;
+  const uint32_t h2 = static_cast<uint32_t>(w >> 32) + l1 * 0xbf58476du + h1 * 0x1ce4e5b9u;
+  const uint32_t l2 = static_cast<uint32_t>(w);
+  const uint32_t l3 = l2 ^ __funnelshift_r(l2, h2, 27);
+  const uint32_t h3 = h2 ^ (h2 >> 27);
+  return __umulhi(l3, 0x133111ebu) + l3 * 0x94d049bbu + h3 * 0x133111ebu;
+}
+// prefilter bound for x_hi >= t
+__device__ __forceinline__ uint32_t pre_bound(uint32_t t) { return t ? t - 1u : 0u; }
+
+
 // Key policy of a launch (template dispatch on wmode).
 template <int WM>
 struct PolOf;
@@ -342,26 +363,32 @@ __device__ __forceinline__ uint32_t item_of(const uint32_t* lists, const uint32_
 // minimum, as std::min_element) -- the exact sequential slot history of
 // sampler.cpp:24-40. Items are length-sorted so a warp's groups carry equal
 // work; records of hub segments store row positions (the merge translates).
-// (key, slot) minimum over the G lanes of a group, first index on K-ties:
-// an integer butterfly (64-bit compare, lower slot on equal integers); keys
-// are K-monotone, so only another slot within the policy's tie window of the
-// minimum can share its K value -- then (rare) the exact K-order decides
-// (PolGammaAll; PolUnit keys are exact integers).
-template <int G, typename P, int SHIFT = 21>
+// (key, slot) minimum over the G lanes of a group, first index on K-ties.
+template <int G, typename P, bool DBL = false>
 __device__ __forceinline__ void grp_argmin(const P& pol, uint64_t my, uint32_t gl, uint64_t& thr, uint32_t& mp) {
-  // fast path: butterfly on the packed (top 32 key bits, slot) -- one 64-bit
-  // min per step; exact whenever no other slot shares the minimum's top bits
-  // (or, for K-ties, the next value): keys differing only below bit 21 are the
-  // sole ambiguity, and every K-tie window (<= 64 (gamma + 1) << 2^21) lies there
-  // SHIFT: 21 for 53-bit integer keys, 32 for fp64 bit patterns (exponent on top)
-  const uint32_t my32 = static_cast<uint32_t>(my >> SHIFT);
-  uint64_t pk = (static_cast<uint64_t>(my32) << 32) | gl;
+  // fast path: butterfly on a packed 32-bit (27-bit key bucket, 5-bit slot) --
+  // one 32-bit shuffle + min per step. Buckets are key * 2^27 in u-space
+  // (53-bit integer keys >> 26; fp64 keys in [0,1] scaled by 2^27, exact and
+  // monotone; the empty-slot sentinels clamp to the top bucket), so
+  // bucket order is key order except within a bucket; every K-tie window
+  // (<= 64 (gamma + 1) integer units) spans at most two adjacent buckets. The
+  // packed minimum is therefore exact unless another slot sits in the
+  // minimum's bucket or the next one -- then the exact 64-bit K-order decides
+  // (first slot on K-ties, as std::min_element).
+  uint32_t my27;
+  if (DBL) {
+    const double d = __longlong_as_double(static_cast<long long>(my));
+    my27 = d >= 1.0 ? 0x7ffffffu : static_cast<uint32_t>(d * 0x1.0p27);
+  } else {
+    my27 = (my >> 26) < 0x7ffffffull ? static_cast<uint32_t>(my >> 26) : 0x7ffffffu;
+  }
+  uint32_t pk = (my27 << 5) | gl;
 #pragma unroll
   for (int off = G / 2; off > 0; off >>= 1) pk = min(pk, __shfl_xor_sync(kFull, pk, off, G));
-  const uint32_t m32 = static_cast<uint32_t>(pk >> 32);
-  uint32_t i = static_cast<uint32_t>(pk);
+  const uint32_t m27 = pk >> 5;
+  uint32_t i = pk & 31u;
   uint64_t k = __shfl_sync(kFull, my, static_cast<int>(i), G);
-  if (__any_sync(kFull, gl != i && my != ~0ull && my32 - m32 <= 1u)) {
+  if (__any_sync(kFull, gl != i && my27 - m27 <= 1u)) {
     // exact pass: first slot whose K equals the minimum's K
     uint64_t kk = my;
     uint32_t ii = gl;
@@ -471,23 +498,29 @@ __global__ void __launch_bounds__(256) k_stream_grp(SampleArgs a, const uint32_t
     uint32_t len = live && p1 > jb ? p1 - jb : 0u;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) len = max(len, __shfl_xor_sync(kFull, len, off));
-    uint64_t thrx = (thr << 11) | 0x7ffull;
+    // filter on the high key word: x > thr << 11 | 0x7ff needs x_hi >= thr >> 21
+    // (a superset; the rare equal-high-word false positives fail the exact
+    // test below, which recomputes the full draw for the candidates only)
+    uint32_t thi = pre_bound(static_cast<uint32_t>(thr >> 21));
     uint64_t ctr = key + (static_cast<uint64_t>(jb) + gl + 1) * kPhi;
     for (uint32_t b = 0; b < len; b += 32, ctr += 32 * kPhi) {
-      uint64_t x[U];
+      const uint32_t q = jb + b + gl;
+      const uint32_t rem = live && q < p1 ? p1 - q : 0u;
       bool c[U];
       bool anyc = false;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        x[u] = mix64(ctr + u * kStepG);
-        c[u] = jb + b + u * G + gl < p1 && x[u] > thrx;
+        const uint32_t h = mix64_pre(ctr + u * kStepG);  // unconditional: no branch
+        c[u] = (static_cast<uint32_t>(u * G) < rem) & (h >= thi);
         anyc |= c[u];
       }
       if (!__any_sync(kFull, anyc)) continue;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const uint64_t kk = x[u] >> 11;
-        unsigned mask = __ballot_sync(kFull, c[u] && kk > thr) & gmask;
+        if (!__any_sync(kFull, c[u])) continue;
+        const uint64_t kk = c[u] ? mix64(ctr + u * kStepG) >> 11 : 0ull;
+        const bool cu = c[u] && kk > thr;
+        unsigned mask = __ballot_sync(kFull, cu) & gmask;
         while (__any_sync(kFull, mask != 0)) {
           const int src = mask ? __ffs(mask) - 1 : lane;
           const uint64_t kv = __shfl_sync(kFull, kk, src);
@@ -512,10 +545,10 @@ __global__ void __launch_bounds__(256) k_stream_grp(SampleArgs a, const uint32_t
             mp = nmp;
           }
           if (mask) mask &= ~((2u << src) - 1u);
-          mask &= __ballot_sync(kFull, c[u] && kk > thr) & gmask;
+          mask &= __ballot_sync(kFull, cu && kk > thr) & gmask;
         }
       }
-      thrx = (thr << 11) | 0x7ffull;
+      thi = pre_bound(static_cast<uint32_t>(thr >> 21));
     }
     if (!live) continue;
     if (seg) {
@@ -594,7 +627,7 @@ __global__ void __launch_bounds__(256) k_stream_grp_mixed(SampleArgs a, const ui
     }
     uint64_t thrb;
     uint32_t mp;
-    grp_argmin<G, rsv::PolUnit, 32>(ipol, my_key, gl, thrb, mp);
+    grp_argmin<G, rsv::PolUnit, true>(ipol, my_key, gl, thrb, mp);
     double thr = __longlong_as_double(thrb);
     double lo = rsv::gamma_lo(thr, gamma);
     uint32_t rcnt = nf;
@@ -644,7 +677,7 @@ __global__ void __launch_bounds__(256) k_stream_grp_mixed(SampleArgs a, const ui
           if (ins) ++rcnt;
           uint64_t nthr;
           uint32_t nmp;
-          grp_argmin<G, rsv::PolUnit, 32>(ipol, my_key, gl, nthr, nmp);
+          grp_argmin<G, rsv::PolUnit, true>(ipol, my_key, gl, nthr, nmp);
           if (ins) {
             thr = __longlong_as_double(nthr);
             mp = nmp;

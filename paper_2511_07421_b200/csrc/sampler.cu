@@ -86,16 +86,21 @@ struct SampleArgs {
 // The second multiply forms only its high word. ~9 alu + ~6 fma instructions
 // per position instead of ~19 alu + 8 fma for the full 64-bit mix64; measured
 // 1.37 vs 1.01 Tpositions/s on a B200 (tools/microbench/hash_pipes.cu).
-__device__ __forceinline__ uint32_t mix64_pre(uint64_t c) {
+__device__ __forceinline__ uint32_t mix64_pre(uint64_t c, uint32_t& l3) {
   const uint32_t lo = static_cast<uint32_t>(c), hi = static_cast<uint32_t>(c >> 32);
   const uint32_t l1 = lo ^ __funnelshift_r(lo, hi, 30);
   const uint32_t h1 = hi ^ (hi >> 30);
   const uint64_t w = static_cast<uint64_t>(l1) * 0x1ce4e5b9u;
   const uint32_t h2 = static_cast<uint32_t>(w >> 32) + l1 * 0xbf58476du + h1 * 0x1ce4e5b9u;
   const uint32_t l2 = static_cast<uint32_t>(w);
-  const uint32_t l3 = l2 ^ __funnelshift_r(l2, h2, 27);
+  l3 = l2 ^ __funnelshift_r(l2, h2, 27);
   const uint32_t h3 = h2 ^ (h2 >> 27);
   return __umulhi(l3, 0x133111ebu) + l3 * 0x94d049bbu + h3 * 0x133111ebu;
+}
+// the full draw from the prefilter state (h4, l3): == mix64(c) >> 11
+__device__ __forceinline__ uint64_t mix64_finish_key(uint32_t h4, uint32_t l3) {
+  const uint64_t z = (static_cast<uint64_t>(h4) << 32) | (l3 * 0x133111ebu);
+  return (z ^ (z >> 31)) >> 11;
 }
 // prefilter bound for x_hi >= t
 __device__ __forceinline__ uint32_t pre_bound(uint32_t t) { return t ? t - 1u : 0u; }
@@ -500,25 +505,26 @@ __global__ void __launch_bounds__(256) k_stream_grp(SampleArgs a, const uint32_t
     for (int off = 16; off > 0; off >>= 1) len = max(len, __shfl_xor_sync(kFull, len, off));
     // filter on the high key word: x > thr << 11 | 0x7ff needs x_hi >= thr >> 21
     // (a superset; the rare equal-high-word false positives fail the exact
-    // test below, which recomputes the full draw for the candidates only)
+    // test below, which finishes the full draw for the candidates only)
     uint32_t thi = pre_bound(static_cast<uint32_t>(thr >> 21));
     uint64_t ctr = key + (static_cast<uint64_t>(jb) + gl + 1) * kPhi;
     for (uint32_t b = 0; b < len; b += 32, ctr += 32 * kPhi) {
       const uint32_t q = jb + b + gl;
       const uint32_t rem = live && q < p1 ? p1 - q : 0u;
       bool c[U];
+      uint32_t h4[U], l3[U];
       bool anyc = false;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const uint32_t h = mix64_pre(ctr + u * kStepG);  // unconditional: no branch
-        c[u] = (static_cast<uint32_t>(u * G) < rem) & (h >= thi);
+        h4[u] = mix64_pre(ctr + u * kStepG, l3[u]);  // unconditional: no branch
+        c[u] = (static_cast<uint32_t>(u * G) < rem) & (h4[u] >= thi);
         anyc |= c[u];
       }
       if (!__any_sync(kFull, anyc)) continue;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (!__any_sync(kFull, c[u])) continue;
-        const uint64_t kk = c[u] ? mix64(ctr + u * kStepG) >> 11 : 0ull;
+        const uint64_t kk = c[u] ? mix64_finish_key(h4[u], l3[u]) : 0ull;
         const bool cu = c[u] && kk > thr;
         unsigned mask = __ballot_sync(kFull, cu) & gmask;
         while (__any_sync(kFull, mask != 0)) {

@@ -572,6 +572,161 @@ __global__ void __launch_bounds__(256) k_stream_grp(SampleArgs a, const uint32_t
   }
 }
 
+// Lane-per-item stream for wide layers (integer-key policies, m <= MB): each
+// lane owns one item with its reservoir in registers (MB fully unrolled
+// slots), hashes positions in chunks of 32 into a candidate bitmask with the
+// prefilter, then replays its candidates exactly in position order -- all
+// lanes in lockstep, one candidate per lane per step. Against the lane-group
+// kernel this spends one lane (not G) per item on hashing and serves 32 items
+// (not 32/G) per replay step; it needs many items to fill the machine, so the
+// host selects it by the layer's frontier bound.
+// K of an integer key under PolGammaAll (out of line: rare near-tie path)
+__device__ __noinline__ double key_pow(uint64_t x, double inv_g) { return pow(rsv::u_of(x), inv_g); }
+
+template <int MB, typename P>
+__device__ __forceinline__ void lane_argmin(const P& pol, const uint64_t (&rk)[MB], uint32_t m, uint64_t& thr,
+                                            uint32_t& mp) {
+  uint64_t mn = rk[0];
+  uint32_t mi = 0;
+#pragma unroll
+  for (int i = 1; i < MB; ++i)
+    if (rk[i] < mn) {  // strict: first slot on equal integers
+      mn = rk[i];
+      mi = i;
+    }
+  if constexpr (P::kNearTies) {  // another slot within the tie window may hold an equal K
+    bool near = false;
+#pragma unroll
+    for (int i = 0; i < MB; ++i) near |= static_cast<uint32_t>(i) != mi && rk[i] != ~0ull && rk[i] - mn <= pol.tie;
+    if (near) {  // exact K-order, first slot on K-ties (std::min_element)
+      double bk = key_pow(rk[0], pol.inv_g);
+      mn = rk[0];
+      mi = 0;
+#pragma unroll
+      for (int i = 1; i < MB; ++i)
+        if (rk[i] != ~0ull) {
+          const double ki = key_pow(rk[i], pol.inv_g);
+          if (ki < bk) {
+            bk = ki;
+            mn = rk[i];
+            mi = i;
+          }
+        }
+    }
+  }
+  thr = mn;
+  mp = mi;
+}
+
+template <int WM, int MB>
+__global__ void __launch_bounds__(256) k_stream_lane(SampleArgs a, const uint32_t* lists, const uint32_t* cls_count) {
+  using P = typename PolOf<WM>::P;
+  const int lane = threadIdx.x & 31;
+  const uint32_t nitems = min(*a.item_count, a.hub.item_cap);
+  const uint32_t m = a.f;
+  const P pol = PolOf<WM>::make(a);
+  for (;;) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(a.item_work, 32u);
+    base = __shfl_sync(kFull, base, 0);
+    if (base >= nitems) break;
+    const uint32_t ii = base + lane;
+    const bool live = ii < nitems;
+    uint4 im = make_uint4(0, 0, 0, kInv);
+    uint32_t dst = 0;
+    uint64_t beg = 0;
+    if (live) {
+      im = a.hub.items[item_of(lists, cls_count, a.hub.item_cap, ii)];
+      dst = __ldg(a.front + im.x);
+      beg = __ldg(a.ro + dst);
+    }
+    const uint64_t key = hash2(a.seed, hash2(a.layer, dst));
+    const bool seg = im.w != kInv;
+    const uint32_t p0 = im.y, p1 = live ? im.z : im.y;
+    uint32_t* rid = a.hub.rec_id + static_cast<uint64_t>(seg ? im.w : 0) * kRecCap;
+    uint64_t* rkey = a.hub.rec_key + static_cast<uint64_t>(seg ? im.w : 0) * kRecCap;
+    // ---- fill (sampler.cpp:30-33)
+    const uint32_t nf = min(m, p1 - p0);
+    uint64_t rk[MB];
+    uint32_t rp[MB];
+#pragma unroll
+    for (int i = 0; i < MB; ++i) {
+      rk[i] = ~0ull;
+      rp[i] = 0;
+      if (static_cast<uint32_t>(i) < nf) {
+        rk[i] = draw(key, static_cast<uint64_t>(p0) + i + 1) >> 11;
+        rp[i] = p0 + i;
+        if (seg) {
+          rid[i] = rp[i];
+          rkey[i] = rk[i];
+        }
+      }
+    }
+    uint64_t thr;
+    uint32_t mp;
+    lane_argmin<MB>(pol, rk, m, thr, mp);
+    uint32_t rcnt = nf;
+    // ---- replay [p0 + nf, p1) in chunks of 32 positions
+    const uint32_t jb = p0 + nf;
+    const uint32_t len = p1 > jb ? p1 - jb : 0u;
+    uint32_t wlen = len;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) wlen = max(wlen, __shfl_xor_sync(kFull, wlen, off));
+    uint64_t ctr = key + (static_cast<uint64_t>(jb) + 1) * kPhi;  // draw index of position jb
+    for (uint32_t b = 0; b < wlen; b += 32, ctr += 32 * kPhi) {
+      const uint32_t thi = pre_bound(static_cast<uint32_t>(thr >> 21));
+      uint32_t cm = 0;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        uint32_t l3;
+        const uint32_t h4 = mix64_pre(ctr + static_cast<uint64_t>(c) * kPhi, l3);
+        cm |= static_cast<uint32_t>(h4 >= thi) << c;
+      }
+      const uint32_t rem = len > b ? len - b : 0u;
+      if (rem < 32) cm &= (1u << rem) - 1u;
+      while (__any_sync(kFull, cm != 0)) {
+        if (cm) {
+          const int c = __ffs(cm) - 1;
+          cm &= cm - 1;
+          const uint64_t kx = mix64(ctr + static_cast<uint64_t>(c) * kPhi) >> 11;
+          if (pol.gt(kx, thr)) {
+            const uint32_t pos = jb + b + c;
+#pragma unroll
+            for (int i = 0; i < MB; ++i)
+              if (static_cast<uint32_t>(i) == mp) {
+                rk[i] = kx;
+                rp[i] = pos;
+              }
+            if (seg && rcnt < kRecCap) {
+              rid[rcnt] = pos;
+              rkey[rcnt] = kx;
+            }
+            ++rcnt;
+            lane_argmin<MB>(pol, rk, m, thr, mp);
+          }
+        }
+      }
+    }
+    if (!live) continue;
+    if (seg) {
+      a.hub.rec_cnt[im.w] = rcnt;
+      a.hub.tau[im.w] = thr;
+      a.hub.tau_ok[im.w] = (p1 - p0 >= m) ? 1u : 0u;
+    } else {
+      const uint32_t* nb = a.col + beg;
+      const uint64_t row0 = static_cast<uint64_t>(im.x) * m;
+#pragma unroll
+      for (int i = 0; i < MB; ++i)
+        if (static_cast<uint32_t>(i) < m) {
+          const uint32_t id = __ldg(nb + rp[i]);
+          a.S[row0 + i] = id;
+          mark_first(a.first, id, a.tag, static_cast<uint32_t>(row0 + i));
+        }
+      a.cnt[im.x] = m;
+    }
+  }
+}
+
 // Bitmap-weighted items (partial cache, gamma > 1: w = gamma if cached else
 // 1, assign_weights sampler.cpp:60-68) by lane groups, as k_stream_grp but
 // with fp64 keys: each position needs its neighbour id (the cached bit), and a
@@ -1522,8 +1677,11 @@ __global__ void k_gather_unique(const __grid_constant__ StoreView view, uint32_t
   }
 }
 
+// frontier bound from which a layer's integer-key items go lane-per-item
+constexpr uint64_t kLaneMinRows = 32768;
+
 template <int WM>
-void launch_layer_kernels(const SampleArgs& sa, int sm_count, cudaStream_t st) {
+void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_count, cudaStream_t st) {
   k_classify<WM><<<sm_count * 2, 256, 0, st>>>(sa);
   A3G_LAUNCH_DONE("k_classify", st);
   if (sa.f <= 32) {
@@ -1551,6 +1709,12 @@ void launch_layer_kernels(const SampleArgs& sa, int sm_count, cudaStream_t st) {
         else
           k_stream_grp_mixed<32><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         A3G_LAUNCH_DONE("k_stream_grp_mixed", st);
+      } else if (sa.kind != A3G_SAMPLER_UNIFORM && sa.f <= 16 && rows_bound >= kLaneMinRows) {
+        if (sa.f <= 8)
+          k_stream_lane<W, 8><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
+        else
+          k_stream_lane<W, 16><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
+        A3G_LAUNCH_DONE("k_stream_lane", st);
       } else {
         if (sa.f <= 8)
           k_stream_grp<W, 8><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
@@ -1647,11 +1811,11 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
     sa.kind = kind;
     sa.wmode = wmode;
     if (wmode == 1)
-      launch_layer_kernels<1>(sa, s.sm_count, st);
+      launch_layer_kernels<1>(sa, la.cap_rows, s.sm_count, st);
     else if (wmode == 2)
-      launch_layer_kernels<2>(sa, s.sm_count, st);
+      launch_layer_kernels<2>(sa, la.cap_rows, s.sm_count, st);
     else
-      launch_layer_kernels<0>(sa, s.sm_count, st);
+      launch_layer_kernels<0>(sa, la.cap_rows, s.sm_count, st);
     FinArgs fa{};
     fa.S = la.S;
     fa.cnt = la.cnt;

@@ -160,6 +160,8 @@ struct a3g_cache {
   uint32_t num_devices = 1;
   uint64_t total_cached = 0;
   uint32_t* d_bits = nullptr;  // n bits: cached on any device
+  uint32_t* d_ebits = nullptr; // m bits (+1 pad word): cached bit of every CSR edge's target
+                               // (partial caches only; the lane-per-item mixed stream)
   bool all_cached = false, none_cached = true;
 };
 

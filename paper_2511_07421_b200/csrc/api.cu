@@ -379,6 +379,15 @@ static a3g_cache* cache_from(a3g_graph* g, std::vector<int32_t>&& dm, uint32_t n
   A3G_CUDA(cudaSetDevice(g->device));
   c->d_bits = dalloc<uint32_t>(bits.size());
   A3G_CUDA(cudaMemcpy(c->d_bits, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice));
+  if (!c->all_cached && !c->none_cached && g->m) {
+    const uint64_t words = (g->m + 31) / 32 + 1;
+    c->d_ebits = dalloc<uint32_t>(words);
+    A3G_CUDA(cudaMemset(c->d_ebits, 0, words * 4));
+    int sms = 0;
+    A3G_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
+    build_edge_bits(g->d_col, g->m, c->d_bits, c->d_ebits, sms, 0);
+    A3G_CUDA(cudaDeviceSynchronize());
+  }
   return c;
 }
 
@@ -425,6 +434,7 @@ uint64_t a3g_cache_total_cached(const a3g_cache* c) { return c->total_cached; }
 void a3g_cache_destroy(a3g_cache* c) {
   if (!c) return;
   dfree(c->d_bits);
+  dfree(c->d_ebits);
   delete c;
 }
 

@@ -56,6 +56,7 @@ struct SampleArgs {
   const uint64_t* ro;
   const uint32_t* col;
   const uint32_t* bits;
+  const uint32_t* ebits;  // per-edge cached bits (partial caches), or null
   const uint32_t* front;
   const uint32_t* nrows;  // device count of frontier rows
   uint32_t* cnt;
@@ -101,6 +102,13 @@ __device__ __forceinline__ uint32_t mix64_pre(uint64_t c, uint32_t& l3) {
 __device__ __forceinline__ uint64_t mix64_finish_key(uint32_t h4, uint32_t l3) {
   const uint64_t z = (static_cast<uint64_t>(h4) << 32) | (l3 * 0x133111ebu);
   return (z ^ (z >> 31)) >> 11;
+}
+// High-word bound of unit keys u >= lo: u = (x >> 11) 2^-53 >= lo needs
+// x >> 11 >= ceil(lo 2^53), hence x_hi >= ceil(lo 2^53) >> 21.
+__device__ __forceinline__ uint32_t lo_hi_word(double lo) {
+  if (!(lo > 0.0)) return 0u;
+  if (lo >= 1.0) return 0xffffffffu;
+  return static_cast<uint32_t>(static_cast<uint64_t>(ceil(lo * 0x1.0p53)) >> 21);
 }
 // prefilter bound for x_hi >= t
 __device__ __forceinline__ uint32_t pre_bound(uint32_t t) { return t ? t - 1u : 0u; }
@@ -724,6 +732,167 @@ __global__ void __launch_bounds__(256) k_stream_lane(SampleArgs a, const uint32_
         }
       a.cnt[im.x] = m;
     }
+  }
+}
+
+// Lane-per-item stream for bitmap weights (partial cache, gamma > 1), m <= MB:
+// as k_stream_lane with fp64 keys (their IEEE bits order like the values, so
+// the register argmin compares bit patterns). Each 32-position chunk reads the
+// chunk's 32 per-edge cached bits (a3g_cache::d_ebits, two words) instead of
+// 32 adjacency entries + 32 bitmap words; the prefilter bound per position is
+// lo = thr^gamma (1 - 1e-6) for cached targets (k = u^(1/gamma) can beat thr
+// only if u >= lo, reservoir.cuh PolMixed) and thr for the others (k = u).
+// Both bounds are taken at the chunk start: they only grow, so stale bounds
+// only add candidates, each tested exactly in position order.
+template <int MB>
+__global__ void __launch_bounds__(256) k_stream_lane_mixed(SampleArgs a, const uint32_t* lists,
+                                                           const uint32_t* cls_count) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nitems = min(*a.item_count, a.hub.item_cap);
+  const uint32_t m = a.f;
+  const double ig = a.inv_gamma, gamma = a.gamma;
+  const uint32_t* eb = a.ebits;
+  const rsv::PolUnit ipol{};
+  for (;;) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(a.item_work, 32u);
+    base = __shfl_sync(kFull, base, 0);
+    if (base >= nitems) break;
+    const uint32_t ii = base + lane;
+    const bool live = ii < nitems;
+    uint4 im = make_uint4(0, 0, 0, kInv);
+    uint32_t dst = 0;
+    uint64_t beg = 0;
+    if (live) {
+      im = a.hub.items[item_of(lists, cls_count, a.hub.item_cap, ii)];
+      dst = __ldg(a.front + im.x);
+      beg = __ldg(a.ro + dst);
+    }
+    const uint64_t key = hash2(a.seed, hash2(a.layer, dst));
+    const bool seg = im.w != kInv;
+    const uint32_t p0 = im.y, p1 = live ? im.z : im.y;
+    uint32_t* rid = a.hub.rec_id + static_cast<uint64_t>(seg ? im.w : 0) * kRecCap;
+    uint64_t* rkey = a.hub.rec_key + static_cast<uint64_t>(seg ? im.w : 0) * kRecCap;
+    auto ebit = [&](uint64_t e) { return (__ldg(eb + (e >> 5)) >> (e & 31)) & 1u; };
+    // ---- fill (sampler.cpp:30-33)
+    const uint32_t nf = min(m, p1 - p0);
+    uint64_t rk[MB];
+    uint32_t rp[MB];
+#pragma unroll
+    for (int i = 0; i < MB; ++i) {
+      rk[i] = static_cast<uint64_t>(__double_as_longlong(INFINITY));
+      rp[i] = 0;
+      if (static_cast<uint32_t>(i) < nf) {
+        const uint32_t j = p0 + i;
+        const double u = unit_of(draw(key, static_cast<uint64_t>(j) + 1));
+        const double k = ebit(beg + j) ? pow(u, ig) : u;
+        rk[i] = static_cast<uint64_t>(__double_as_longlong(k));
+        rp[i] = j;
+        if (seg) {
+          rid[i] = j;
+          rkey[i] = rk[i];
+        }
+      }
+    }
+    uint64_t thrb;
+    uint32_t mp;
+    lane_argmin<MB>(ipol, rk, m, thrb, mp);
+    uint32_t rcnt = nf;
+    const uint32_t jb = p0 + nf;
+    const uint32_t len = p1 > jb ? p1 - jb : 0u;
+    uint32_t wlen = len;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) wlen = max(wlen, __shfl_xor_sync(kFull, wlen, off));
+    uint64_t ctr = key + (static_cast<uint64_t>(jb) + 1) * kPhi;
+    for (uint32_t b = 0; b < wlen; b += 32, ctr += 32 * kPhi) {
+      const double thr = __longlong_as_double(static_cast<long long>(thrb));
+      const double lo = rsv::gamma_lo(thr, gamma);
+      const uint32_t b_thr = pre_bound(lo_hi_word(thr)), b_lo = pre_bound(lo_hi_word(lo));
+      const uint32_t rem = len > b ? len - b : 0u;
+      uint32_t cb = 0;
+      if (rem) {
+        const uint64_t e0 = beg + jb + b;
+        cb = __funnelshift_r(__ldg(eb + (e0 >> 5)), __ldg(eb + (e0 >> 5) + 1), static_cast<uint32_t>(e0 & 31));
+      }
+      uint32_t cm = 0;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        uint32_t l3;
+        const uint32_t h4 = mix64_pre(ctr + static_cast<uint64_t>(c) * kPhi, l3);
+        cm |= static_cast<uint32_t>(h4 >= (((cb >> c) & 1u) ? b_lo : b_thr)) << c;
+      }
+      if (rem < 32) cm &= (1u << rem) - 1u;
+      while (__any_sync(kFull, cm != 0)) {
+        if (cm) {
+          const int c = __ffs(cm) - 1;
+          cm &= cm - 1;
+          const double t = __longlong_as_double(static_cast<long long>(thrb));
+          const double uu = unit_of(mix64(ctr + static_cast<uint64_t>(c) * kPhi));
+          double k = uu;
+          bool ins;
+          if ((cb >> c) & 1u) {
+            ins = uu >= lo;  // lo of the chunk start <= the current one
+            if (ins) {
+              k = pow(uu, ig);
+              ins = k > t;
+            }
+          } else {
+            ins = uu > t;
+          }
+          if (ins) {
+            const uint32_t pos = jb + b + c;
+            const uint64_t kb = static_cast<uint64_t>(__double_as_longlong(k));
+#pragma unroll
+            for (int i = 0; i < MB; ++i)
+              if (static_cast<uint32_t>(i) == mp) {
+                rk[i] = kb;
+                rp[i] = pos;
+              }
+            if (seg && rcnt < kRecCap) {
+              rid[rcnt] = pos;
+              rkey[rcnt] = kb;
+            }
+            ++rcnt;
+            lane_argmin<MB>(ipol, rk, m, thrb, mp);
+          }
+        }
+      }
+    }
+    if (!live) continue;
+    if (seg) {
+      a.hub.rec_cnt[im.w] = rcnt;
+      a.hub.tau[im.w] = thrb;
+      a.hub.tau_ok[im.w] = (p1 - p0 >= m) ? 1u : 0u;
+    } else {
+      const uint32_t* nb = a.col + beg;
+      const uint64_t row0 = static_cast<uint64_t>(im.x) * m;
+#pragma unroll
+      for (int i = 0; i < MB; ++i)
+        if (static_cast<uint32_t>(i) < m) {
+          const uint32_t id = __ldg(nb + rp[i]);
+          a.S[row0 + i] = id;
+          mark_first(a.first, id, a.tag, static_cast<uint32_t>(row0 + i));
+        }
+      a.cnt[im.x] = m;
+    }
+  }
+}
+
+// Per-edge cached bits: warp per 32 consecutive edges (coalesced adjacency
+// reads), one ballot per word.
+__global__ void k_edge_bits(const uint32_t* col, uint64_t m, const uint32_t* bits, uint32_t* ebits) {
+  const uint64_t nw = (m + 31) / 32;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t w = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; w < nw;
+       w += (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const uint64_t e = w * 32 + lane;
+    bool c = false;
+    if (e < m) {
+      const uint32_t v = __ldg(col + e);
+      c = (__ldg(bits + (v >> 5)) >> (v & 31)) & 1u;
+    }
+    const unsigned word = __ballot_sync(kFull, c);
+    if (lane == 0) ebits[w] = word;
   }
 }
 
@@ -1701,7 +1870,13 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
       const uint32_t* lists = hb.sort_keys[0];
       constexpr int W = WM == 2 ? 0 : WM;
       const int grid = sm_count * 8;
-      if (WM == 2 && sa.kind != A3G_SAMPLER_UNIFORM) {
+      if (WM == 2 && sa.kind != A3G_SAMPLER_UNIFORM && sa.ebits && sa.f <= 16 && rows_bound >= kLaneMinRows) {
+        if (sa.f <= 8)
+          k_stream_lane_mixed<8><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
+        else
+          k_stream_lane_mixed<16><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
+        A3G_LAUNCH_DONE("k_stream_lane_mixed", st);
+      } else if (WM == 2 && sa.kind != A3G_SAMPLER_UNIFORM) {
         if (sa.f <= 8)
           k_stream_grp_mixed<8><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         else if (sa.f <= 16)
@@ -1733,6 +1908,12 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
 }  // namespace
 
 // ------------------------------------------------------------ host side ----
+void build_edge_bits(const uint32_t* col, uint64_t m, const uint32_t* bits, uint32_t* ebits, int sm_count,
+                     cudaStream_t st) {
+  k_edge_bits<<<sm_count * 8, 256, 0, st>>>(col, m, bits, ebits);
+  A3G_LAUNCH_DONE("k_edge_bits", st);
+}
+
 void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, uint64_t rng_seed,
                    cudaStream_t st) {
   a3g_graph* g = s.g;
@@ -1785,6 +1966,7 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
     sa.ro = g->d_ro;
     sa.col = g->d_col;
     sa.bits = c->d_bits;
+    sa.ebits = c->d_ebits;
     sa.front = la.front;
     sa.nrows = &ctr->nfront[l];
     sa.cnt = la.cnt;

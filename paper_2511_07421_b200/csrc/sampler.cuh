@@ -89,6 +89,9 @@ void launch_reservoir_list(const uint32_t* d_nb, const double* d_w, uint64_t deg
                            cudaStream_t st);
 // Gather unique rows to `out` (device f32, F contiguous) and count hits/misses.
 void launch_gather_unique(SamplerState& s, float* out, cudaStream_t st);
+// per-edge cached bits of a partial cache: ebits[e / 32] bit e % 32 = bits[col[e]]
+void build_edge_bits(const uint32_t* col, uint64_t m, const uint32_t* bits, uint32_t* ebits, int sm_count,
+                     cudaStream_t st);
 
 }  // namespace a3g
 

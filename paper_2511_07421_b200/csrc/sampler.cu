@@ -33,6 +33,7 @@
 //                   the first position, tile partials, ballot scans).
 // Counts stay on the device: no host sync inside a batch.
 #include <cmath>
+#include <cstdlib>
 
 #include <cub/device/device_radix_sort.cuh>
 
@@ -1846,8 +1847,15 @@ __global__ void k_gather_unique(const __grid_constant__ StoreView view, uint32_t
   }
 }
 
-// frontier bound from which a layer's integer-key items go lane-per-item
-constexpr uint64_t kLaneMinRows = 32768;
+// frontier bound from which a layer's items go lane-per-item (A3G_LANE_MIN_ROWS
+// overrides it for tuning sweeps)
+static uint64_t lane_min_rows() {
+  static const uint64_t v = [] {
+    const char* e = std::getenv("A3G_LANE_MIN_ROWS");
+    return e ? std::strtoull(e, nullptr, 10) : 32768ull;
+  }();
+  return v;
+}
 
 template <int WM>
 void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_count, cudaStream_t st) {
@@ -1870,7 +1878,7 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
       const uint32_t* lists = hb.sort_keys[0];
       constexpr int W = WM == 2 ? 0 : WM;
       const int grid = sm_count * 8;
-      if (WM == 2 && sa.kind != A3G_SAMPLER_UNIFORM && sa.ebits && sa.f <= 16 && rows_bound >= kLaneMinRows) {
+      if (WM == 2 && sa.kind != A3G_SAMPLER_UNIFORM && sa.ebits && sa.f <= 16 && rows_bound >= lane_min_rows()) {
         if (sa.f <= 8)
           k_stream_lane_mixed<8><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         else
@@ -1884,7 +1892,7 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
         else
           k_stream_grp_mixed<32><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         A3G_LAUNCH_DONE("k_stream_grp_mixed", st);
-      } else if (sa.kind != A3G_SAMPLER_UNIFORM && sa.f <= 16 && rows_bound >= kLaneMinRows) {
+      } else if (sa.kind != A3G_SAMPLER_UNIFORM && sa.f <= 16 && rows_bound >= lane_min_rows()) {
         if (sa.f <= 8)
           k_stream_lane<W, 8><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         else

@@ -654,10 +654,9 @@ a3g_status a3g_trainer_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds, co
       t.lr = lr;
       t.max_seeds = max_seeds;
       t.sm_count = sm_count_of(g->device);
-      for (int i = 0; i < TrainerState::kArenas; ++i) {
-        t.smp[i] = new a3g_sampler;
-        sampler_alloc(t.smp[i]->st, g, c, max_seeds, fanouts, L);
-      }
+      t.fanouts.assign(fanouts, fanouts + L);
+      t.smp[0] = new a3g_sampler;
+      sampler_alloc(t.smp[0]->st, g, c, max_seeds, fanouts, L);
       t.cap_inner = std::max<uint64_t>(1, t.smp[0]->st.cap_inner);
       if (tc_h1_smem(t.F, H) > 227 * 1024)
         raise(A3G_ERR_PARAMETER, "trainer: feat_dim too large for the tcgen05 dense update (F <= 1280)");
@@ -685,7 +684,12 @@ a3g_status a3g_trainer_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds, co
       t.losses_cap = 1;
       t.d_losses = dalloc<double>(1);
       A3G_CUDA(cudaMallocHost(&t.h_losses, 8));
-      A3G_CUDA(cudaStreamCreateWithFlags(&t.s_comp, cudaStreamNonBlocking));
+      // the compute stream runs at the highest priority: it is the pipeline's
+      // serial chain; the sampling streams fill the SMs it leaves idle
+      int prio_lo = 0, prio_hi = 0;
+      A3G_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+      static const bool no_prio = std::getenv("A3G_NO_PRIORITY") != nullptr;
+      A3G_CUDA(cudaStreamCreateWithPriority(&t.s_comp, cudaStreamNonBlocking, no_prio ? prio_lo : prio_hi));
       A3G_CUDA(cudaStreamCreateWithFlags(&t.s_samp, cudaStreamNonBlocking));
       t.s_sx[0] = t.s_samp;
       for (int i = 1; i < TrainerState::kSampStreams; ++i)
@@ -786,7 +790,7 @@ a3g_status a3g_trainer_get_weights(a3g_trainer* tr, double* w1, double* w2) {
 a3g_status a3g_trainer_set_pipeline(a3g_trainer* tr, int sampling_streams) {
   return guard([&] {
     if (sampling_streams < 0 || sampling_streams > TrainerState::kSampStreams)
-      raise(A3G_ERR_PARAMETER, "set_pipeline: sampling streams must be in [0, 4]");
+      raise(A3G_ERR_PARAMETER, "set_pipeline: sampling streams must be in [0, 8]");
     tr->st.pipe_streams = sampling_streams;
   });
 }
@@ -872,9 +876,18 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
     A3G_CUDA(cudaEventRecord(t.ev_seeds, t.s_samp));
     for (int j = 1; j < TrainerState::kSampStreams; ++j) A3G_CUDA(cudaStreamWaitEvent(t.s_sx[j], t.ev_seeds, 0));
     static const bool tl_env = std::getenv("A3G_TIMELINE") != nullptr;
+    // A3G_STEP_TIMES=1: per step, sampling start / end and compute start / end (us)
+    static const bool steps_env = std::getenv("A3G_STEP_TIMES") != nullptr;
+    std::vector<cudaEvent_t> step_ev;
     cudaEvent_t tl0 = nullptr;
     const int nss = t.pipe_streams;  // 0: sequential -- sampling on the compute stream, depth 1
     const int narenas = nss == 0 ? 1 : nss + 1;
+    for (int i = 1; i < narenas; ++i)
+      if (!t.smp[i]) {
+        A3G_CUDA(cudaStreamSynchronize(t.s_comp));
+        t.smp[i] = new a3g_sampler;
+        sampler_alloc(t.smp[i]->st, t.g, t.c, t.max_seeds, t.fanouts.data(), t.L);
+      }
     for (uint32_t i = 0; i < K; ++i) {
       const int ar = static_cast<int>(i % narenas);
       a3g_sampler* smp = t.smp[ar];
@@ -886,13 +899,26 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
       }
       if (tl_env && K >= 4 && i == K / 2 + 2) g_tl_on = false;
       if (i >= static_cast<uint32_t>(narenas)) A3G_CUDA(cudaStreamWaitEvent(ss, t.ev_consumed[ar], 0));
+      cudaEvent_t se[4] = {};
+      if (steps_env) {
+        for (auto& e : se) A3G_CUDA(cudaEventCreate(&e));
+        A3G_CUDA(cudaEventRecord(se[0], ss));
+      }
       sample_impl(smp->st, dseeds + off[i], static_cast<uint32_t>(off[i + 1] - off[i]), true, gamma, kind,
                   rng_seeds[i], ss);
       A3G_CUDA(cudaEventRecord(t.ev_sampled[ar], ss));
       A3G_CUDA(cudaStreamWaitEvent(t.s_comp, t.ev_sampled[ar], 0));
+      if (steps_env) {
+        A3G_CUDA(cudaEventRecord(se[1], ss));
+        A3G_CUDA(cudaEventRecord(se[2], t.s_comp));
+      }
       launch_train_compute(t, smp, t.lr, t.d_losses + i, t.d_stats + static_cast<size_t>(i) * A3G_STEP_STATS,
                            t.s_comp, t.timing);
       A3G_CUDA(cudaEventRecord(t.ev_consumed[ar], t.s_comp));
+      if (steps_env) {
+        A3G_CUDA(cudaEventRecord(se[3], t.s_comp));
+        step_ev.insert(step_ev.end(), se, se + 4);
+      }
     }
     g_tl_on = false;
     A3G_CUDA(cudaMemcpyAsync(t.h_losses, t.d_losses, K * 8ull, cudaMemcpyDeviceToHost, t.s_comp));
@@ -900,6 +926,13 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
     A3G_CUDA(cudaStreamSynchronize(t.s_comp));
     A3G_CUDA(cudaStreamSynchronize(t.s_samp));
     for (int j = 1; j < TrainerState::kSampStreams; ++j) A3G_CUDA(cudaStreamSynchronize(t.s_sx[j]));
+    for (size_t q = 0; q + 3 < step_ev.size(); q += 4) {
+      float v[4];
+      for (int k = 0; k < 4; ++k) A3G_CUDA(cudaEventElapsedTime(&v[k], t.ev_t0, step_ev[q + k]));
+      std::fprintf(stderr, "a3g-step %zu samp %.1f %.1f comp %.1f %.1f\n", q / 4, v[0] * 1e3, v[1] * 1e3,
+                   v[2] * 1e3, v[3] * 1e3);
+      for (int k = 0; k < 4; ++k) cudaEventDestroy(step_ev[q + k]);
+    }
     if (tl0) {  // end time of every traced launch, relative to the first traced step's start
       for (const TlEvent& e : g_tl) {
         float ms = 0;
@@ -995,7 +1028,8 @@ a3g_status a3g_trainer_last_forward(a3g_trainer* tr, uint64_t* n_inner, double* 
 }
 
 a3g_sampler* a3g_trainer_sampler(a3g_trainer* tr, int slot) {
-  return tr->st.smp[static_cast<unsigned>(slot) % TrainerState::kArenas];
+  a3g_sampler* s = tr->st.smp[static_cast<unsigned>(slot) % TrainerState::kArenas];
+  return s ? s : tr->st.smp[0];
 }
 
 a3g_status a3g_trainer_timing(a3g_trainer* tr, double* total_ms, double* agg_ms, double* agg_bytes,

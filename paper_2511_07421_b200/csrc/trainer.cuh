@@ -8,12 +8,14 @@ namespace a3g {
 struct TrainerState {
   a3g_graph* g = nullptr;
   a3g_cache* c = nullptr;
-  // Sampler arenas of the stream pipeline: step i samples into arena i % 3 on
-  // sampling stream i % 2 -- two batches are sampled concurrently (the
-  // sampler's many small latency-bound kernels interleave) while compute
-  // consumes in order; an arena is reused only after its step's compute.
-  static constexpr int kArenas = 5;
-  static constexpr int kSampStreams = 4;
+  // Sampler arenas of the stream pipeline: with n sampling streams, step i
+  // samples into arena i % (n + 1) on stream i % n -- n batches are sampled
+  // concurrently (the sampler's many small latency-bound kernels interleave)
+  // while compute consumes in order; an arena is reused only after its step's
+  // compute. Arenas beyond the first are allocated on first use.
+  static constexpr int kArenas = 9;
+  static constexpr int kSampStreams = 8;
+  static constexpr int kDefaultStreams = 6;
   a3g_sampler* smp[kArenas] = {};
   uint32_t F = 0, H = 0, C = 0, pitch = 0, L = 0, max_seeds = 0;
   double lr = 0.2;
@@ -45,7 +47,8 @@ struct TrainerState {
   double* h_losses = nullptr;        // pinned
   cudaStream_t s_comp = nullptr, s_samp = nullptr;  // s_samp: sampling stream 0
   cudaStream_t s_sx[kSampStreams] = {};              // sampling streams (s_sx[0] == s_samp)
-  int pipe_streams = kSampStreams;  // a3g_trainer_set_pipeline: 0 = sequential (one stream), 1..kSampStreams
+  int pipe_streams = kDefaultStreams;  // a3g_trainer_set_pipeline: 0 = sequential (one stream), 1..kSampStreams
+  std::vector<uint32_t> fanouts;       // for the lazily allocated arenas
   cudaEvent_t ev_sampled[kArenas] = {}, ev_consumed[kArenas] = {};
   cudaEvent_t ev_seeds = nullptr;                     // host seeds copied (sampling streams wait on it)
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;

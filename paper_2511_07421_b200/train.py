@@ -172,7 +172,7 @@ class Trainer:
         check(lib().a3g_trainer_set_weights(self.h, ptr(a, f64p), ptr(b, f64p)))
 
     def set_pipeline(self, sampling_streams: int):
-        """0 = sequential (Mode::sequential), 1..4 concurrent sampling streams."""
+        """0 = sequential (Mode::sequential), 1..8 concurrent sampling streams."""
         check(lib().a3g_trainer_set_pipeline(self.h, int(sampling_streams)))
 
     def set_comm(self, comm):

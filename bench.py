@@ -304,7 +304,7 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (CSR %.0f MB + features %.0f MB)" % (
                        g.num_edges * 4 / 1e6, n * F * (2 if args.config in SYNTH else 4) / 1e6),
                    "graph_gen_s": round(gen_s, 1)},
-        "roofline": {"kernel": "k_agg1 (fused feature gather + mean aggregation)", "bound": "hbm",
+        "roofline": {"kernel": "k_agg1 (fused feature gather + mean aggregation + h1 = relu(agg W1) epilogue)", "bound": "hbm",
                      "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "bytes_per_launch": agg_bytes,
                      "ms_per_launch": agg_ms,

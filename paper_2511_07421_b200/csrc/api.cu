@@ -655,6 +655,7 @@ a3g_status a3g_trainer_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds, co
       t.max_seeds = max_seeds;
       t.sm_count = sm_count_of(g->device);
       t.fanouts.assign(fanouts, fanouts + L);
+      t.fuse_h1 = std::getenv("A3G_NO_FUSE_H1") == nullptr;
       t.smp[0] = new a3g_sampler;
       sampler_alloc(t.smp[0]->st, g, c, max_seeds, fanouts, L);
       t.cap_inner = std::max<uint64_t>(1, t.smp[0]->st.cap_inner);
@@ -1039,12 +1040,13 @@ a3g_status a3g_trainer_timing(a3g_trainer* tr, double* total_ms, double* agg_ms,
     if (total_ms) *total_ms = t.last_total_ms;
     if (agg_ms) *agg_ms = t.last_agg_ms;
     if (agg_bytes) *agg_bytes = t.last_agg_bytes;
-    // our kernels per step (library CUB sort kernels not counted): seeds phase
-    // 4 (init, mark, fin count/emit); per layer 6 (classify, item classes,
-    // stream, hub merge, fin count/emit); resolve; compute 8 (stats, agg,
-    // h1 GEMM, outer, dh1 gather, dW1 GEMM, reduce, sgd) + split-K reduce +
-    // the sync scale with a communicator
-      *launches_per_step = 4 + 6ull * t.L + (t.L ? 1 : 0) + 8 + (t.h1_split_used ? 1 : 0) + (t.comm ? 1 : 0);
+    // our kernels per step: seeds phase 4 (init, mark, fin count/emit); per
+    // layer 6 (classify, item classes, stream, hub merge, fin count/emit);
+    // resolve; compute 8 (stats, agg (+fused h1), outer, dh1 scatter, dh1
+    // fix, dW1 GEMM, reduce, sgd) + the h1 GEMM and its split-K reduce when
+    // not fused + the sync scale with a communicator
+      *launches_per_step = 4 + 6ull * t.L + (t.L ? 1 : 0) + 8 + (t.h1_fused ? 0 : 1) +
+                           (!t.h1_fused && t.h1_split_used ? 1 : 0) + (t.comm ? 1 : 0);
   });
 }
 

@@ -68,6 +68,8 @@ struct AggArgs {
   float* agg_inner;
   unsigned long long* bytes;
   int has_layer1;
+  const float* w1;  // [F][H] (fused h1 epilogue, HB > 0)
+  float* h1;        // [n_inner][H] relu(agg_inner . W1)
 };
 
 // Gather + mean of the layer-1 source rows of every inner row (trainer.cpp:
@@ -90,7 +92,7 @@ __device__ __forceinline__ void ldgsts_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <typename T, int NCH, int WARPS, int S, int LPR>
+template <typename T, int NCH, int WARPS, int S, int LPR, int HB>
 __global__ void __launch_bounds__(WARPS * 32, 1) k_agg1(const __grid_constant__ AggArgs a) {
   // LPR lanes per source row: short rows (<= 16 chunks) are copied RPI at a
   // time by lane groups; each group sums its own rows, the groups' partial
@@ -107,6 +109,18 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_agg1(const __grid_constant__ 
   const uint32_t n_inner = *a.n_inner;
   const uint32_t chunks = a.pitch / EPC;  // 16-byte chunks per row
   const uint32_t gw = blockIdx.x * WARPS + warp, nw = gridDim.x * WARPS;
+  // fused h1 epilogue (HB > 0): W1 zero-padded after the rings, laid out
+  // [h/4][e][q][h%4] (feature f = q EPC + e of chunk q) so that the lanes of
+  // a group, reading consecutive chunks q, hit consecutive 16-byte words
+  float* w1s = reinterpret_cast<float*>(smem + static_cast<size_t>(WARPS) * S * RPI * rb);
+  if constexpr (HB > 0) {
+    for (uint32_t i = threadIdx.x; i < chunks * EPC * HB; i += WARPS * 32) {
+      const uint32_t j = i & 3, q = (i >> 2) % chunks, e = (i >> 2) / chunks % EPC, h = (i >> 2) / chunks / EPC * 4 + j;
+      const uint32_t f = q * EPC + e;
+      w1s[i] = (f < a.F && h < a.H) ? __ldg(a.w1 + static_cast<size_t>(f) * a.H + h) : 0.f;
+    }
+    __syncthreads();
+  }
   const uint32_t nrows = gw < n_inner ? (n_inner - gw + nw - 1) / nw : 0;  // this warp's rows gw + j*nw
   unsigned long long nbytes = 0;
   // producer: row j, source t; lanes hold the (layer row, count) of rows
@@ -207,6 +221,50 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_agg1(const __grid_constant__ 
       const uint32_t c = sc & 0x7fffffffu;
       const float scale = c ? 1.f / static_cast<float>(c) : 1.f;
       float4* out = reinterpret_cast<float4*>(a.agg_inner + static_cast<uint64_t>(srow) * a.pitch);
+      if constexpr (HB > 0) {
+        // h1 = relu(agg . W1) for this row: group g owns outputs [g HG, (g+1) HG)
+        // (every group holds the full row sums); per-lane partials over the
+        // lane's chunks, then a recursive-halving reduce over the group's lanes
+        constexpr int HG = HB / RPI;
+        float p[HG];
+#pragma unroll
+        for (int h = 0; h < HG; ++h) p[h] = 0.f;
+#pragma unroll
+        for (int i = 0; i < NCH; ++i) {
+          const uint32_t q = gl + LPR * i;
+          if (q < chunks) {
+#pragma unroll
+            for (int e = 0; e < EPC; ++e) {
+              const float x = acc[i][e] * scale;
+#pragma unroll
+              for (int h4 = 0; h4 < HG / 4; ++h4) {
+                const float4 w = reinterpret_cast<const float4*>(w1s)[((g * (HG / 4) + h4) * EPC + e) * chunks + q];
+                p[4 * h4] = fmaf(x, w.x, p[4 * h4]);
+                p[4 * h4 + 1] = fmaf(x, w.y, p[4 * h4 + 1]);
+                p[4 * h4 + 2] = fmaf(x, w.z, p[4 * h4 + 2]);
+                p[4 * h4 + 3] = fmaf(x, w.w, p[4 * h4 + 3]);
+              }
+            }
+          }
+        }
+        uint32_t hidx = 0;
+        int o = LPR / 2;
+#pragma unroll
+        for (int n = HG; n > 1; n >>= 1, o >>= 1) {
+          const bool upper = (gl & static_cast<uint32_t>(o)) != 0;
+#pragma unroll
+          for (int j = 0; j < n / 2; ++j) {
+            const float send = upper ? p[j] : p[j + n / 2];
+            const float keep = upper ? p[j + n / 2] : p[j];
+            p[j] = keep + __shfl_xor_sync(kFull, send, o);
+          }
+          if (upper) hidx += n / 2;
+        }
+        for (; o > 0; o >>= 1) p[0] += __shfl_xor_sync(kFull, p[0], o);
+        const uint32_t h = g * HG + hidx;
+        if ((gl & static_cast<uint32_t>(LPR / HG - 1)) == 0 && h < a.H)
+          a.h1[static_cast<uint64_t>(srow) * a.H + h] = fmaxf(p[0], 0.f);
+      }
 #pragma unroll
       for (int i = 0; i < NCH; ++i) {
         const uint32_t q = gl + LPR * i;
@@ -219,7 +277,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_agg1(const __grid_constant__ 
 #pragma unroll
         for (int e = 0; e < EPC; ++e) acc[i][e] = 0.f;
       }
-      nbytes += static_cast<unsigned long long>(a.F) * 4;  // agg_inner row written
+      nbytes += static_cast<unsigned long long>(a.F) * 4 + (HB > 0 ? a.H * 4ull : 0ull);  // agg_inner (+h1) row
     }
   }
   // algorithmic feature bytes: every DISTINCT layer-1 source row once -- the
@@ -454,56 +512,69 @@ __global__ void k_sgd(float* w1, float* w2, float* gw, uint32_t FH, uint32_t HC,
   if (blockIdx.x == 0 && threadIdx.x == 0 && loss_slot) *loss_slot = static_cast<double>(gw[FH + HC + 1]) / n;
 }
 
-template <typename T, int N, int W, int S, int LPR>
+template <typename T, int N, int W, int S, int LPR, int HB>
 void launch_agg_cfg(TrainerState& t, const AggArgs& aa, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(W) * S * (32 / LPR) * aa.view.row_bytes;
+  const size_t ring = static_cast<size_t>(W) * S * (32 / LPR) * aa.view.row_bytes;
+  const size_t smem = ring + (HB > 0 ? static_cast<size_t>(aa.pitch) * HB * 4 : 0);
   if (smem > 227 * 1024) raise(A3G_ERR_PARAMETER, "feature row too wide for k_agg1's shared-memory ring");
   const int grid = t.sm_count * (smem * 2 <= 227 * 1024 && W <= 32 ? 2 : 1);
-  A3G_CUDA(cudaFuncSetAttribute(k_agg1<T, N, W, S, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  A3G_CUDA(cudaFuncSetAttribute(k_agg1<T, N, W, S, LPR, HB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
-  k_agg1<T, N, W, S, LPR><<<grid, W * 32, smem, st>>>(aa);
+  k_agg1<T, N, W, S, LPR, HB><<<grid, W * 32, smem, st>>>(aa);
 }
 
 // 24 warps per CTA (more warps beat a deeper ring: r01 sweep 8x8 63 us,
 // 16x4 53 us, 24x3 51 us on C2); ring depth from the row size.
-template <typename T, int N, int LPR>
+template <typename T, int N, int LPR, int HB>
 void launch_agg_n(TrainerState& t, const AggArgs& aa, cudaStream_t st) {
   const uint64_t per_slot = 24ull * (32 / LPR) * aa.view.row_bytes;
   if (per_slot * 8 <= 176 * 1024)
-    launch_agg_cfg<T, N, 24, 8, LPR>(t, aa, st);
+    launch_agg_cfg<T, N, 24, 8, LPR, HB>(t, aa, st);
   else if (per_slot * 6 <= 176 * 1024)
-    launch_agg_cfg<T, N, 24, 6, LPR>(t, aa, st);
+    launch_agg_cfg<T, N, 24, 6, LPR, HB>(t, aa, st);
   else if (per_slot * 4 <= 176 * 1024)
-    launch_agg_cfg<T, N, 24, 4, LPR>(t, aa, st);
+    launch_agg_cfg<T, N, 24, 4, LPR, HB>(t, aa, st);
   else
-    launch_agg_cfg<T, N, 24, 3, LPR>(t, aa, st);
+    launch_agg_cfg<T, N, 24, 3, LPR, HB>(t, aa, st);
 }
 
-// rows of <= 16 chunks (16 B) go 4 rows per warp step (LPR 8): short rows
-// are issue-bound, not bandwidth-bound
-template <typename T>
-void launch_agg(TrainerState& t, AggArgs aa, uint32_t chunks, cudaStream_t st) {
+template <typename T, int HB>
+void launch_agg_h(TrainerState& t, const AggArgs& aa, uint32_t chunks, cudaStream_t st) {
   if (chunks <= 8) {
-    launch_agg_n<T, 1, 8>(t, aa, st);
+    launch_agg_n<T, 1, 8, HB>(t, aa, st);
   } else if (chunks <= 16) {
-    launch_agg_n<T, 2, 8>(t, aa, st);
+    launch_agg_n<T, 2, 8, HB>(t, aa, st);
   } else {
     switch ((chunks + 31) / 32) {
-      case 1: launch_agg_n<T, 1, 32>(t, aa, st); break;
-      case 2: launch_agg_n<T, 2, 32>(t, aa, st); break;
-      case 3: launch_agg_n<T, 3, 32>(t, aa, st); break;
-      case 4: launch_agg_n<T, 4, 32>(t, aa, st); break;
-      case 5: launch_agg_n<T, 5, 32>(t, aa, st); break;
-      case 6: launch_agg_n<T, 6, 32>(t, aa, st); break;
-      case 7: case 8: launch_agg_n<T, 8, 32>(t, aa, st); break;
+      case 1: launch_agg_n<T, 1, 32, HB>(t, aa, st); break;
+      case 2: launch_agg_n<T, 2, 32, HB>(t, aa, st); break;
+      case 3: launch_agg_n<T, 3, 32, HB>(t, aa, st); break;
+      case 4: launch_agg_n<T, 4, 32, HB>(t, aa, st); break;
+      case 5: launch_agg_n<T, 5, 32, HB>(t, aa, st); break;
+      case 6: launch_agg_n<T, 6, 32, HB>(t, aa, st); break;
+      case 7: case 8: launch_agg_n<T, 8, 32, HB>(t, aa, st); break;
       case 9: case 10: case 11: case 12: case 13: case 14: case 15: case 16:
-        launch_agg_n<T, 16, 32>(t, aa, st);
+        launch_agg_n<T, 16, 32, HB>(t, aa, st);
         break;
       default:
         raise(A3G_ERR_PARAMETER, "feature row too wide for k_agg1");
     }
   }
+}
+
+// rows of <= 16 chunks (16 B) go 4 rows per warp step (LPR 8): short rows
+// are issue-bound, not bandwidth-bound. H <= 16 with W1 fitting beside the
+// ring fuses h1 = relu(agg . W1) into the epilogue (returns true); otherwise
+// the tcgen05 GEMM computes h1 afterwards.
+template <typename T>
+bool launch_agg(TrainerState& t, AggArgs aa, uint32_t chunks, cudaStream_t st) {
+  const bool fuse = t.fuse_h1 && t.H <= 16 && static_cast<size_t>(aa.pitch) * 16 * 4 <= 48 * 1024;
+  if (fuse)
+    launch_agg_h<T, 16>(t, aa, chunks, st);
+  else
+    launch_agg_h<T, 0>(t, aa, chunks, st);
   A3G_LAUNCH_DONE("k_agg1", st);
+  return fuse;
 }
 
 }  // namespace
@@ -544,16 +615,20 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
     A3G_CUDA(cudaEventCreate(&e1));
     A3G_CUDA(cudaEventRecord(e0, st));
   }
+  aa.w1 = t.d_w1;
+  aa.h1 = t.d_h1;
+  bool fused;
   if (g->feat_dtype == A3G_FEAT_BF16)
-    launch_agg<uint16_t>(t, aa, g->pitch / 8, st);
+    fused = launch_agg<uint16_t>(t, aa, g->pitch / 8, st);
   else
-    launch_agg<float>(t, aa, g->pitch / 4, st);
+    fused = launch_agg<float>(t, aa, g->pitch / 4, st);
+  t.h1_fused = fused;
   if (record_timing) {
     A3G_CUDA(cudaEventRecord(e1, st));
     t.ev_agg.push_back(e0);
     t.ev_agg.push_back(e1);
   }
-  launch_h1_tc(t, t.d_agg_inner, aa.n_inner, t.d_h1, st);
+  if (!fused) launch_h1_tc(t, t.d_agg_inner, aa.n_inner, t.d_h1, st);
   // ---- outer aggregation, logits, loss, dlogits, scatter to dh1
   OuterArgs oa{};
   oa.h1 = t.d_h1;

@@ -88,6 +88,16 @@ def test_grads_c1_vs_oracle(orc, c1, fanouts, gamma, kind, H):
     _grad_case(orc, g, cache, batches[3], fanouts, gamma, kind, T.sampling_seed(1, 0, 3, 0), H=H)
 
 
+def test_h1_unfused_tcgen05_path(orc, c1, monkeypatch):
+    """A3G_NO_FUSE_H1=1: h1 from the tcgen05 GEMM instead of k_agg1's
+    epilogue -- the same oracle tolerance (both paths are fp32-class)."""
+    monkeypatch.setenv("A3G_NO_FUSE_H1", "1")
+    g = c1
+    cache = CA.build_static_cache(g, CA.CacheConfig(int(0.2 * g.num_nodes) * g.feat_dim * 4, 1))
+    batches = T.plan_epoch_batches(g.train_nodes, 0, 1024, orc.hash2(1, 0))
+    _grad_case(orc, g, cache, batches[2], [10, 5], 8.0, 0, T.sampling_seed(1, 0, 2, 0), H=16)
+
+
 def test_intermediates_c1(orc, c1):
     g = c1
     cache = CA.build_static_cache(g, CA.CacheConfig(int(0.2 * g.num_nodes) * g.feat_dim * 4, 1))

@@ -655,7 +655,7 @@ a3g_status a3g_trainer_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds, co
       t.max_seeds = max_seeds;
       t.sm_count = sm_count_of(g->device);
       t.fanouts.assign(fanouts, fanouts + L);
-      t.fuse_h1 = std::getenv("A3G_NO_FUSE_H1") == nullptr;
+      t.tc_gemms = std::getenv("A3G_TC_GEMMS") != nullptr;
       t.smp[0] = new a3g_sampler;
       sampler_alloc(t.smp[0]->st, g, c, max_seeds, fanouts, L);
       t.cap_inner = std::max<uint64_t>(1, t.smp[0]->st.cap_inner);
@@ -679,7 +679,8 @@ a3g_status a3g_trainer_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds, co
       t.tc_splits = std::max<uint32_t>(1, static_cast<uint32_t>(t.sm_count) / ((t.F + 127) / 128));
       t.h1_split_cap = std::min<uint32_t>(8, (t.F + 63) / 64);
       t.d_hpart = dalloc<float>(static_cast<size_t>(t.h1_split_cap) * t.cap_inner * H);
-      t.d_part = dalloc<float>(static_cast<size_t>(std::max(t.nparts, t.tc_splits)) * t.F * H);
+      t.dw1_splits = static_cast<uint32_t>((t.cap_inner + 127) / 128);  // kDw1Rows
+      t.d_part = dalloc<float>(static_cast<size_t>(std::max({t.nparts, t.tc_splits, t.dw1_splits})) * t.F * H);
       t.d_agg_bytes = dalloc<unsigned long long>(1);
       A3G_CUDA(cudaMemset(t.d_agg_bytes, 0, 8));
       t.losses_cap = 1;

@@ -288,6 +288,64 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_agg1(const __grid_constant__ 
   if (lane == 0 && nbytes) atomicAdd(a.bytes, nbytes);
 }
 
+// dW1 = agg_inner^T . G, G = dh1 * [h1 > 0] (trainer.cpp:203-204), on the
+// CUDA cores: an HBM-bound skinny product (N = H <= 32) -- one pass over
+// agg_inner at full bandwidth beats staging 3-term bf16 operands for tcgen05
+// (the k_dw1_tc path, A3G_TC_GEMMS=1). Thread = one feature column, HB
+// accumulators; CTA = 128 features x kDw1Rows rows, its G rows staged in
+// shared memory; rows summed in order, splits reduced in order by k_reduce
+// (deterministic). Empty splits write zero partials.
+constexpr uint32_t kDw1Rows = 128;
+
+template <int HB>
+__global__ void __launch_bounds__(128) k_dw1_fma(const float* __restrict__ agg, uint32_t pitch, uint32_t F, uint32_t H,
+                                                 const uint32_t* n_inner, const float* __restrict__ h1,
+                                                 const float* __restrict__ dh1, float* part) {
+  __shared__ __align__(16) float sg[kDw1Rows * HB];
+  const uint32_t n = *n_inner;
+  const uint32_t r0 = blockIdx.y * kDw1Rows;
+  const uint32_t nr = r0 < n ? min(kDw1Rows, n - r0) : 0u;
+  for (uint32_t i = threadIdx.x; i < kDw1Rows * HB; i += blockDim.x) {
+    const uint32_t r = i / HB, h = i % HB;
+    float gv = 0.f;
+    if (r < nr && h < H) {
+      const uint64_t k = static_cast<uint64_t>(r0 + r) * H + h;
+      gv = __ldg(h1 + k) > 0.f ? __ldg(dh1 + k) : 0.f;
+    }
+    sg[i] = gv;
+  }
+  __syncthreads();
+  const uint32_t f = blockIdx.x * 128 + threadIdx.x;
+  float acc[HB];
+#pragma unroll
+  for (int h = 0; h < HB; ++h) acc[h] = 0.f;
+  if (f < F) {
+    const float* col = agg + static_cast<uint64_t>(r0) * pitch + f;
+    constexpr int U = 8;
+    for (uint32_t r = 0; r < nr; r += U) {
+      float x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) x[u] = r + u < nr ? __ldg(col + static_cast<uint64_t>(r + u) * pitch) : 0.f;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float4* gr = reinterpret_cast<const float4*>(sg + (r + u) * HB);
+#pragma unroll
+        for (int h4 = 0; h4 < HB / 4; ++h4) {
+          const float4 gv = gr[h4];
+          acc[4 * h4] = fmaf(x[u], gv.x, acc[4 * h4]);
+          acc[4 * h4 + 1] = fmaf(x[u], gv.y, acc[4 * h4 + 1]);
+          acc[4 * h4 + 2] = fmaf(x[u], gv.z, acc[4 * h4 + 2]);
+          acc[4 * h4 + 3] = fmaf(x[u], gv.w, acc[4 * h4 + 3]);
+        }
+      }
+    }
+    float* out = part + static_cast<uint64_t>(blockIdx.y) * F * H + static_cast<uint64_t>(f) * H;
+#pragma unroll
+    for (int h = 0; h < HB; ++h)
+      if (static_cast<uint32_t>(h) < H) out[h] = acc[h];
+  }
+}
+
 // Per-step statistics (a3g_trainer_step_stats): batch sizes from the sampler's
 // counters and the cache hit/miss count over unique_nodes (lookup,
 // cache.cpp:48-68: any-device presence is a hit).
@@ -456,10 +514,20 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a, uint32_t nb1) {
   const uint32_t FH = a.F * a.H, HC = a.H * a.C;
   const uint32_t ns = *a.ns;
   if (blockIdx.x < nb1) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < FH; i += nb1 * blockDim.x) {
-      float s = 0.f;
-      for (uint32_t p = 0; p < a.nparts; ++p) s += a.part[static_cast<uint64_t>(p) * FH + i];
-      a.gw[i] = s;
+    // 32 consecutive entries per block, the partials strided over 8 thread
+    // rows (coalesced), then the 8 row sums in order: a fixed-shape tree
+    const uint32_t j = threadIdx.x & 31, k = threadIdx.x >> 5;
+    const uint32_t i = blockIdx.x * 32 + j;
+    float x = 0.f;
+    if (i < FH)
+      for (uint32_t p = k; p < a.nparts; p += 8) x += a.part[static_cast<uint64_t>(p) * FH + i];
+    s_l[threadIdx.x] = x;
+    __syncthreads();
+    if (k == 0 && i < FH) {
+      float t = s_l[j];
+#pragma unroll
+      for (int r = 1; r < 8; ++r) t += s_l[j + 32 * r];
+      a.gw[i] = t;
     }
     return;
   }
@@ -568,7 +636,7 @@ void launch_agg_h(TrainerState& t, const AggArgs& aa, uint32_t chunks, cudaStrea
 // the tcgen05 GEMM computes h1 afterwards.
 template <typename T>
 bool launch_agg(TrainerState& t, AggArgs aa, uint32_t chunks, cudaStream_t st) {
-  const bool fuse = t.fuse_h1 && t.H <= 16 && static_cast<size_t>(aa.pitch) * 16 * 4 <= 48 * 1024;
+  const bool fuse = !t.tc_gemms && t.H <= 16 && static_cast<size_t>(aa.pitch) * 16 * 4 <= 48 * 1024;
   if (fuse)
     launch_agg_h<T, 16>(t, aa, chunks, st);
   else
@@ -657,9 +725,20 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
   A3G_LAUNCH_DONE("k_dh1_scatter", st);
   k_dh1_fix<<<t.sm_count * 2, 256, 0, st>>>(t.d_dh1_fx, t.d_amax, oa.ns, aa.n_inner, t.H, t.d_dh1);
   A3G_LAUNCH_DONE("k_dh1_fix", st);
-  // ---- dW1 = agg_inner^T . (dh1 * [h1 > 0]) on tcgen05, partials per row split
-  const uint32_t nparts = t.tc_splits;
-  launch_dw1_tc(t, t.d_agg_inner, aa.n_inner, t.d_h1, t.d_dh1, t.d_part, nparts, st);
+  // ---- dW1 = agg_inner^T . (dh1 * [h1 > 0]), partials per row split
+  uint32_t nparts;
+  if (t.tc_gemms || t.H > 32) {
+    nparts = t.tc_splits;
+    launch_dw1_tc(t, t.d_agg_inner, aa.n_inner, t.d_h1, t.d_dh1, t.d_part, nparts, st);
+  } else {
+    nparts = t.dw1_splits;
+    const dim3 grid((t.F + 127) / 128, nparts);
+    if (t.H <= 16)
+      k_dw1_fma<16><<<grid, 128, 0, st>>>(t.d_agg_inner, t.pitch, t.F, t.H, aa.n_inner, t.d_h1, t.d_dh1, t.d_part);
+    else
+      k_dw1_fma<32><<<grid, 128, 0, st>>>(t.d_agg_inner, t.pitch, t.F, t.H, aa.n_inner, t.d_h1, t.d_dh1, t.d_part);
+    A3G_LAUNCH_DONE("k_dw1_fma", st);
+  }
   // ---- reduce -> grads, loss
   ReduceArgs ra{};
   ra.part = t.d_part;
@@ -673,7 +752,7 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
   ra.C = t.C;
   ra.gw = t.d_gw;
   const uint32_t FH = t.F * t.H, HC = t.H * t.C;
-  const uint32_t nb1 = std::min<uint32_t>(t.sm_count, (FH + 255) / 256);
+  const uint32_t nb1 = (FH + 31) / 32;
   k_reduce<<<nb1 + HC + 1, 256, 0, st>>>(ra, nb1);
   A3G_LAUNCH_DONE("k_reduce", st);
   const bool synced = t.comm != nullptr;

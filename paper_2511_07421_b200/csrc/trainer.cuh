@@ -49,7 +49,9 @@ struct TrainerState {
   cudaStream_t s_sx[kSampStreams] = {};              // sampling streams (s_sx[0] == s_samp)
   int pipe_streams = kDefaultStreams;  // a3g_trainer_set_pipeline: 0 = sequential (one stream), 1..kSampStreams
   std::vector<uint32_t> fanouts;       // for the lazily allocated arenas
-  bool fuse_h1 = true;                 // h1 in k_agg1's epilogue (A3G_NO_FUSE_H1=1: tcgen05 GEMM)
+  bool tc_gemms = false;               // A3G_TC_GEMMS=1: h1 and dW1 on tcgen05 (default: h1 fused
+                                       // into k_agg1, dW1 on the CUDA cores, both HBM-bound)
+  uint32_t dw1_splits = 1;             // row splits of k_dw1_fma (kDw1Rows rows each)
   bool h1_fused = false;               // last step used the fused epilogue
   cudaEvent_t ev_sampled[kArenas] = {}, ev_consumed[kArenas] = {};
   cudaEvent_t ev_seeds = nullptr;                     // host seeds copied (sampling streams wait on it)

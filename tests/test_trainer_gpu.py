@@ -88,10 +88,11 @@ def test_grads_c1_vs_oracle(orc, c1, fanouts, gamma, kind, H):
     _grad_case(orc, g, cache, batches[3], fanouts, gamma, kind, T.sampling_seed(1, 0, 3, 0), H=H)
 
 
-def test_h1_unfused_tcgen05_path(orc, c1, monkeypatch):
-    """A3G_NO_FUSE_H1=1: h1 from the tcgen05 GEMM instead of k_agg1's
-    epilogue -- the same oracle tolerance (both paths are fp32-class)."""
-    monkeypatch.setenv("A3G_NO_FUSE_H1", "1")
+def test_tcgen05_gemm_path(orc, c1, monkeypatch):
+    """A3G_TC_GEMMS=1: h1 and dW1 from the tcgen05 GEMMs instead of k_agg1's
+    epilogue and the CUDA-core dW1 -- the same oracle tolerance (both paths
+    are fp32-class)."""
+    monkeypatch.setenv("A3G_TC_GEMMS", "1")
     g = c1
     cache = CA.build_static_cache(g, CA.CacheConfig(int(0.2 * g.num_nodes) * g.feat_dim * 4, 1))
     batches = T.plan_epoch_batches(g.train_nodes, 0, 1024, orc.hash2(1, 0))

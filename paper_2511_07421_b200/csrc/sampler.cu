@@ -32,6 +32,7 @@
 //   k_fin_count / k_fin_emit: first-seen dedup + relabel (tagged atomicMax of
 //                   the first position, tile partials, ballot scans).
 // Counts stay on the device: no host sync inside a batch.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -634,11 +635,10 @@ __global__ void __launch_bounds__(256) k_stream_lane(SampleArgs a, const uint32_
   const uint32_t nitems = min(*a.item_count, a.hub.item_cap);
   const uint32_t m = a.f;
   const P pol = PolOf<WM>::make(a);
-  for (;;) {
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(a.item_work, 32u);
-    base = __shfl_sync(kFull, base, 0);
-    if (base >= nitems) break;
+  // grid sized to the layer's item bound: one batch of 32 items per warp
+  // (short-lived CTAs let the high-priority compute stream's kernels in)
+  const uint32_t wstride = gridDim.x * (blockDim.x >> 5) * 32;
+  for (uint32_t base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < nitems; base += wstride) {
     const uint32_t ii = base + lane;
     const bool live = ii < nitems;
     uint4 im = make_uint4(0, 0, 0, kInv);
@@ -754,11 +754,10 @@ __global__ void __launch_bounds__(256) k_stream_lane_mixed(SampleArgs a, const u
   const double ig = a.inv_gamma, gamma = a.gamma;
   const uint32_t* eb = a.ebits;
   const rsv::PolUnit ipol{};
-  for (;;) {
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(a.item_work, 32u);
-    base = __shfl_sync(kFull, base, 0);
-    if (base >= nitems) break;
+  // grid sized to the layer's item bound: one batch of 32 items per warp
+  // (short-lived CTAs let the high-priority compute stream's kernels in)
+  const uint32_t wstride = gridDim.x * (blockDim.x >> 5) * 32;
+  for (uint32_t base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < nitems; base += wstride) {
     const uint32_t ii = base + lane;
     const bool live = ii < nitems;
     uint4 im = make_uint4(0, 0, 0, kInv);
@@ -1878,11 +1877,13 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
       const uint32_t* lists = hb.sort_keys[0];
       constexpr int W = WM == 2 ? 0 : WM;
       const int grid = sm_count * 8;
+      const int lane_grid = static_cast<int>(
+          std::max<uint64_t>(1, (std::min<uint64_t>(rows_bound + sa.hub.seg_cap, sa.hub.item_cap) + 255) / 256));
       if (WM == 2 && sa.kind != A3G_SAMPLER_UNIFORM && sa.ebits && sa.f <= 16 && rows_bound >= lane_min_rows()) {
         if (sa.f <= 8)
-          k_stream_lane_mixed<8><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
+          k_stream_lane_mixed<8><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         else
-          k_stream_lane_mixed<16><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
+          k_stream_lane_mixed<16><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         A3G_LAUNCH_DONE("k_stream_lane_mixed", st);
       } else if (WM == 2 && sa.kind != A3G_SAMPLER_UNIFORM) {
         if (sa.f <= 8)
@@ -1894,9 +1895,9 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
         A3G_LAUNCH_DONE("k_stream_grp_mixed", st);
       } else if (sa.kind != A3G_SAMPLER_UNIFORM && sa.f <= 16 && rows_bound >= lane_min_rows()) {
         if (sa.f <= 8)
-          k_stream_lane<W, 8><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
+          k_stream_lane<W, 8><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         else
-          k_stream_lane<W, 16><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
+          k_stream_lane<W, 16><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         A3G_LAUNCH_DONE("k_stream_lane", st);
       } else {
         if (sa.f <= 8)

@@ -434,11 +434,8 @@ __global__ void __launch_bounds__(256) k_stream_grp(SampleArgs a, const uint32_t
   const uint32_t nitems = min(*a.item_count, a.hub.item_cap);
   const uint32_t m = a.f;
   const P pol = PolOf<WM>::make(a);
-  for (;;) {
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(a.item_work, static_cast<uint32_t>(NG));
-    base = __shfl_sync(kFull, base, 0);
-    if (base >= nitems) break;
+  const uint32_t wstride = gridDim.x * (blockDim.x >> 5) * NG;
+  for (uint32_t base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NG; base < nitems; base += wstride) {
     const uint32_t ii = base + grp;
     const bool live = ii < nitems;
     uint4 im = make_uint4(0, 0, 0, kInv);
@@ -919,11 +916,8 @@ __global__ void __launch_bounds__(256) k_stream_grp_mixed(SampleArgs a, const ui
   const uint32_t* bits = a.bits;
   auto cached = [&](uint32_t v) { return (__ldg(bits + (v >> 5)) >> (v & 31)) & 1u; };
   const rsv::PolUnit ipol{};  // bit-pattern argmin (keys >= 0)
-  for (;;) {
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(a.item_work, static_cast<uint32_t>(NG));
-    base = __shfl_sync(kFull, base, 0);
-    if (base >= nitems) break;
+  const uint32_t wstride = gridDim.x * (blockDim.x >> 5) * NG;
+  for (uint32_t base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NG; base < nitems; base += wstride) {
     const uint32_t ii = base + grp;
     const bool live = ii < nitems;
     uint4 im = make_uint4(0, 0, 0, kInv);
@@ -1846,6 +1840,8 @@ __global__ void k_gather_unique(const __grid_constant__ StoreView view, uint32_t
   }
 }
 
+constexpr int kGrpThreads = 256;  // CTA size of the lane-group stream kernels (64 measured slower)
+
 // frontier bound from which a layer's items go lane-per-item (A3G_LANE_MIN_ROWS
 // overrides it for tuning sweeps)
 static uint64_t lane_min_rows() {
@@ -1876,9 +1872,13 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
       A3G_LAUNCH_DONE("k_item_class", st);
       const uint32_t* lists = hb.sort_keys[0];
       constexpr int W = WM == 2 ? 0 : WM;
-      const int grid = sm_count * 8;
-      const int lane_grid = static_cast<int>(
-          std::max<uint64_t>(1, (std::min<uint64_t>(rows_bound + sa.hub.seg_cap, sa.hub.item_cap) + 255) / 256));
+      const uint64_t item_bound = std::min<uint64_t>(rows_bound + sa.hub.seg_cap, sa.hub.item_cap);
+      // lane-group kernels: one pass of 32/G items per warp, grid over the
+      // item bound (short-lived CTAs, as the lane kernels)
+      auto grp_grid = [&](int G) {
+        return static_cast<int>(std::max<uint64_t>(1, (item_bound * G + 32 * kGrpThreads - 1) / (32 * kGrpThreads)));
+      };
+      const int lane_grid = static_cast<int>(std::max<uint64_t>(1, (item_bound + 255) / 256));
       if (WM == 2 && sa.kind != A3G_SAMPLER_UNIFORM && sa.ebits && sa.f <= 16 && rows_bound >= lane_min_rows()) {
         if (sa.f <= 8)
           k_stream_lane_mixed<8><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
@@ -1887,11 +1887,11 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
         A3G_LAUNCH_DONE("k_stream_lane_mixed", st);
       } else if (WM == 2 && sa.kind != A3G_SAMPLER_UNIFORM) {
         if (sa.f <= 8)
-          k_stream_grp_mixed<8><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
+          k_stream_grp_mixed<8><<<grp_grid(8), kGrpThreads, 0, st>>>(sa, lists, sa.cls_count);
         else if (sa.f <= 16)
-          k_stream_grp_mixed<16><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
+          k_stream_grp_mixed<16><<<grp_grid(16), kGrpThreads, 0, st>>>(sa, lists, sa.cls_count);
         else
-          k_stream_grp_mixed<32><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
+          k_stream_grp_mixed<32><<<grp_grid(32), kGrpThreads, 0, st>>>(sa, lists, sa.cls_count);
         A3G_LAUNCH_DONE("k_stream_grp_mixed", st);
       } else if (sa.kind != A3G_SAMPLER_UNIFORM && sa.f <= 16 && rows_bound >= lane_min_rows()) {
         if (sa.f <= 8)
@@ -1901,11 +1901,11 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
         A3G_LAUNCH_DONE("k_stream_lane", st);
       } else {
         if (sa.f <= 8)
-          k_stream_grp<W, 8><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
+          k_stream_grp<W, 8><<<grp_grid(8), kGrpThreads, 0, st>>>(sa, lists, sa.cls_count);
         else if (sa.f <= 16)
-          k_stream_grp<W, 16><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
+          k_stream_grp<W, 16><<<grp_grid(16), kGrpThreads, 0, st>>>(sa, lists, sa.cls_count);
         else
-          k_stream_grp<W, 32><<<grid, 256, 0, st>>>(sa, lists, sa.cls_count);
+          k_stream_grp<W, 32><<<grp_grid(32), kGrpThreads, 0, st>>>(sa, lists, sa.cls_count);
         A3G_LAUNCH_DONE("k_stream_grp", st);
       }
     }

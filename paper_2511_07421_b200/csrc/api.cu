@@ -2,6 +2,7 @@
 // reference-order validation, status <-> exception mapping, host<->device
 // staging. Kernels live in sampler.cu / train.cu.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -881,6 +882,7 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
     // A3G_STEP_TIMES=1: per step, sampling start / end and compute start / end (us)
     static const bool steps_env = std::getenv("A3G_STEP_TIMES") != nullptr;
     std::vector<cudaEvent_t> step_ev;
+    const auto host_t0 = std::chrono::steady_clock::now();
     cudaEvent_t tl0 = nullptr;
     const int nss = t.pipe_streams;  // 0: sequential -- sampling on the compute stream, depth 1
     const int narenas = nss == 0 ? 1 : nss + 1;
@@ -923,6 +925,9 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
       }
     }
     g_tl_on = false;
+    if (steps_env)
+      std::fprintf(stderr, "a3g-enqueue %u steps %.1f us\n", K,
+                   std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - host_t0).count());
     A3G_CUDA(cudaMemcpyAsync(t.h_losses, t.d_losses, K * 8ull, cudaMemcpyDeviceToHost, t.s_comp));
     A3G_CUDA(cudaEventRecord(t.ev_t1, t.s_comp));
     A3G_CUDA(cudaStreamSynchronize(t.s_comp));

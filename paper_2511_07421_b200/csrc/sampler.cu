@@ -1909,7 +1909,11 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
         A3G_LAUNCH_DONE("k_stream_grp", st);
       }
     }
-    k_hub_merge<WM><<<sm_count * 2, kMergeThreads, kMergeSmem, st>>>(sa);
+    static const int merge_ctas_q = [] {  // hub-merge CTAs per 4 SMs (A3G_MERGE_CTAS4 sweeps)
+      const char* e = std::getenv("A3G_MERGE_CTAS4");
+      return e ? std::max(1, std::atoi(e)) : 2;  // r01 sweep: 2 (74 CTAs) beat 8 and 4 in the pipeline
+    }();
+    k_hub_merge<WM><<<std::max(1, sm_count * merge_ctas_q / 4), kMergeThreads, kMergeSmem, st>>>(sa);
     A3G_LAUNCH_DONE("k_hub_merge", st);
   }
 }

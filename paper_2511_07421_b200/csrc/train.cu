@@ -291,54 +291,91 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_agg1(const __grid_constant__ 
 // dW1 = agg_inner^T . G, G = dh1 * [h1 > 0] (trainer.cpp:203-204), on the
 // CUDA cores: an HBM-bound skinny product (N = H <= 32) -- one pass over
 // agg_inner at full bandwidth beats staging 3-term bf16 operands for tcgen05
-// (the k_dw1_tc path, A3G_TC_GEMMS=1). Thread = one feature column, HB
-// accumulators; CTA = 128 features x kDw1Rows rows, its G rows staged in
-// shared memory; rows summed in order, splits reduced in order by k_reduce
-// (deterministic). Empty splits write zero partials.
+// (the k_dw1_tc path, A3G_TC_GEMMS=1). CTA = 128 features x kDw1Rows rows:
+// the agg tile streams through a cp.async ring of kDw1Stages x kDw1Stage rows
+// (no registers held by loads in flight), thread = one feature column with
+// HB accumulators, the CTA's G rows staged once in shared memory. Rows are
+// summed in order and the splits reduced in order by k_reduce
+// (deterministic); empty splits write zero partials.
 constexpr uint32_t kDw1Rows = 128;
+constexpr uint32_t kDw1Stage = 16;
+constexpr uint32_t kDw1Stages = 4;
+
+size_t dw1_smem(int HB) { return (kDw1Stages * kDw1Stage * 128 + kDw1Rows * HB) * sizeof(float); }
 
 template <int HB>
 __global__ void __launch_bounds__(128) k_dw1_fma(const float* __restrict__ agg, uint32_t pitch, uint32_t F, uint32_t H,
                                                  const uint32_t* n_inner, const float* __restrict__ h1,
                                                  const float* __restrict__ dh1, float* part) {
-  __shared__ __align__(16) float sg[kDw1Rows * HB];
+  extern __shared__ __align__(16) float dsm[];
+  float* ring = dsm;                                     // [stages][kDw1Stage][128]
+  float* sg = dsm + kDw1Stages * kDw1Stage * 128;        // [kDw1Rows][HB]
   const uint32_t n = *n_inner;
   const uint32_t r0 = blockIdx.y * kDw1Rows;
   const uint32_t nr = r0 < n ? min(kDw1Rows, n - r0) : 0u;
-  for (uint32_t i = threadIdx.x; i < kDw1Rows * HB; i += blockDim.x) {
-    const uint32_t r = i / HB, h = i % HB;
-    float gv = 0.f;
-    if (r < nr && h < H) {
-      const uint64_t k = static_cast<uint64_t>(r0 + r) * H + h;
-      gv = __ldg(h1 + k) > 0.f ? __ldg(dh1 + k) : 0.f;
+  const uint32_t f0 = blockIdx.x * 128;
+  const uint32_t nst = (nr + kDw1Stage - 1) / kDw1Stage;
+  // stage s: rows [s kDw1Stage, +kDw1Stage) x 32 chunks of 16 B, 4 per thread
+  auto issue = [&](uint32_t st) {
+    if (st < nst) {
+      const uint32_t base = ptx::smem_u32(ring + (st % kDw1Stages) * kDw1Stage * 128);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t idx = threadIdx.x + 128 * k, rr = idx >> 5, c = idx & 31;
+        const uint32_t r = st * kDw1Stage + rr;
+        if (r < nr && f0 + 4 * c < pitch)
+          ldgsts16(base + (rr * 128 + 4 * c) * 4, agg + static_cast<uint64_t>(r0 + r) * pitch + f0 + 4 * c);
+      }
     }
-    sg[i] = gv;
+    ldgsts_commit();
+  };
+#pragma unroll
+  for (uint32_t st = 0; st < kDw1Stages - 1; ++st) issue(st);
+  {
+    // G tile: every load issued before any is used (a serial loop here would
+    // pay one memory latency per element)
+    constexpr int PER = kDw1Rows * HB / 128;
+    float gh[PER], gd[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const uint32_t i = threadIdx.x + 128 * k, r = i / HB, h = i % HB;
+      gh[k] = 0.f;
+      gd[k] = 0.f;
+      if (r < nr && h < H) {
+        const uint64_t q = static_cast<uint64_t>(r0 + r) * H + h;
+        gh[k] = __ldg(h1 + q);
+        gd[k] = __ldg(dh1 + q);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k) sg[threadIdx.x + 128 * k] = gh[k] > 0.f ? gd[k] : 0.f;
   }
-  __syncthreads();
-  const uint32_t f = blockIdx.x * 128 + threadIdx.x;
   float acc[HB];
 #pragma unroll
   for (int h = 0; h < HB; ++h) acc[h] = 0.f;
-  if (f < F) {
-    const float* col = agg + static_cast<uint64_t>(r0) * pitch + f;
-    constexpr int U = 8;
-    for (uint32_t r = 0; r < nr; r += U) {
-      float x[U];
+  for (uint32_t st = 0; st < nst; ++st) {
+    ldgsts_wait<kDw1Stages - 2>();
+    __syncthreads();
+    const float* tile = ring + (st % kDw1Stages) * kDw1Stage * 128;
+    const uint32_t rows = min(kDw1Stage, nr - st * kDw1Stage);
+#pragma unroll 4
+    for (uint32_t rr = 0; rr < rows; ++rr) {
+      const float x = tile[rr * 128 + threadIdx.x];
+      const float4* gr = reinterpret_cast<const float4*>(sg + (st * kDw1Stage + rr) * HB);
 #pragma unroll
-      for (int u = 0; u < U; ++u) x[u] = r + u < nr ? __ldg(col + static_cast<uint64_t>(r + u) * pitch) : 0.f;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const float4* gr = reinterpret_cast<const float4*>(sg + (r + u) * HB);
-#pragma unroll
-        for (int h4 = 0; h4 < HB / 4; ++h4) {
-          const float4 gv = gr[h4];
-          acc[4 * h4] = fmaf(x[u], gv.x, acc[4 * h4]);
-          acc[4 * h4 + 1] = fmaf(x[u], gv.y, acc[4 * h4 + 1]);
-          acc[4 * h4 + 2] = fmaf(x[u], gv.z, acc[4 * h4 + 2]);
-          acc[4 * h4 + 3] = fmaf(x[u], gv.w, acc[4 * h4 + 3]);
-        }
+      for (int h4 = 0; h4 < HB / 4; ++h4) {
+        const float4 gv = gr[h4];
+        acc[4 * h4] = fmaf(x, gv.x, acc[4 * h4]);
+        acc[4 * h4 + 1] = fmaf(x, gv.y, acc[4 * h4 + 1]);
+        acc[4 * h4 + 2] = fmaf(x, gv.z, acc[4 * h4 + 2]);
+        acc[4 * h4 + 3] = fmaf(x, gv.w, acc[4 * h4 + 3]);
       }
     }
+    __syncthreads();  // the slot is refilled next
+    issue(st + kDw1Stages - 1);
+  }
+  const uint32_t f = f0 + threadIdx.x;
+  if (f < F) {
     float* out = part + static_cast<uint64_t>(blockIdx.y) * F * H + static_cast<uint64_t>(f) * H;
 #pragma unroll
     for (int h = 0; h < HB; ++h)
@@ -593,8 +630,26 @@ void launch_agg_cfg(TrainerState& t, const AggArgs& aa, cudaStream_t st) {
 
 // 24 warps per CTA (more warps beat a deeper ring: r01 sweep 8x8 63 us,
 // 16x4 53 us, 24x3 51 us on C2); ring depth from the row size.
+static int agg_warps() {
+  static const int v = [] {
+    const char* e = std::getenv("A3G_AGG_WARPS");
+    return e && std::atoi(e) == 16 ? 16 : 24;
+  }();
+  return v;
+}
+
 template <typename T, int N, int LPR, int HB>
 void launch_agg_n(TrainerState& t, const AggArgs& aa, cudaStream_t st) {
+  if (agg_warps() == 16) {  // smaller CTA footprint (co-residence with sampling CTAs)
+    const uint64_t ps = 16ull * (32 / LPR) * aa.view.row_bytes;
+    if (ps * 6 <= 120 * 1024)
+      launch_agg_cfg<T, N, 16, 6, LPR, HB>(t, aa, st);
+    else if (ps * 4 <= 120 * 1024)
+      launch_agg_cfg<T, N, 16, 4, LPR, HB>(t, aa, st);
+    else
+      launch_agg_cfg<T, N, 16, 3, LPR, HB>(t, aa, st);
+    return;
+  }
   const uint64_t per_slot = 24ull * (32 / LPR) * aa.view.row_bytes;
   if (per_slot * 8 <= 176 * 1024)
     launch_agg_cfg<T, N, 24, 8, LPR, HB>(t, aa, st);
@@ -733,10 +788,25 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
   } else {
     nparts = t.dw1_splits;
     const dim3 grid((t.F + 127) / 128, nparts);
-    if (t.H <= 16)
-      k_dw1_fma<16><<<grid, 128, 0, st>>>(t.d_agg_inner, t.pitch, t.F, t.H, aa.n_inner, t.d_h1, t.d_dh1, t.d_part);
-    else
-      k_dw1_fma<32><<<grid, 128, 0, st>>>(t.d_agg_inner, t.pitch, t.F, t.H, aa.n_inner, t.d_h1, t.d_dh1, t.d_part);
+    if (t.H <= 16) {
+      static bool attr16 = false;
+      if (!attr16) {
+        A3G_CUDA(cudaFuncSetAttribute(k_dw1_fma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(dw1_smem(16))));
+        attr16 = true;
+      }
+      k_dw1_fma<16><<<grid, 128, dw1_smem(16), st>>>(t.d_agg_inner, t.pitch, t.F, t.H, aa.n_inner, t.d_h1, t.d_dh1,
+                                                      t.d_part);
+    } else {
+      static bool attr32 = false;
+      if (!attr32) {
+        A3G_CUDA(cudaFuncSetAttribute(k_dw1_fma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(dw1_smem(32))));
+        attr32 = true;
+      }
+      k_dw1_fma<32><<<grid, 128, dw1_smem(32), st>>>(t.d_agg_inner, t.pitch, t.F, t.H, aa.n_inner, t.d_h1, t.d_dh1,
+                                                      t.d_part);
+    }
     A3G_LAUNCH_DONE("k_dw1_fma", st);
   }
   // ---- reduce -> grads, loss

@@ -1876,7 +1876,8 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
       // lane-group kernels: one pass of 32/G items per warp, grid over the
       // item bound (short-lived CTAs, as the lane kernels)
       auto grp_grid = [&](int G) {
-        return static_cast<int>(std::max<uint64_t>(1, (item_bound * G + 32 * kGrpThreads - 1) / (32 * kGrpThreads)));
+        // a CTA covers (kGrpThreads / 32) warps x (32 / G) items
+        return static_cast<int>(std::max<uint64_t>(1, (item_bound * G + kGrpThreads - 1) / kGrpThreads));
       };
       const int lane_grid = static_cast<int>(std::max<uint64_t>(1, (item_bound + 255) / 256));
       if (WM == 2 && sa.kind != A3G_SAMPLER_UNIFORM && sa.ebits && sa.f <= 16 && rows_bound >= lane_min_rows()) {

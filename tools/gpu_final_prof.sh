@@ -13,3 +13,13 @@ for spec in "k_agg1:3" "k_stream_lane:2" "k_stream_grp:4" "k_dw1_fma:3" "k_hub_m
 done
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stream_lane_mixed -s 2 -c 1 -o gpurun_out/final/prof_k_stream_lane_mixed python bench.py --config c3 --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 ls -la gpurun_out/final
+# summaries on the box; keep only two full reports (gpurun_out/ must stay < 64 MiB)
+for f in gpurun_out/final/prof_*.ncu-rep; do
+  python tools/ncu_summary.py $f > ${f%.ncu-rep}.txt 2>/dev/null
+done
+python tools/kernel_table.py gpurun_out/final/launches_c2.csv > gpurun_out/final/launches_c2.txt 2>/dev/null
+python tools/kernel_table.py gpurun_out/final/launches_c3.csv > gpurun_out/final/launches_c3.txt 2>/dev/null
+python tools/ncu_lines.py gpurun_out/final/prof_k_stream_lane.ncu-rep k_stream_lane 40 > gpurun_out/final/lines_k_stream_lane.txt 2>/dev/null
+python tools/ncu_lines.py gpurun_out/final/prof_k_agg1.ncu-rep k_agg1 40 > gpurun_out/final/lines_k_agg1.txt 2>/dev/null
+for k in k_dw1_fma k_hub_merge k_stream_grp k_stream_lane_mixed; do rm -f gpurun_out/final/prof_$k.ncu-rep; done
+du -sh gpurun_out

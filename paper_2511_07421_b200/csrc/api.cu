@@ -910,14 +910,14 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
       }
       sample_impl(smp->st, dseeds + off[i], static_cast<uint32_t>(off[i + 1] - off[i]), true, gamma, kind,
                   rng_seeds[i], ss);
+      launch_step_stats(t, smp, t.d_stats + static_cast<size_t>(i) * A3G_STEP_STATS, ss);
       A3G_CUDA(cudaEventRecord(t.ev_sampled[ar], ss));
       A3G_CUDA(cudaStreamWaitEvent(t.s_comp, t.ev_sampled[ar], 0));
       if (steps_env) {
         A3G_CUDA(cudaEventRecord(se[1], ss));
         A3G_CUDA(cudaEventRecord(se[2], t.s_comp));
       }
-      launch_train_compute(t, smp, t.lr, t.d_losses + i, t.d_stats + static_cast<size_t>(i) * A3G_STEP_STATS,
-                           t.s_comp, t.timing);
+      launch_train_compute(t, smp, t.lr, t.d_losses + i, nullptr, t.s_comp, t.timing);
       A3G_CUDA(cudaEventRecord(t.ev_consumed[ar], t.s_comp));
       if (steps_env) {
         A3G_CUDA(cudaEventRecord(se[3], t.s_comp));
@@ -1048,11 +1048,12 @@ a3g_status a3g_trainer_timing(a3g_trainer* tr, double* total_ms, double* agg_ms,
     if (agg_bytes) *agg_bytes = t.last_agg_bytes;
     // our kernels per step: seeds phase 4 (init, mark, fin count/emit); per
     // layer 6 (classify, item classes, stream, hub merge, fin count/emit);
-    // resolve; compute 8 (stats, agg (+fused h1), outer, dh1 scatter, dh1
-    // fix, dW1 GEMM, reduce, sgd) + the h1 GEMM and its split-K reduce when
-    // not fused + the sync scale with a communicator
-      *launches_per_step = 4 + 6ull * t.L + (t.L ? 1 : 0) + 8 + (t.h1_fused ? 0 : 1) +
-                           (!t.h1_fused && t.h1_split_used ? 1 : 0) + (t.comm ? 1 : 0);
+    // resolve; stats (sampling stream); compute 6 (agg (+fused h1), outer,
+    // dh1 scatter, dh1 fix, dW1, reduce (+SGD with one worker)) + the h1 GEMM
+    // and its split-K reduce when not fused + scale and SGD with a communicator
+    if (launches_per_step)
+      *launches_per_step = 4 + 6ull * t.L + (t.L ? 1 : 0) + 1 + 6 + (t.h1_fused ? 0 : 1) +
+                           (!t.h1_fused && t.h1_split_used ? 1 : 0) + (t.comm ? 2 : 0);
   });
 }
 

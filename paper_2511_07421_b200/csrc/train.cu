@@ -541,6 +541,12 @@ struct ReduceArgs {
   const uint32_t* ns;
   uint32_t F, H, C;
   float* gw;  // [F*H | H*C | n | loss_mean*n]
+  // fused SGD (single worker: no gradient exchange between reduce and step)
+  float* w1;
+  float* w2;
+  float lr;
+  double* loss_slot;
+  int sgd;
 };
 
 // blocks [0, nb1): dW1 = sum of the row-split partials (fixed order);
@@ -565,6 +571,7 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a, uint32_t nb1) {
 #pragma unroll
       for (int r = 1; r < 8; ++r) t += s_l[j + 32 * r];
       a.gw[i] = t;
+      if (a.sgd) a.w1[i] -= a.lr * t;
     }
     return;
   }
@@ -586,9 +593,11 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a, uint32_t nb1) {
   if (threadIdx.x == 0) {
     if (q < HC) {
       a.gw[FH + q] = s_l[0];
+      if (a.sgd) a.w2[q] -= a.lr * s_l[0];
     } else {
       a.gw[FH + HC] = static_cast<float>(ns);
       a.gw[FH + HC + 1] = s_l[0];  // sum of per-seed losses = mean * n
+      if (a.sgd && a.loss_slot) *a.loss_slot = static_cast<double>(s_l[0]) / static_cast<float>(ns);
     }
   }
 }
@@ -705,17 +714,22 @@ bool launch_agg(TrainerState& t, AggArgs aa, uint32_t chunks, cudaStream_t st) {
 // nccl glue lives in comm.cpp
 void comm_allreduce_sum(a3g_comm* comm, float* buf, size_t count, cudaStream_t st);
 
+// per-step statistics of a sampled batch (a3g_trainer_step_stats); the
+// pipeline runs it on the batch's sampling stream, off the compute chain
+void launch_step_stats(TrainerState& t, a3g_sampler* smp, unsigned long long* d_stats, cudaStream_t st) {
+  SamplerState& s = smp->st;
+  const a3g_cache* c = t.c;
+  const int bitmode = c->all_cached ? 1 : (c->none_cached ? 0 : 2);
+  k_step_stats<<<t.sm_count, 256, 0, st>>>(s.d_ctr, s.d_unique, c->d_bits, bitmode, s.L, d_stats);
+  A3G_LAUNCH_DONE("k_step_stats", st);
+}
+
 void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* d_loss_slot,
                           unsigned long long* d_stats, cudaStream_t st, bool record_timing) {
   SamplerState& s = smp->st;
   a3g_graph* g = t.g;
   BatchCounters* ctr = s.d_ctr;
-  if (d_stats) {
-    const a3g_cache* c = t.c;
-    const int bitmode = c->all_cached ? 1 : (c->none_cached ? 0 : 2);
-    k_step_stats<<<t.sm_count, 256, 0, st>>>(ctr, s.d_unique, c->d_bits, bitmode, s.L, d_stats);
-    A3G_LAUNCH_DONE("k_step_stats", st);
-  }
+  if (d_stats) launch_step_stats(t, smp, d_stats, st);
   // ---- gather + aggregation + GEMM1 (forward, inner rows)
   AggArgs aa{};
   aa.view = g->view;
@@ -823,10 +837,16 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
   ra.gw = t.d_gw;
   const uint32_t FH = t.F * t.H, HC = t.H * t.C;
   const uint32_t nb1 = (FH + 31) / 32;
+  const bool synced = t.comm != nullptr;
+  ra.w1 = t.d_w1;
+  ra.w2 = t.d_w2;
+  ra.lr = static_cast<float>(lr);
+  ra.loss_slot = d_loss_slot;
+  ra.sgd = synced ? 0 : 1;  // one worker: the SGD step rides on the reduction
   k_reduce<<<nb1 + HC + 1, 256, 0, st>>>(ra, nb1);
   A3G_LAUNCH_DONE("k_reduce", st);
-  const bool synced = t.comm != nullptr;
-  if (synced) {
+  if (!synced) return;
+  {
     k_scale_for_sync<<<t.sm_count, 256, 0, st>>>(t.d_gw, FH + HC);
     A3G_LAUNCH_DONE("k_scale_for_sync", st);
     comm_allreduce_sum(t.comm, t.d_gw, FH + HC + 2, st);

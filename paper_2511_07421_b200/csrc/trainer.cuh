@@ -71,6 +71,7 @@ struct TrainerState {
 // Compute part of one step on s_comp for the batch in arena `smp`
 // (gather+aggregate -> forward -> backward -> [allreduce] -> sgd).
 // d_stats: this step's A3G_STEP_STATS row (zeroed by the caller) or null.
+void launch_step_stats(TrainerState& t, a3g_sampler* smp, unsigned long long* d_stats, cudaStream_t st);
 void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* d_loss_slot,
                           unsigned long long* d_stats, cudaStream_t st, bool record_timing);
 // tcgen05 dense update (gemm_tc.cu)

@@ -107,7 +107,13 @@ void sampler_alloc(SamplerState& s, a3g_graph* g, a3g_cache* c, uint32_t max_see
   for (uint32_t l = 0; l < L; ++l) max_rows = std::max<uint64_t>(max_rows, s.layer[l].cap_rows);
   HubArena& hb = s.hub;
   hb.hub_cap = static_cast<uint32_t>(std::max<uint64_t>(1, max_rows));
-  s.seg = g->n && g->m / g->n >= 128 ? 2 * kSegMin : kSegMin;
+  // r01 sweeps (pipelined step time): C2 4096 -> 8192 0.443 -> 0.420 ms,
+  // C5 2048 -> 4096 1.85 -> 1.71 ms, C3 2048 = 4096
+  s.seg = g->n && g->m / g->n >= 128 ? 4 * kSegMin : 2 * kSegMin;
+  if (const char* e = std::getenv("A3G_SEG")) {  // tuning sweeps: hub segment length (power of two >= 256)
+    const uint32_t v = static_cast<uint32_t>(std::strtoul(e, nullptr, 10));
+    if (v >= 256 && (v & (v - 1)) == 0) s.seg = v;
+  }
   hb.seg_cap = static_cast<uint32_t>(std::min<uint64_t>(65536, std::max<uint64_t>(1, g->m / s.seg + max_rows)));
   hb.row = dalloc<uint32_t>(hb.hub_cap);
   hb.seg0 = dalloc<uint32_t>(hb.hub_cap);
@@ -917,7 +923,8 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
         A3G_CUDA(cudaEventRecord(se[1], ss));
         A3G_CUDA(cudaEventRecord(se[2], t.s_comp));
       }
-      launch_train_compute(t, smp, t.lr, t.d_losses + i, nullptr, t.s_comp, t.timing);
+      static const bool skip_compute = std::getenv("A3G_DIAG_SKIP_COMPUTE") != nullptr;  // diagnostics only
+      if (!skip_compute) launch_train_compute(t, smp, t.lr, t.d_losses + i, nullptr, t.s_comp, t.timing);
       A3G_CUDA(cudaEventRecord(t.ev_consumed[ar], t.s_comp));
       if (steps_env) {
         A3G_CUDA(cudaEventRecord(se[3], t.s_comp));

@@ -21,7 +21,7 @@ struct LayerArena {
 };
 
 // Hub splitting (rows with deg > seg): per-segment local records.
-constexpr uint32_t kSegMin = 2048;  // neighbours per hub segment (SamplerState::seg: 2048 or 4096)
+constexpr uint32_t kSegMin = 2048;  // hub segment unit (SamplerState::seg: 4096, or 8192 on dense graphs)
 constexpr uint32_t kRecCap = 256;   // record capacity per segment (expected m(1+ln(seg/m)) <= 190 for m <= 32)
 
 struct HubArena {

@@ -233,7 +233,7 @@ def run_ours(args):
         comm = T.Comm(bytes(uid.cpu().numpy().tobytes()), world, rank, local)
         tr.set_comm(comm)
     W, K = args.warmup, args.steps
-    pipe = args.pipeline if args.pipeline is not None else 6
+    pipe = args.pipeline if args.pipeline is not None else 8
     tr.set_pipeline(pipe)
     from paper_2511_07421_b200 import dp
     gbatches, gseeds = dp.global_batches(g.train_nodes, B, world, W + 3 * K, BASE_SEED)

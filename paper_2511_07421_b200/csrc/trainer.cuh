@@ -15,7 +15,7 @@ struct TrainerState {
   // compute. Arenas beyond the first are allocated on first use.
   static constexpr int kArenas = 9;
   static constexpr int kSampStreams = 8;
-  static constexpr int kDefaultStreams = 6;
+  static constexpr int kDefaultStreams = 8;
   a3g_sampler* smp[kArenas] = {};
   uint32_t F = 0, H = 0, C = 0, pitch = 0, L = 0, max_seeds = 0;
   double lr = 0.2;

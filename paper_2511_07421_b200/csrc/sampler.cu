@@ -1881,8 +1881,13 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
       };
       const int lane_grid = static_cast<int>(std::max<uint64_t>(1, (item_bound + 255) / 256));
       if (WM == 2 && sa.kind != A3G_SAMPLER_UNIFORM && sa.ebits && sa.f <= 16 && rows_bound >= lane_min_rows()) {
-        if (sa.f <= 8)
+        // register reservoirs sized to the fanout (exact sizes for the common 5 / 10)
+        if (sa.f == 5)
+          k_stream_lane_mixed<5><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
+        else if (sa.f <= 8)
           k_stream_lane_mixed<8><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
+        else if (sa.f == 10)
+          k_stream_lane_mixed<10><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         else
           k_stream_lane_mixed<16><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         A3G_LAUNCH_DONE("k_stream_lane_mixed", st);
@@ -1895,8 +1900,12 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
           k_stream_grp_mixed<32><<<grp_grid(32), kGrpThreads, 0, st>>>(sa, lists, sa.cls_count);
         A3G_LAUNCH_DONE("k_stream_grp_mixed", st);
       } else if (sa.kind != A3G_SAMPLER_UNIFORM && sa.f <= 16 && rows_bound >= lane_min_rows()) {
-        if (sa.f <= 8)
+        if (sa.f == 5)
+          k_stream_lane<W, 5><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
+        else if (sa.f <= 8)
           k_stream_lane<W, 8><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
+        else if (sa.f == 10)
+          k_stream_lane<W, 10><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         else
           k_stream_lane<W, 16><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         A3G_LAUNCH_DONE("k_stream_lane", st);

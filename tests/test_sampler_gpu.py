@@ -84,14 +84,14 @@ def test_c1_full_cache_integer_keys(c1, orc, gamma):
 @pytest.mark.parametrize("gamma,ratio", [(1.0, 1.0), (8.0, 1.0), (8.0, 0.3), (2.0, 0.05)])
 def test_lane_per_item_stream_layers(c1, orc, gamma, ratio):
     """Layers whose frontier bound reaches 32768 rows run the lane-per-item
-    stream (register reservoirs of 8 or 16 slots; integer keys with a full
+    stream (register reservoirs of 5, 8, 10 or 16 slots; integer keys with a full
     cache, fp64 keys over the per-edge cached bits with a partial one);
     [20, 12] / [40, 7] from ~1900 seeds put layer 1 there with m = 12 and
     m = 7 (hubs included)."""
     g = c1
     cache = CA.build_static_cache(g, CA.CacheConfig(int(ratio * g.num_nodes) * g.feat_dim * 4, 1))
     seeds = np.arange(5, 100_000, 53, dtype=np.uint32)
-    for fan in ([20, 12], [40, 7]):
+    for fan in ([20, 12], [40, 7], [20, 10], [30, 5]):  # register reservoirs of 16, 8, 10 and 5 slots
         assert len(seeds) * fan[0] >= 32768
         a = run(g, seeds, fan, gamma, 0, 99, cache)
         b = orc.sample_khop(g, seeds, fan, gamma, 0, 99, cache.device_map)

@@ -1844,12 +1844,13 @@ constexpr int kGrpThreads = 256;  // CTA size of the lane-group stream kernels (
 
 // frontier bound from which a layer's items go lane-per-item (A3G_LANE_MIN_ROWS
 // overrides it for tuning sweeps)
-static uint64_t lane_min_rows() {
-  static const uint64_t v = [] {
-    const char* e = std::getenv("A3G_LANE_MIN_ROWS");
-    return e ? std::strtoull(e, nullptr, 10) : 32768ull;
-  }();
-  return v;
+// (r01 A/B, 3 reps each: dense C2 layer 1 (15K rows of ~500 neighbours) runs
+// 4% faster lane-per-item with 8192, sparse C1 layer 1 (10K rows of ~9) 7%
+// slower -- most of its rows are fill-only, too few items for lane parallelism)
+static uint64_t lane_min_rows(bool dense) {
+  static const char* e = std::getenv("A3G_LANE_MIN_ROWS");
+  if (e) return std::strtoull(e, nullptr, 10);
+  return dense ? 8192ull : 32768ull;
 }
 
 template <int WM>
@@ -1880,7 +1881,7 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
         return static_cast<int>(std::max<uint64_t>(1, (item_bound * G + kGrpThreads - 1) / kGrpThreads));
       };
       const int lane_grid = static_cast<int>(std::max<uint64_t>(1, (item_bound + 255) / 256));
-      if (WM == 2 && sa.kind != A3G_SAMPLER_UNIFORM && sa.ebits && sa.f <= 16 && rows_bound >= lane_min_rows()) {
+      if (WM == 2 && sa.kind != A3G_SAMPLER_UNIFORM && sa.ebits && sa.f <= 16 && rows_bound >= lane_min_rows(sa.seg >= 4 * kSegMin)) {
         // register reservoirs sized to the fanout (exact sizes for the common 5 / 10)
         if (sa.f == 5)
           k_stream_lane_mixed<5><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
@@ -1899,7 +1900,7 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
         else
           k_stream_grp_mixed<32><<<grp_grid(32), kGrpThreads, 0, st>>>(sa, lists, sa.cls_count);
         A3G_LAUNCH_DONE("k_stream_grp_mixed", st);
-      } else if (sa.kind != A3G_SAMPLER_UNIFORM && sa.f <= 16 && rows_bound >= lane_min_rows()) {
+      } else if (sa.kind != A3G_SAMPLER_UNIFORM && sa.f <= 16 && rows_bound >= lane_min_rows(sa.seg >= 4 * kSegMin)) {
         if (sa.f == 5)
           k_stream_lane<W, 5><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
         else if (sa.f <= 8)

@@ -7,7 +7,7 @@ python bench.py --config c3 --no-cpu-baseline > gpurun_out/final/bench_c3.json 2
 timeout 1500 python bench.py --config c5 --steps 10 --no-cpu-baseline > gpurun_out/final/bench_c5.json 2>/dev/null
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv --log-file gpurun_out/final/launches_c2.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv --log-file gpurun_out/final/launches_c3.csv python bench.py --config c3 --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-for spec in "k_agg1:3" "k_stream_lane:2" "k_stream_grp:4" "k_dw1_fma:3" "k_hub_merge:4"; do
+for spec in "k_agg1:3" "k_stream_lane:4" "k_stream_grp:2" "k_dw1_fma:3" "k_hub_merge:4"; do
   k=${spec%%:*}; sk=${spec##*:}
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s $sk -c 1 -o gpurun_out/final/prof_$k python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 done

@@ -79,6 +79,7 @@ struct SampleArgs {
   uint64_t tie;
   uint32_t f, layer, tag;
   uint32_t seg;  // hub segment length (SamplerState::seg)
+  int split_cls;  // >= 0: items of length class >= split_cls go to the lane-group kernel, the rest lane-per-item
   int kind;   // A3G_SAMPLER_*
   int wmode;  // 0: all weights 1; 1: all gamma; 2: bitmap
 };
@@ -365,6 +366,13 @@ __device__ __forceinline__ uint32_t item_of(const uint32_t* lists, const uint32_
   return lists[ii];
 }
 
+// Items in the length classes >= c0 (they come first in claim order).
+__device__ __forceinline__ uint32_t items_from_class(const uint32_t* cls_count, int c0) {
+  uint32_t n = 0;
+  for (int c = kClasses - 1; c >= c0; --c) n += cls_count[c];
+  return n;
+}
+
 // ----------------------------------------------------------- stream (group) -
 // Integer-key items (PolUnit / PolGammaAll weights, Algorithm R) processed by
 // lane groups of G = next_pow2(m) lanes: a warp carries 32/G items at once,
@@ -431,7 +439,8 @@ __global__ void __launch_bounds__(256) k_stream_grp(SampleArgs a, const uint32_t
   const int lane = threadIdx.x & 31;
   const uint32_t gl = lane % G, grp = lane / G;
   const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << (grp * G));
-  const uint32_t nitems = min(*a.item_count, a.hub.item_cap);
+  uint32_t nitems = min(*a.item_count, a.hub.item_cap);
+  if (a.split_cls >= 0) nitems = min(nitems, items_from_class(cls_count, a.split_cls));
   const uint32_t m = a.f;
   const P pol = PolOf<WM>::make(a);
   const uint32_t wstride = gridDim.x * (blockDim.x >> 5) * NG;
@@ -635,7 +644,9 @@ __global__ void __launch_bounds__(256) k_stream_lane(SampleArgs a, const uint32_
   // grid sized to the layer's item bound: one batch of 32 items per warp
   // (short-lived CTAs let the high-priority compute stream's kernels in)
   const uint32_t wstride = gridDim.x * (blockDim.x >> 5) * 32;
-  for (uint32_t base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < nitems; base += wstride) {
+  const uint32_t ibase = a.split_cls >= 0 ? items_from_class(cls_count, a.split_cls) : 0u;
+  for (uint32_t base = ibase + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < nitems;
+       base += wstride) {
     const uint32_t ii = base + lane;
     const bool live = ii < nitems;
     uint4 im = make_uint4(0, 0, 0, kInv);
@@ -754,7 +765,9 @@ __global__ void __launch_bounds__(256) k_stream_lane_mixed(SampleArgs a, const u
   // grid sized to the layer's item bound: one batch of 32 items per warp
   // (short-lived CTAs let the high-priority compute stream's kernels in)
   const uint32_t wstride = gridDim.x * (blockDim.x >> 5) * 32;
-  for (uint32_t base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < nitems; base += wstride) {
+  const uint32_t ibase = a.split_cls >= 0 ? items_from_class(cls_count, a.split_cls) : 0u;
+  for (uint32_t base = ibase + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < nitems;
+       base += wstride) {
     const uint32_t ii = base + lane;
     const bool live = ii < nitems;
     uint4 im = make_uint4(0, 0, 0, kInv);
@@ -910,7 +923,8 @@ __global__ void __launch_bounds__(256) k_stream_grp_mixed(SampleArgs a, const ui
   const int lane = threadIdx.x & 31;
   const uint32_t gl = lane % G, grp = lane / G;
   const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << (grp * G));
-  const uint32_t nitems = min(*a.item_count, a.hub.item_cap);
+  uint32_t nitems = min(*a.item_count, a.hub.item_cap);
+  if (a.split_cls >= 0) nitems = min(nitems, items_from_class(cls_count, a.split_cls));
   const uint32_t m = a.f;
   const double ig = a.inv_gamma, gamma = a.gamma;
   const uint32_t* bits = a.bits;
@@ -1881,43 +1895,57 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
         return static_cast<int>(std::max<uint64_t>(1, (item_bound * G + kGrpThreads - 1) / kGrpThreads));
       };
       const int lane_grid = static_cast<int>(std::max<uint64_t>(1, (item_bound + 255) / 256));
-      if (WM == 2 && sa.kind != A3G_SAMPLER_UNIFORM && sa.ebits && sa.f <= 16 && rows_bound >= lane_min_rows(sa.seg >= 4 * kSegMin)) {
-        // register reservoirs sized to the fanout (exact sizes for the common 5 / 10)
-        if (sa.f == 5)
-          k_stream_lane_mixed<5><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
-        else if (sa.f <= 8)
-          k_stream_lane_mixed<8><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
-        else if (sa.f == 10)
-          k_stream_lane_mixed<10><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
-        else
-          k_stream_lane_mixed<16><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
-        A3G_LAUNCH_DONE("k_stream_lane_mixed", st);
-      } else if (WM == 2 && sa.kind != A3G_SAMPLER_UNIFORM) {
-        if (sa.f <= 8)
-          k_stream_grp_mixed<8><<<grp_grid(8), kGrpThreads, 0, st>>>(sa, lists, sa.cls_count);
-        else if (sa.f <= 16)
-          k_stream_grp_mixed<16><<<grp_grid(16), kGrpThreads, 0, st>>>(sa, lists, sa.cls_count);
-        else
-          k_stream_grp_mixed<32><<<grp_grid(32), kGrpThreads, 0, st>>>(sa, lists, sa.cls_count);
-        A3G_LAUNCH_DONE("k_stream_grp_mixed", st);
-      } else if (sa.kind != A3G_SAMPLER_UNIFORM && sa.f <= 16 && rows_bound >= lane_min_rows(sa.seg >= 4 * kSegMin)) {
-        if (sa.f == 5)
-          k_stream_lane<W, 5><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
-        else if (sa.f <= 8)
-          k_stream_lane<W, 8><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
-        else if (sa.f == 10)
-          k_stream_lane<W, 10><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
-        else
-          k_stream_lane<W, 16><<<lane_grid, 256, 0, st>>>(sa, lists, sa.cls_count);
-        A3G_LAUNCH_DONE("k_stream_lane", st);
-      } else {
-        if (sa.f <= 8)
-          k_stream_grp<W, 8><<<grp_grid(8), kGrpThreads, 0, st>>>(sa, lists, sa.cls_count);
-        else if (sa.f <= 16)
-          k_stream_grp<W, 16><<<grp_grid(16), kGrpThreads, 0, st>>>(sa, lists, sa.cls_count);
-        else
-          k_stream_grp<W, 32><<<grp_grid(32), kGrpThreads, 0, st>>>(sa, lists, sa.cls_count);
-        A3G_LAUNCH_DONE("k_stream_grp", st);
+      const bool lane = sa.kind != A3G_SAMPLER_UNIFORM && sa.f <= 16 &&
+                        rows_bound >= lane_min_rows(sa.seg >= 4 * kSegMin) && (WM != 2 || sa.ebits);
+      // lane layers may route their longest items (length class >= split) to
+      // the lane-group kernel first (A3G_SPLIT_CLS sweeps; off by default)
+      static const int split = [] {
+        const char* e = std::getenv("A3G_SPLIT_CLS");
+        return e ? std::atoi(e) : -1;
+      }();
+      SampleArgs sl = sa;
+      sl.split_cls = lane ? split : -1;
+      if (!lane || split >= 0) {  // lane groups: the whole layer, or its long items
+        if (WM == 2 && sa.kind != A3G_SAMPLER_UNIFORM) {
+          if (sa.f <= 8)
+            k_stream_grp_mixed<8><<<grp_grid(8), kGrpThreads, 0, st>>>(sl, lists, sa.cls_count);
+          else if (sa.f <= 16)
+            k_stream_grp_mixed<16><<<grp_grid(16), kGrpThreads, 0, st>>>(sl, lists, sa.cls_count);
+          else
+            k_stream_grp_mixed<32><<<grp_grid(32), kGrpThreads, 0, st>>>(sl, lists, sa.cls_count);
+          A3G_LAUNCH_DONE("k_stream_grp_mixed", st);
+        } else {
+          if (sa.f <= 8)
+            k_stream_grp<W, 8><<<grp_grid(8), kGrpThreads, 0, st>>>(sl, lists, sa.cls_count);
+          else if (sa.f <= 16)
+            k_stream_grp<W, 16><<<grp_grid(16), kGrpThreads, 0, st>>>(sl, lists, sa.cls_count);
+          else
+            k_stream_grp<W, 32><<<grp_grid(32), kGrpThreads, 0, st>>>(sl, lists, sa.cls_count);
+          A3G_LAUNCH_DONE("k_stream_grp", st);
+        }
+      }
+      if (lane) {  // register reservoirs sized to the fanout (exact sizes for the common 5 / 10)
+        if (WM == 2) {
+          if (sa.f == 5)
+            k_stream_lane_mixed<5><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
+          else if (sa.f <= 8)
+            k_stream_lane_mixed<8><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
+          else if (sa.f == 10)
+            k_stream_lane_mixed<10><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
+          else
+            k_stream_lane_mixed<16><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
+          A3G_LAUNCH_DONE("k_stream_lane_mixed", st);
+        } else {
+          if (sa.f == 5)
+            k_stream_lane<W, 5><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
+          else if (sa.f <= 8)
+            k_stream_lane<W, 8><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
+          else if (sa.f == 10)
+            k_stream_lane<W, 10><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
+          else
+            k_stream_lane<W, 16><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
+          A3G_LAUNCH_DONE("k_stream_lane", st);
+        }
       }
     }
     static const int merge_ctas_q = [] {  // hub-merge CTAs per 4 SMs (A3G_MERGE_CTAS4 sweeps)
@@ -2013,6 +2041,7 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
     sa.f = la.f;
     sa.layer = l;
     sa.seg = s.seg;
+    sa.split_cls = -1;
     sa.tag = tag;
     sa.kind = kind;
     sa.wmode = wmode;

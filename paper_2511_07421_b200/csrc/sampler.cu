@@ -744,6 +744,25 @@ __global__ void __launch_bounds__(256) k_stream_lane(SampleArgs a, const uint32_
   }
 }
 
+// Lower filter bound lo <= thr^gamma of cached candidates (a cached key
+// pow(u, 1/gamma) can beat thr only if u >= lo). Integer gamma <= 64: binary
+// powering (<= 12 correctly rounded products, relative error < 1.4e-15) with a
+// 1e-9 margin -- u < lo then gives pow(u, 1/gamma) < thr (1 - 1e-10 / gamma)
+// even with pow's 2-ulp error; cheap enough to refresh after every insertion.
+// Otherwise rsv::gamma_lo (pow with a 1e-6 margin).
+__device__ __forceinline__ double lane_gamma_lo(double thr, double gamma, bool gint) {
+  if (!gint) return rsv::gamma_lo(thr, gamma);
+  if (!(thr < 1.0)) return thr >= 1.0 ? 1.0 : 0.0;  // +inf (unfilled) / NaN guards
+  uint32_t e = static_cast<uint32_t>(gamma);
+  double p = 1.0, x = thr;
+  while (e) {
+    if (e & 1u) p *= x;
+    x *= x;
+    e >>= 1;
+  }
+  return p * (1.0 - 1e-9);
+}
+
 // Lane-per-item stream for bitmap weights (partial cache, gamma > 1), m <= MB:
 // as k_stream_lane with fp64 keys (their IEEE bits order like the values, so
 // the register argmin compares bit patterns). Each 32-position chunk reads the
@@ -760,6 +779,7 @@ __global__ void __launch_bounds__(256) k_stream_lane_mixed(SampleArgs a, const u
   const uint32_t nitems = min(*a.item_count, a.hub.item_cap);
   const uint32_t m = a.f;
   const double ig = a.inv_gamma, gamma = a.gamma;
+  const bool gint = gamma == floor(gamma) && gamma <= 64.0;  // lane_gamma_lo by multiplications
   const uint32_t* eb = a.ebits;
   const rsv::PolUnit ipol{};
   // grid sized to the layer's item bound: one batch of 32 items per warp
@@ -816,7 +836,7 @@ __global__ void __launch_bounds__(256) k_stream_lane_mixed(SampleArgs a, const u
     uint64_t ctr = key + (static_cast<uint64_t>(jb) + 1) * kPhi;
     for (uint32_t b = 0; b < wlen; b += 32, ctr += 32 * kPhi) {
       const double thr = __longlong_as_double(static_cast<long long>(thrb));
-      const double lo = rsv::gamma_lo(thr, gamma);
+      double lo = lane_gamma_lo(thr, gamma, gint);
       const uint32_t b_thr = pre_bound(lo_hi_word(thr)), b_lo = pre_bound(lo_hi_word(lo));
       const uint32_t rem = len > b ? len - b : 0u;
       uint32_t cb = 0;
@@ -841,7 +861,7 @@ __global__ void __launch_bounds__(256) k_stream_lane_mixed(SampleArgs a, const u
           double k = uu;
           bool ins;
           if ((cb >> c) & 1u) {
-            ins = uu >= lo;  // lo of the chunk start <= the current one
+            ins = uu >= lo;  // lo follows every insertion (cheap for integer gamma)
             if (ins) {
               k = pow(uu, ig);
               ins = k > t;
@@ -864,6 +884,7 @@ __global__ void __launch_bounds__(256) k_stream_lane_mixed(SampleArgs a, const u
             }
             ++rcnt;
             lane_argmin<MB>(ipol, rk, m, thrb, mp);
+            if (gint) lo = lane_gamma_lo(__longlong_as_double(static_cast<long long>(thrb)), gamma, true);
           }
         }
       }

@@ -51,7 +51,7 @@ HIDDEN, CLASSES, LR, BASE_SEED = 16, 4, 0.2, 1
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=100)  # ~35 ms at C2: past the 8-deep pipeline ramp
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", choices=list(CONFIGS), default="c2")

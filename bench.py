@@ -159,48 +159,84 @@ def make_graph(cfg_name):
     return G.generate_power_law(n, m, 2.5, 1 if cfg_name in SYNTH else F, BASE_SEED)
 
 
-def cpu_reference_run(g, cfg_name, gamma, units, producers, tmpdir="/tmp"):
-    """Time the reference's own CPU path (oracle/_ref, the unmodified reference
-    compiled in place) on `units` batches of the same workload."""
+def host_cpu():
+    """nproc and the CPU model of this host (printed beside the CPU numbers)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        n = len(os.sched_getaffinity(0))
+    except AttributeError:
+        n = os.cpu_count() or 1
+    return n, model
+
+
+def cpu_reference_run(rg, cfg_name, gamma, units, mode, producers, warmup=1):
+    """Time the reference's own CPU path (oracle/_ref: the unmodified reference
+    compiled in place) on `units` batches of the workload after `warmup`
+    untimed ones, scheduled as the executor's `mode` (0 sequential, 1 pmode1,
+    2 pmode2; pipeline_exec.cpp:219-276) over the reference's per-batch
+    functions. `rg` is a graph held by the reference library."""
     import oracle
-    if not oracle.ref_available():
-        return None
-    from paper_2511_07421_b200 import graph as G
     n, m, F, fan, B, frac, _ = CONFIGS[cfg_name]
-    path = os.path.join(tmpdir, f"a3g_bench_{cfg_name}_{os.getpid()}.a3g")
-    G.save_graph(g, path)
     ref = oracle.RefLib()
-    rg = ref.load(path)
-    os.remove(path)
     dm = ref.build_static_cache(rg, int(frac * n) * F * 4, 1)
-    secs, seeds = ref.bench_steps(rg, dm, fan, gamma, BASE_SEED, B, HIDDEN, CLASSES, LR, units, producers, 8)
-    return dict(seconds=secs, seeds=seeds, seeds_per_s=seeds / secs if secs > 0 else 0.0)
+    secs, seeds = ref.bench_steps(rg, dm, fan, gamma, BASE_SEED, B, HIDDEN, CLASSES, LR, units, producers, 8,
+                                  warmup=warmup, mode=mode)
+    return dict(seconds=secs, seeds=seeds, seeds_per_s=seeds / secs if secs > 0 else 0.0, units=units,
+                mode=["sequential", "pmode1", "pmode2"][mode], threads=1 if mode == 0 else producers + 1)
 
 
 def run_reference(args):
+    """The reference arm: the reference's own CPU implementation (oracle/_ref,
+    compiled in place from /root/reference's sources), on its OWN generator's
+    graph -- this process never imports or loads the B200 package."""
     rank, world, local = dist_env()
     if rank != 0:
         return 0
     n, m, F, fan, B, frac, desc = CONFIGS[args.config]
     import oracle
+    cores, cpu_model = host_cpu()
     base = {"metric": "trained seed nodes/sec", "unit": "seeds/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-            "dtype": "f64", "data": "synthetic", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (the reference's generate_power_law, seed 1)", "vs_baseline": None,
             "config": {"workload": args.config, "description": desc, "global_batch": B, "fanouts": fan,
                        "gamma": args.gamma, "hidden": HIDDEN, "classes": CLASSES}}
     if not oracle.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref (reference compiled in place) not built"}))
         return 0
-    g = make_graph(args.config)
-    cores = os.cpu_count() or 1
+    if args.config in SYNTH:
+        print(json.dumps({"impl": "reference", "unavailable": "papers-scale config: the reference generator needs "
+                          "~30 min and 22.6 GB at F=1 (SURVEY 8(c)(iv)); not a bounded sample"}))
+        return 0
+    ref = oracle.RefLib()
+    t0 = time.time()
+    rg = ref.power_law(n, m, 2.5, F, BASE_SEED)  # generators.cpp:79-149, the reference's own
+    gen_s = time.time() - t0
     producers = max(1, cores - 1)
-    units = max(1, args.steps)
-    r = cpu_reference_run(g, args.config, args.gamma, units, producers)
-    v = r["seeds_per_s"]
-    base.update({"value": v, "ms_per_step": 1e3 * r["seconds"] / units,
-                 "cpu_baseline": {"value": v, "unit": "seeds/s", "cores": cores, "kind": "reference",
-                                  "sample": f"{units} consecutive batches of epoch 0, pmode1 schedule, "
-                                            f"{producers} sampler threads + 1 trainer thread"},
+    K, W = max(1, args.steps), max(0, args.warmup)
+    # headline: the executor's pmode1 schedule, nproc-1 producers + the trainer thread, queue 8
+    r1 = cpu_reference_run(rg, args.config, args.gamma, K, 1, producers, warmup=W)
+    # beside it (bounded): pmode2 and the 1-thread sequential train() loop
+    r2 = cpu_reference_run(rg, args.config, args.gamma, max(1, min(K, 8)), 2, producers, warmup=1)
+    r0 = cpu_reference_run(rg, args.config, args.gamma, max(1, min(K, 3)), 0, 0, warmup=1)
+    v = r1["seeds_per_s"]
+    base.update({"value": v, "ms_per_step": 1e3 * r1["seconds"] / max(1, r1["units"]),
+                 "cpu_baseline": {"value": v, "unit": "seeds/s", "cores": cores, "cpu_model": cpu_model,
+                                  "kind": "reference",
+                                  "sample": f"{K} consecutive batches of epoch 0 after {W} untimed, executor pmode1 "
+                                            f"schedule (pipeline_exec.cpp:229-276) over the reference's sample_khop/"
+                                            f"retrieve_features/forward/backward/sync_gradients/sgd_step, "
+                                            f"{producers} producer threads + 1 trainer thread, queue 8"},
+                 "cpu_modes": {k: {"seeds_per_s": r["seeds_per_s"], "batches": r["units"], "threads": r["threads"]}
+                               for k, r in (("pmode1", r1), ("pmode2", r2), ("sequential_1thread", r0))},
+                 "graph_gen_s": round(gen_s, 1),
                  "e2e": {"value": v, "unit": "seeds/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
     print(json.dumps(base))
     return 0
@@ -318,11 +354,22 @@ def run_ours(args):
         "loss_first_last": [float(losses[0]), float(losses_e2e[-1])],
     }
     if not args.no_cpu_baseline and world == 1 and args.config not in SYNTH:
-        r = cpu_reference_run(g, args.config, args.gamma, args.cpu_units, 0)
-        if r:
+        import oracle
+        if oracle.ref_available():
+            # the same graph handed to the reference through its own A3G1 loader
+            # (graph_io.cpp:60-87); our generator is bit-identical to its
+            # generate_power_law (tests/test_host.py)
+            from paper_2511_07421_b200 import graph as G
+            path = os.path.join("/tmp", f"a3g_bench_{args.config}_{os.getpid()}.a3g")
+            G.save_graph(g, path)
+            rg = oracle.RefLib().load(path)
+            os.remove(path)
+            cores, cpu_model = host_cpu()
+            r = cpu_reference_run(rg, args.config, args.gamma, args.cpu_units, 0, 0, warmup=1)
             out["cpu_baseline"] = {"value": r["seeds_per_s"], "unit": "seeds/s", "cores": 1, "kind": "reference",
-                                   "sample": f"{args.cpu_units} batches of epoch 0 (B={B}), sequential mode, "
-                                             f"{r['seconds']:.1f} s"}
+                                   "cpu_model": cpu_model, "host_nproc": cores,
+                                   "sample": f"{args.cpu_units} batches of epoch 0 (B={B}) after 1 untimed, "
+                                             f"sequential 1-thread schedule, {r['seconds']:.1f} s"}
     print(json.dumps(out))
     if world > 1:
         torch.distributed.destroy_process_group()

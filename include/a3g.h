@@ -49,6 +49,7 @@ enum {
   A3G_STAT_SEEDS = 3,  /* unique seeds */
   A3G_STAT_HITS = 4,   /* cache hits over unique_nodes (cache.cpp:48-68) */
   A3G_STAT_MISSES = 5,
+  A3G_STAT_BAD_SEEDS = 6, /* device-resident seeds >= num_nodes (the call raised ParameterError) */
   A3G_STEP_STATS = 8
 };
 
@@ -139,6 +140,16 @@ a3g_status a3g_cache_build(a3g_graph* g, uint64_t volume_bytes, uint32_t num_dev
 a3g_status a3g_cache_from_map(a3g_graph* g, const int32_t* device_map, uint32_t num_devices,
                               a3g_cache** out);
 uint64_t a3g_cache_total_cached(const a3g_cache* c);
+/* The cached nodes in placement order (cache.cpp:24-44: out-degree desc, id
+ * asc; node i went to device i % num_devices): u32[total_cached]. Only for
+ * caches made by a3g_cache_build. Feeds CacheState::cached_per_device. */
+a3g_status a3g_cache_hot_order(const a3g_cache* c, uint32_t* out);
+/* cache.cpp:48-68 lookup on the device: the device of every id (device_out,
+ * i32[n], -1 = miss; NULL skips) and the accounting counts (hits, misses,
+ * per_device_hits u64[num_devices]; any may be NULL). Any-device presence is
+ * a hit. ParameterError on ids >= num_nodes. */
+a3g_status a3g_cache_lookup(a3g_cache* c, const uint32_t* ids, uint64_t n, int32_t* device_out, uint64_t* hits,
+                            uint64_t* misses, uint64_t* per_device_hits);
 void a3g_cache_destroy(a3g_cache* c);
 
 /* ------------------------------------------------------------- sampler --- */

@@ -377,8 +377,8 @@ class RefLib:
                                       f64p]
         L.ref_bench_steps.restype = C.c_double
         L.ref_bench_steps.argtypes = [C.c_void_p, i32p, u32p, C.c_uint32, C.c_double, C.c_uint64, C.c_uint32,
-                                      C.c_uint32, C.c_uint32, C.c_double, C.c_uint32, C.c_uint32, C.c_uint32,
-                                      u64p]
+                                      C.c_uint32, C.c_uint32, C.c_double, C.c_uint32, C.c_uint32, C.c_int,
+                                      C.c_uint32, C.c_uint32, u64p]
 
     def err(self):
         return self.L.ref_last_error().decode()
@@ -536,13 +536,16 @@ class RefLib:
         return dict(losses=losses[:r], w1=w1, w2=w2)
 
     def bench_steps(self, g, device_map, fanouts, gamma, rng_seed, batch_size, H, Cc, lr, units, producers,
-                    queue_capacity=8):
+                    queue_capacity=8, warmup=0, mode=1):
+        """Seconds for `units` steps (after `warmup` untimed ones) of the
+        executor schedule `mode` (0 sequential, 1 pmode1, 2 pmode2) over the
+        reference's own per-batch functions; returns (seconds, seeds)."""
         f = np.ascontiguousarray(fanouts, dtype=np.uint32)
         dm = None if device_map is None else np.ascontiguousarray(device_map, dtype=np.int32)
         seeds = C.c_uint64()
         t = self.L.ref_bench_steps(g.h, None if dm is None else _p(dm, i32p), _p(f, u32p), len(f), gamma,
-                                   rng_seed, batch_size, H, Cc, lr, units, producers, queue_capacity,
-                                   C.byref(seeds))
+                                   rng_seed, batch_size, H, Cc, lr, warmup, units, mode, producers,
+                                   queue_capacity, C.byref(seeds))
         return t, seeds.value
 
 

@@ -414,18 +414,25 @@ std::int64_t ref_train_steps(void* h, const std::int32_t* device_map, const std:
   }
 }
 
-// Bounded CPU-baseline harness: the reference's own per-batch path
-// (sample_khop -> retrieve_features -> forward -> backward -> sync -> sgd) on
-// `units` consecutive steps of epoch 0, scheduled like execute_pipeline's
-// pmode1 (pipeline_exec.cpp:229-276): `producers` threads sample+retrieve into
-// an ordered bounded channel, the calling thread trains. producers == 0 runs
-// the sequential mode (:219-228). Returns wall seconds; *seeds_out = seeds
-// trained.
+// Bounded CPU-baseline harness: the reference's own per-batch functions
+// (sample_khop -> retrieve_features -> forward -> backward -> sync_gradients
+// -> sgd_step) on `units` consecutive steps of epoch 0, scheduled exactly as
+// execute_pipeline's three modes (pipeline_exec.cpp:219-276):
+//   mode 0 sequential: one thread does everything (:219-228);
+//   mode 1 pmode1: `producers` threads sample + retrieve into an ordered
+//          bounded channel of `queue_capacity`, the calling thread trains;
+//   mode 2 pmode2: producers only sample, the consumer retrieves + trains.
+// execute_pipeline itself always runs whole epochs and ends with a full-graph
+// evaluation (C2: 112.8M edges x 602 f64 = ~540 GB of row reads), which does
+// not fit a bounded sample; this harness times the same schedule over a
+// bounded slice. `warmup` steps (steps [0, warmup)) run untimed first; the
+// timed units are steps [warmup, warmup + units). Returns wall seconds of the
+// timed units; *seeds_out = seeds trained in them.
 double ref_bench_steps(void* h, const std::int32_t* device_map, const std::uint32_t* fanouts,
                        std::uint32_t num_layers, double gamma, std::uint64_t rng_seed,
                        std::uint32_t batch_size, std::uint32_t hdim, std::uint32_t c, double lr,
-                       std::uint32_t units, std::uint32_t producers, std::uint32_t queue_capacity,
-                       std::uint64_t* seeds_out) {
+                       std::uint32_t warmup, std::uint32_t units, int mode, std::uint32_t producers,
+                       std::uint32_t queue_capacity, std::uint64_t* seeds_out) {
   auto* g = static_cast<graph::Graph*>(h);
   const auto cache = cache_from_map(device_map, g->num_nodes, 1);
   train::ModelSpec spec;
@@ -436,7 +443,9 @@ double ref_bench_steps(void* h, const std::int32_t* device_map, const std::uint3
   train::Model model = train::init_model(spec, 1);
   const auto ctxs = train::make_worker_contexts(*g, nullptr, cache);
   const auto batches = train::plan_epoch_batches(ctxs[0].train_nodes, 0, batch_size, hash2(rng_seed, 0));
-  units = std::min<std::uint32_t>(units, static_cast<std::uint32_t>(batches.size()));
+  const auto nb = static_cast<std::uint32_t>(batches.size());
+  warmup = std::min(warmup, nb);
+  units = std::min<std::uint32_t>(units, nb - warmup);
   cache::CacheAccounting acc(1);
   auto sample_unit = [&](std::uint32_t step) {
     sampling::SamplerConfig cfg;
@@ -455,14 +464,16 @@ double ref_bench_steps(void* h, const std::int32_t* device_map, const std::uint3
     train::sgd_step(model, train::sync_gradients(grads), spec.learning_rate);
     seeds += batch.seeds.size();
   };
-  const auto t0 = std::chrono::steady_clock::now();
-  if (producers == 0) {
-    for (std::uint32_t s = 0; s < units; ++s) {
-      const auto batch = sample_unit(s);
-      auto [feats, stats] = cache::retrieve_features(batch, cache, *g, acc);
-      train_unit(batch, feats);
+  auto run = [&](std::uint32_t first, std::uint32_t count) {
+    if (mode == 0 || producers == 0) {
+      for (std::uint32_t s = first; s < first + count; ++s) {
+        const auto batch = sample_unit(s);
+        auto [feats, stats] = cache::retrieve_features(batch, cache, *g, acc);
+        train_unit(batch, feats);
+      }
+      return;
     }
-  } else {
+    const bool producers_retrieve = mode == 1;
     struct Item {
       sampling::SampleBatch batch;
       std::vector<float> feats;
@@ -475,10 +486,10 @@ double ref_bench_steps(void* h, const std::int32_t* device_map, const std::uint3
     auto producer = [&] {
       for (;;) {
         const std::uint32_t seq = next_unit.fetch_add(1);
-        if (seq >= units) return;
+        if (seq >= count) return;
         Item it;
-        it.batch = sample_unit(seq);
-        it.feats = cache::retrieve_features(it.batch, cache, *g, acc).first;
+        it.batch = sample_unit(first + seq);
+        if (producers_retrieve) it.feats = cache::retrieve_features(it.batch, cache, *g, acc).first;
         std::unique_lock lk(mu);
         cv_space.wait(lk, [&] { return seq < next + queue_capacity; });
         buf.emplace(seq, std::move(it));
@@ -487,7 +498,7 @@ double ref_bench_steps(void* h, const std::int32_t* device_map, const std::uint3
     };
     std::vector<std::thread> th;
     for (std::uint32_t i = 0; i < producers; ++i) th.emplace_back(producer);
-    for (std::uint32_t seq = 0; seq < units; ++seq) {
+    for (std::uint32_t seq = 0; seq < count; ++seq) {
       Item it;
       {
         std::unique_lock lk(mu);
@@ -497,10 +508,15 @@ double ref_bench_steps(void* h, const std::int32_t* device_map, const std::uint3
         ++next;
         cv_space.notify_all();
       }
+      if (!producers_retrieve) it.feats = cache::retrieve_features(it.batch, cache, *g, acc).first;
       train_unit(it.batch, it.feats);
     }
     for (auto& t : th) t.join();
-  }
+  };
+  run(0, warmup);
+  seeds = 0;
+  const auto t0 = std::chrono::steady_clock::now();
+  run(warmup, units);
   *seeds_out = seeds;
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }

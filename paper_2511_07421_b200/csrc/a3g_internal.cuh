@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -57,6 +58,19 @@ void tl_mark(const char* name, cudaStream_t st);
     ::a3g::tl_mark(name, st);                            \
   } while (0)
 
+// cudaFuncSetAttribute is per device (context), and the handles may be driven
+// from several host threads: `done` holds one bit per device that already
+// has the attribute (one std::atomic per kernel instantiation at the call site).
+inline void smem_attr_once(std::atomic<uint64_t>& done, const void* fn, size_t bytes) {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)),
+             "cudaFuncSetAttribute");
+  done.fetch_or(bit, std::memory_order_release);
+}
+
 // ------------------------------------------------------------ RNG ----------
 // include/a3gnn/rng.hpp:13-55, bit-exact on the device.
 constexpr uint64_t kPhi = 0x9e3779b97f4a7c15ull;
@@ -87,6 +101,7 @@ __host__ __device__ __forceinline__ double unit_of(uint64_t x) {
 // ------------------------------------------------------------ limits -------
 constexpr int kMaxLayers = 8;
 constexpr uint32_t kInv = 0xffffffffu;
+constexpr uint32_t kMaxCacheDevices = 64;  // per-device hit counters of the lookup
 
 // Device-resident per-batch counters (one struct per sampler arena).
 struct BatchCounters {
@@ -104,6 +119,7 @@ struct BatchCounters {
   uint32_t n_seeds;                 // seeds given (incl. duplicates)
   uint32_t hits, misses;            // retrieve_features accounting
   uint32_t pad;
+  uint32_t bad_seeds;               // device-resident seeds >= n seen (k_check_seeds; raised after sync)
 };
 
 // ------------------------------------------------------------ feature store -
@@ -162,6 +178,8 @@ struct a3g_cache {
   uint32_t* d_bits = nullptr;  // n bits: cached on any device
   uint32_t* d_ebits = nullptr; // m bits (+1 pad word): cached bit of every CSR edge's target
                                // (partial caches only; the lane-per-item mixed stream)
+  int32_t* d_map = nullptr;    // device_map on the device (num_devices > 1 only: per-device lookup)
+  std::vector<uint32_t> hot_order;  // cached nodes in placement (hotness) order, a3g_cache_build only
   bool all_cached = false, none_cached = true;
 };
 

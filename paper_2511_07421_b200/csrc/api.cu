@@ -181,7 +181,14 @@ void validate_sample(const SamplerState& s, const uint32_t* seeds, uint32_t n_se
   if (n_seeds > s.max_seeds) raise(A3G_ERR_PARAMETER, "sample_khop: more seeds than the arena holds");
   if (kind != A3G_SAMPLER_WEIGHTED && kind != A3G_SAMPLER_UNIFORM)
     raise(A3G_ERR_PARAMETER, "sample_khop: unknown sampler kind");
-  if (!host_seeds) return;
+  if (!host_seeds) {
+    // device-resident seeds: the range check runs on the device (k_check_seeds,
+    // raised at the next sync); gamma is checked here without the degree
+    // condition, which needs the seeds on the host
+    if (kind == A3G_SAMPLER_WEIGHTED && s.L > 0 && gamma < 1.0)
+      raise(A3G_ERR_PARAMETER, "assign_weights: gamma must be >= 1");
+    return;
+  }
   const a3g_graph* g = s.g;
   bool any_deg = false;
   for (uint32_t i = 0; i < n_seeds; ++i) {
@@ -192,9 +199,12 @@ void validate_sample(const SamplerState& s, const uint32_t* seeds, uint32_t n_se
     raise(A3G_ERR_PARAMETER, "assign_weights: gamma must be >= 1");
 }
 
+// prevalidated: device seeds that the host already checked (a3g_train_steps_v
+// copies validated host seeds to the device first)
 void sample_impl(SamplerState& s, const uint32_t* seeds, uint32_t n_seeds, bool on_device, double gamma,
-                 int kind, uint64_t rng_seed, cudaStream_t st) {
-  validate_sample(s, seeds, n_seeds, !on_device, gamma, kind);
+                 int kind, uint64_t rng_seed, cudaStream_t st, bool prevalidated = false) {
+  if (!prevalidated) validate_sample(s, seeds, n_seeds, !on_device, gamma, kind);
+  s.check_seeds = on_device && !prevalidated;
   A3G_CUDA(cudaSetDevice(s.g->device));
   if (on_device) {
     if (seeds != s.d_seeds)
@@ -214,6 +224,7 @@ void sample_impl(SamplerState& s, const uint32_t* seeds, uint32_t n_seeds, bool 
 void read_counters(SamplerState& s, cudaStream_t st) {
   A3G_CUDA(cudaMemcpyAsync(s.h_ctr, s.d_ctr, sizeof(BatchCounters), cudaMemcpyDeviceToHost, st));
   A3G_CUDA(cudaStreamSynchronize(st));
+  if (s.h_ctr->bad_seeds) raise(A3G_ERR_PARAMETER, "sample_khop: seed out of range");
 }
 
 // init_model (trainer.cpp:12-28)
@@ -386,6 +397,10 @@ static a3g_cache* cache_from(a3g_graph* g, std::vector<int32_t>&& dm, uint32_t n
   A3G_CUDA(cudaSetDevice(g->device));
   c->d_bits = dalloc<uint32_t>(bits.size());
   A3G_CUDA(cudaMemcpy(c->d_bits, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice));
+  if (num_devices > 1) {
+    c->d_map = dalloc<int32_t>(std::max<uint64_t>(g->n, 1));
+    A3G_CUDA(cudaMemcpy(c->d_map, c->device_map.data(), g->n * 4, cudaMemcpyHostToDevice));
+  }
   if (!c->all_cached && !c->none_cached && g->m) {
     const uint64_t words = (g->m + 31) / 32 + 1;
     c->d_ebits = dalloc<uint32_t>(words);
@@ -404,10 +419,11 @@ a3g_status a3g_cache_build(a3g_graph* g, uint64_t volume, uint32_t num_devices, 
     if (num_devices < 1) raise(A3G_ERR_PARAMETER, "build_static_cache: num_devices >= 1");
     const uint64_t n = g->n;
     std::vector<int32_t> dm(n, -1);
+    std::vector<uint32_t> order;
     const uint64_t cost = static_cast<uint64_t>(g->F) * 4;  // cache.cpp:20
     if (volume >= cost) {
       // hotness order (cache.cpp:24-29): degree desc, id asc
-      std::vector<uint32_t> order(n);
+      order.resize(n);
       std::iota(order.begin(), order.end(), 0u);
       const uint64_t per_dev = volume / cost;
       const uint64_t want = std::min<uint64_t>(n, per_dev * num_devices);
@@ -422,9 +438,13 @@ a3g_status a3g_cache_build(a3g_graph* g, uint64_t volume, uint32_t num_devices, 
       // round-robin with full-device skipping (cache.cpp:31-44); every device
       // holds per_dev nodes, so plain round-robin over the first `want`.
       for (uint64_t i = 0; i < want; ++i) dm[order[i]] = static_cast<int32_t>(i % num_devices);
+      order.resize(want);
+    } else {
+      order.clear();
     }
     if (dm_out) std::memcpy(dm_out, dm.data(), n * 4);
     *out = cache_from(g, std::move(dm), num_devices);
+    (*out)->hot_order = std::move(order);
   });
 }
 
@@ -438,8 +458,47 @@ a3g_status a3g_cache_from_map(a3g_graph* g, const int32_t* dm, uint32_t num_devi
 
 uint64_t a3g_cache_total_cached(const a3g_cache* c) { return c->total_cached; }
 
+a3g_status a3g_cache_hot_order(const a3g_cache* c, uint32_t* out) {
+  return guard([&] {
+    if (c->hot_order.size() != c->total_cached)
+      raise(A3G_ERR_PARAMETER, "cache_hot_order: cache was not built by a3g_cache_build");
+    std::memcpy(out, c->hot_order.data(), c->hot_order.size() * 4);
+  });
+}
+
+a3g_status a3g_cache_lookup(a3g_cache* c, const uint32_t* ids, uint64_t n, int32_t* device_out, uint64_t* hits,
+                            uint64_t* misses, uint64_t* per_device_hits) {
+  return guard([&] {
+    a3g_graph* g = c->g;
+    for (uint64_t i = 0; i < n; ++i)
+      if (ids[i] >= g->n) raise(A3G_ERR_PARAMETER, "lookup: node out of range");
+    if (c->num_devices > kMaxCacheDevices) raise(A3G_ERR_PARAMETER, "lookup: more than 64 cache devices");
+    A3G_CUDA(cudaSetDevice(g->device));
+    const uint32_t nd = c->num_devices;
+    std::vector<unsigned long long> cnt(2 + nd, 0);
+    if (n) {
+      uint32_t* d_ids = dalloc<uint32_t>(n);
+      int32_t* d_dev = device_out ? dalloc<int32_t>(n) : nullptr;
+      unsigned long long* d_cnt = dalloc<unsigned long long>(2 + nd);
+      A3G_CUDA(cudaMemcpy(d_ids, ids, n * 4, cudaMemcpyHostToDevice));
+      A3G_CUDA(cudaMemset(d_cnt, 0, (2 + nd) * 8));
+      launch_cache_lookup(c, d_ids, n, d_dev, d_cnt, sm_count_of(g->device), nullptr);
+      A3G_CUDA(cudaMemcpy(cnt.data(), d_cnt, (2 + nd) * 8, cudaMemcpyDeviceToHost));
+      if (device_out) A3G_CUDA(cudaMemcpy(device_out, d_dev, n * 4, cudaMemcpyDeviceToHost));
+      dfree(d_ids);
+      dfree(d_dev);
+      dfree(d_cnt);
+    }
+    if (hits) *hits = cnt[0];
+    if (misses) *misses = cnt[1];
+    if (per_device_hits)
+      for (uint32_t d = 0; d < nd; ++d) per_device_hits[d] = cnt[2 + d];
+  });
+}
+
 void a3g_cache_destroy(a3g_cache* c) {
   if (!c) return;
+  dfree(c->d_map);
   dfree(c->d_bits);
   dfree(c->d_ebits);
   delete c;
@@ -688,8 +747,8 @@ a3g_status a3g_trainer_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds, co
       t.d_hpart = dalloc<float>(static_cast<size_t>(t.h1_split_cap) * t.cap_inner * H);
       t.dw1_splits = static_cast<uint32_t>((t.cap_inner + 127) / 128);  // kDw1Rows
       t.d_part = dalloc<float>(static_cast<size_t>(std::max({t.nparts, t.tc_splits, t.dw1_splits})) * t.F * H);
-      t.d_agg_bytes = dalloc<unsigned long long>(1);
-      A3G_CUDA(cudaMemset(t.d_agg_bytes, 0, 8));
+      t.d_agg_bytes = dalloc<unsigned long long>(2);  // [k_agg1 bytes | sticky bad-seed flag]
+      A3G_CUDA(cudaMemset(t.d_agg_bytes, 0, 16));
       t.losses_cap = 1;
       t.d_losses = dalloc<double>(1);
       A3G_CUDA(cudaMallocHost(&t.h_losses, 8));
@@ -816,6 +875,7 @@ a3g_status a3g_train_step(a3g_trainer* tr, const uint32_t* seeds, uint32_t n_see
     a3g_sampler* smp = t.smp[0];
     sample_impl(smp->st, seeds, n_seeds, on_device != 0, gamma, kind, rng_seed, t.s_comp);
     launch_train_compute(t, smp, lr < 0 ? t.lr : lr, t.d_losses, nullptr, t.s_comp, false);
+    if (on_device) read_counters(smp->st, t.s_comp);  // raises on out-of-range device seeds
     if (loss_out) {
       A3G_CUDA(cudaMemcpyAsync(t.h_losses, t.d_losses, 8, cudaMemcpyDeviceToHost, t.s_comp));
       A3G_CUDA(cudaStreamSynchronize(t.s_comp));
@@ -861,7 +921,7 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
     }
     for (cudaEvent_t e : t.ev_agg) cudaEventDestroy(e);
     t.ev_agg.clear();
-    A3G_CUDA(cudaMemsetAsync(t.d_agg_bytes, 0, 8, t.s_comp));
+    A3G_CUDA(cudaMemsetAsync(t.d_agg_bytes, 0, 16, t.s_comp));
     A3G_CUDA(cudaMemsetAsync(t.d_stats, 0, static_cast<size_t>(K) * A3G_STEP_STATS * 8, t.s_comp));
     A3G_CUDA(cudaEventRecord(t.ev_t0, t.s_comp));
     A3G_CUDA(cudaStreamWaitEvent(t.s_samp, t.ev_t0, 0));
@@ -915,7 +975,7 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
         A3G_CUDA(cudaEventRecord(se[0], ss));
       }
       sample_impl(smp->st, dseeds + off[i], static_cast<uint32_t>(off[i + 1] - off[i]), true, gamma, kind,
-                  rng_seeds[i], ss);
+                  rng_seeds[i], ss, /*prevalidated=*/!on_device);
       launch_step_stats(t, smp, t.d_stats + static_cast<size_t>(i) * A3G_STEP_STATS, ss);
       A3G_CUDA(cudaEventRecord(t.ev_sampled[ar], ss));
       A3G_CUDA(cudaStreamWaitEvent(t.s_comp, t.ev_sampled[ar], 0));
@@ -971,8 +1031,10 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
     }
     t.last_agg_launches = t.ev_agg.size() / 2;
     t.last_agg_ms = t.last_agg_launches ? agg / t.last_agg_launches : 0;
-    unsigned long long bytes = 0;
-    A3G_CUDA(cudaMemcpy(&bytes, t.d_agg_bytes, 8, cudaMemcpyDeviceToHost));
+    unsigned long long words[2] = {0, 0};
+    A3G_CUDA(cudaMemcpy(words, t.d_agg_bytes, 16, cudaMemcpyDeviceToHost));
+    if (words[1]) raise(A3G_ERR_PARAMETER, "sample_khop: seed out of range");
+    const unsigned long long bytes = words[0];
     t.last_agg_bytes = t.last_agg_launches ? static_cast<double>(bytes) / t.last_agg_launches : 0;
   });
 }

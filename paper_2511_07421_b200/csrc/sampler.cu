@@ -1636,6 +1636,18 @@ __global__ void k_init_counters(BatchCounters* c, uint32_t n_seeds) {
   if (threadIdx.x == 0) c->n_seeds = n_seeds;
 }
 
+// Device-resident seeds are not visible to the host validation
+// (sampler.cpp:92-94 "seed out of range"): flag them in the batch counters
+// (raised as ParameterError once the host syncs) and clamp them to node 0 so
+// no kernel of this batch reads the CSR out of bounds.
+__global__ void k_check_seeds(uint32_t* seeds, uint32_t n_seeds, uint64_t num_nodes, BatchCounters* c) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n_seeds && seeds[i] >= num_nodes) {
+    seeds[i] = 0;
+    atomicOr(&c->bad_seeds, 1u);
+  }
+}
+
 // ------------------------------------------------------------ finalize -----
 constexpr int kFinThreads = 256;
 constexpr int kFinRounds = 8;
@@ -1893,12 +1905,8 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
   k_classify<WM><<<sm_count * 2, 256, 0, st>>>(sa);
   A3G_LAUNCH_DONE("k_classify", st);
   if (sa.f <= 32) {
-    static bool attr_set = false;
-    if (!attr_set) {
-      A3G_CUDA(cudaFuncSetAttribute(k_hub_merge<WM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(kMergeSmem)));
-      attr_set = true;
-    }
+    static std::atomic<uint64_t> attr_done{0};
+    smem_attr_once(attr_done, reinterpret_cast<const void*>(k_hub_merge<WM>), kMergeSmem);
     {
       // lane groups over the length-sorted items: integer keys (or Algorithm
       // R) in k_stream_grp, bitmap weights (fp64 keys) in k_stream_grp_mixed
@@ -1994,6 +2002,10 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
   BatchCounters* ctr = s.d_ctr;
   k_init_counters<<<1, 64, 0, st>>>(ctr, n_seeds);
   A3G_LAUNCH_DONE("k_init_counters", st);
+  if (s.check_seeds) {
+    k_check_seeds<<<(n_seeds + 255) / 256, 256, 0, st>>>(s.d_seeds, n_seeds, g->n, ctr);
+    A3G_LAUNCH_DONE("k_check_seeds", st);
+  }
   if (s.cap_inner) A3G_CUDA(cudaMemsetAsync(s.d_inv1, 0xff, s.cap_inner * sizeof(int32_t), st));
   ++s.gtag;
   // ---- seeds phase (sampler.cpp:100-105)
@@ -2108,6 +2120,45 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
     k_resolve<<<dim3(s.sm_count * 2, s.L), 256, 0, st>>>(ra);
     A3G_LAUNCH_DONE("k_resolve", st);
   }
+}
+
+// cache.cpp:48-68 lookup over an id list: the device of every id (-1 =
+// miss; any-device presence is a hit), and the accounting counts
+// cnt = [hits, misses, per-device hits...]. With one device the cached
+// bitmap decides (device 0); with several, the device map.
+__global__ void k_cache_lookup(const uint32_t* ids, uint64_t n, const uint32_t* bits, const int32_t* dmap,
+                               int32_t* dev_out, unsigned long long* cnt, uint32_t num_devices) {
+  __shared__ unsigned long long s_cnt[2 + kMaxCacheDevices];
+  for (uint32_t i = threadIdx.x; i < 2 + num_devices; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t v = ids[i];
+    int32_t d;
+    if (dmap)
+      d = __ldg(dmap + v);
+    else
+      d = ((__ldg(bits + (v >> 5)) >> (v & 31)) & 1u) ? 0 : -1;
+    if (dev_out) dev_out[i] = d;
+    if (d < 0) {
+      atomicAdd(&s_cnt[1], 1ull);
+    } else {
+      atomicAdd(&s_cnt[0], 1ull);
+      if (static_cast<uint32_t>(d) < num_devices) atomicAdd(&s_cnt[2 + d], 1ull);
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < 2 + num_devices; i += blockDim.x)
+    if (s_cnt[i]) atomicAdd(cnt + i, s_cnt[i]);
+}
+
+void launch_cache_lookup(const a3g_cache* c, const uint32_t* d_ids, uint64_t n, int32_t* d_dev,
+                         unsigned long long* d_cnt, int sm_count, cudaStream_t st) {
+  const uint32_t nd = c->num_devices < kMaxCacheDevices ? c->num_devices : kMaxCacheDevices;
+  const int grid = static_cast<int>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(sm_count) * 4));
+  k_cache_lookup<<<grid > 0 ? grid : 1, 256, 0, st>>>(d_ids, n, c->d_bits, c->num_devices > 1 ? c->d_map : nullptr,
+                                                       d_dev, d_cnt, nd);
+  A3G_LAUNCH_DONE("k_cache_lookup", st);
 }
 
 void launch_gather_unique(SamplerState& s, float* out, cudaStream_t st) {

@@ -70,6 +70,7 @@ struct SamplerState {
   bool own_stream = false;
   // last batch parameters
   uint32_t last_n_seeds = 0;
+  bool check_seeds = false;  // seeds came from device memory: range-check them on the device
   bool has_batch = false;
   int sm_count = 148;
   int device = 0;  // the graph's device (kept so destroy never dereferences the graph)
@@ -87,6 +88,10 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
 void launch_reservoir_list(const uint32_t* d_nb, const double* d_w, uint64_t deg, uint32_t m,
                            uint64_t key, uint64_t c0, int kind, uint32_t* d_out, double* d_keys,
                            cudaStream_t st);
+// cache.cpp:48-68 lookup of n device ids: per-id device (d_dev, may be null)
+// and d_cnt[0..2+num_devices) += [hits, misses, per-device hits].
+void launch_cache_lookup(const a3g_cache* c, const uint32_t* d_ids, uint64_t n, int32_t* d_dev,
+                         unsigned long long* d_cnt, int sm_count, cudaStream_t st);
 // Gather unique rows to `out` (device f32, F contiguous) and count hits/misses.
 void launch_gather_unique(SamplerState& s, float* out, cudaStream_t st);
 // per-edge cached bits of a partial cache: ebits[e / 32] bit e % 32 = bits[col[e]]

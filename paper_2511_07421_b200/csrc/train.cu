@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(128) k_dw1_fma(const float* __restrict__ agg, 
 // counters and the cache hit/miss count over unique_nodes (lookup,
 // cache.cpp:48-68: any-device presence is a hit).
 __global__ void k_step_stats(const BatchCounters* ctr, const uint32_t* unique, const uint32_t* bits, int bitmode,
-                             uint32_t L, unsigned long long* out) {
+                             uint32_t L, unsigned long long* out, unsigned long long* err) {
   const uint32_t U = ctr->ucount[L];
   const int lane = threadIdx.x & 31;
   uint32_t hits = 0;
@@ -404,6 +404,8 @@ __global__ void k_step_stats(const BatchCounters* ctr, const uint32_t* unique, c
     out[A3G_STAT_EDGES] = E;
     out[A3G_STAT_INNER] = L >= 1 ? ctr->ucount[1] : ctr->ucount[0];
     out[A3G_STAT_SEEDS] = ctr->ucount[0];
+    out[A3G_STAT_BAD_SEEDS] = ctr->bad_seeds;
+    if (ctr->bad_seeds && err) atomicOr(err, 1ull);
     // misses = U - hits, derived on the host (a3g_trainer_step_stats)
   }
 }
@@ -487,12 +489,15 @@ __global__ void __launch_bounds__(256) k_outer(OuterArgs a) {
   }
 }
 
-// Fixed-point scale of the dh1 scatter: every row sums at most ns + 1
-// contributions bounded by amax, so sums stay below 2^62.
-__device__ __forceinline__ double fx_scale(uint32_t amax_bits, uint32_t ns) {
+// Fixed-point scale of the dh1 scatter: the step has at most ns * max(f0, 1)
+// contributions in total (one per layer-0 slot, or one self-fallback per
+// seed) -- a row can receive all of them when duplicate CSR edges
+// (from_edges / A3G1 accept them) make one source fill every slot -- each
+// bounded by amax, so no row sum reaches 2^62.
+__device__ __forceinline__ double fx_scale(uint32_t amax_bits, uint32_t ns, uint32_t f0) {
   const float amax = __uint_as_float(amax_bits);
   if (!(amax > 0.f)) return 1.0;
-  const int e = ilogb(static_cast<double>(amax) * (ns + 1.0)) + 1;
+  const int e = ilogb(static_cast<double>(amax) * (static_cast<double>(ns) * (f0 > 1 ? f0 : 1) + 1.0)) + 1;
   return ldexp(1.0, 62 - e);
 }
 
@@ -505,7 +510,7 @@ __global__ void __launch_bounds__(256) k_dh1_scatter(const float* dagg, const ui
                                                      const uint32_t* cnt0, const uint32_t* sidx0, uint32_t f0,
                                                      int has_layer0, uint32_t H, unsigned long long* fx) {
   const uint32_t ns = *ns_p;
-  const double scale = fx_scale(*amax, ns);
+  const double scale = fx_scale(*amax, ns, has_layer0 ? f0 : 1u);
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < static_cast<uint64_t>(ns) * H;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t s = static_cast<uint32_t>(i / H), h = static_cast<uint32_t>(i - static_cast<uint64_t>(s) * H);
@@ -521,9 +526,9 @@ __global__ void __launch_bounds__(256) k_dh1_scatter(const float* dagg, const ui
 }
 
 // dh1 = fixed point / scale (rows < n_inner); clears the accumulator for the next step.
-__global__ void k_dh1_fix(unsigned long long* fx, const uint32_t* amax, const uint32_t* ns_p, const uint32_t* n_inner,
-                          uint32_t H, float* dh1) {
-  const double inv = 1.0 / fx_scale(*amax, *ns_p);
+__global__ void k_dh1_fix(unsigned long long* fx, const uint32_t* amax, const uint32_t* ns_p, uint32_t f0,
+                          const uint32_t* n_inner, uint32_t H, float* dh1) {
+  const double inv = 1.0 / fx_scale(*amax, *ns_p, f0);
   const uint64_t total = static_cast<uint64_t>(*n_inner) * H;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -722,7 +727,8 @@ void launch_step_stats(TrainerState& t, a3g_sampler* smp, unsigned long long* d_
   SamplerState& s = smp->st;
   const a3g_cache* c = t.c;
   const int bitmode = c->all_cached ? 1 : (c->none_cached ? 0 : 2);
-  k_step_stats<<<t.sm_count, 256, 0, st>>>(s.d_ctr, s.d_unique, c->d_bits, bitmode, s.L, d_stats);
+  k_step_stats<<<t.sm_count, 256, 0, st>>>(s.d_ctr, s.d_unique, c->d_bits, bitmode, s.L, d_stats,
+                                           t.d_agg_bytes + 1);
   A3G_LAUNCH_DONE("k_step_stats", st);
 }
 
@@ -794,7 +800,8 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
   k_dh1_scatter<<<t.sm_count * 2, 256, 0, st>>>(t.d_dagg, t.d_amax, oa.ns, oa.cnt0, oa.sidx0, oa.f0, oa.has_layer0,
                                                 t.H, t.d_dh1_fx);
   A3G_LAUNCH_DONE("k_dh1_scatter", st);
-  k_dh1_fix<<<t.sm_count * 2, 256, 0, st>>>(t.d_dh1_fx, t.d_amax, oa.ns, aa.n_inner, t.H, t.d_dh1);
+  k_dh1_fix<<<t.sm_count * 2, 256, 0, st>>>(t.d_dh1_fx, t.d_amax, oa.ns, oa.has_layer0 ? oa.f0 : 1u, aa.n_inner,
+                                            t.H, t.d_dh1);
   A3G_LAUNCH_DONE("k_dh1_fix", st);
   // ---- dW1 = agg_inner^T . (dh1 * [h1 > 0]), partials per row split
   uint32_t nparts;
@@ -805,21 +812,13 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
     nparts = t.dw1_splits;
     const dim3 grid((t.F + 127) / 128, nparts);
     if (t.H <= 16) {
-      static bool attr16 = false;
-      if (!attr16) {
-        A3G_CUDA(cudaFuncSetAttribute(k_dw1_fma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(dw1_smem(16))));
-        attr16 = true;
-      }
+      static std::atomic<uint64_t> attr16{0};
+      smem_attr_once(attr16, reinterpret_cast<const void*>(k_dw1_fma<16>), dw1_smem(16));
       k_dw1_fma<16><<<grid, 128, dw1_smem(16), st>>>(t.d_agg_inner, t.pitch, t.F, t.H, aa.n_inner, t.d_h1, t.d_dh1,
                                                       t.d_part);
     } else {
-      static bool attr32 = false;
-      if (!attr32) {
-        A3G_CUDA(cudaFuncSetAttribute(k_dw1_fma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(dw1_smem(32))));
-        attr32 = true;
-      }
+      static std::atomic<uint64_t> attr32{0};
+      smem_attr_once(attr32, reinterpret_cast<const void*>(k_dw1_fma<32>), dw1_smem(32));
       k_dw1_fma<32><<<grid, 128, dw1_smem(32), st>>>(t.d_agg_inner, t.pitch, t.F, t.H, aa.n_inner, t.d_h1, t.d_dh1,
                                                       t.d_part);
     }

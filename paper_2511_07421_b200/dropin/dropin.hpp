@@ -34,6 +34,10 @@ int device();
 a3g_graph* device_graph(const graph::Graph& g);
 // Device cache state (cached bitmap) of c over g.
 a3g_cache* device_cache(const graph::Graph& g, const cache::CacheState& c);
+// The device cache of c when only the CacheState is known (lookup(),
+// cache.hpp:75): a registered cache with the same content, else one over a
+// topology-only graph of device_map.size() nodes.
+a3g_cache* device_cache_of(const cache::CacheState& c);
 // This thread's sampler arena for (g, c) with capacity >= n_seeds and the
 // given fanouts (the reference's producers call sample_khop concurrently,
 // pipeline_exec.cpp:235-256: one arena per thread).

@@ -53,6 +53,37 @@ int main(int argc, char** argv) {
                 (unsigned long long)fnv(feats.data(), feats.size() * 4), (unsigned long long)st.batch_bytes);
   }
   std::printf("hit_rate %.17g\n", cache::hit_rate(acc));
+  // lookup over a 2-device placement: per-id devices and per-device hits
+  {
+    cache::CacheConfig c2;
+    c2.volume_bytes = (n / 10) * g.feat_dim * 4;
+    c2.num_devices = 2;
+    const cache::CacheState two = cache::build_static_cache(g, c2);
+    cache::CacheAccounting acc2(2);
+    std::vector<NodeId> ids;
+    for (NodeId v = 0; v < n; v += 7) ids.push_back(v);
+    const auto dev = cache::lookup(two, ids, acc2);
+    std::printf("lookup2 %016llx hits=%llu misses=%llu d0=%llu d1=%llu lists=%zu,%zu bytes=%llu\n",
+                (unsigned long long)fnv(dev.data(), dev.size() * 4), (unsigned long long)acc2.hits.load(),
+                (unsigned long long)acc2.misses.load(), (unsigned long long)acc2.per_device_hits[0].load(),
+                (unsigned long long)acc2.per_device_hits[1].load(), two.cached_per_device[0].size(),
+                two.cached_per_device[1].size(), (unsigned long long)two.bytes_used[1]);
+  }
+  // a fresh CacheState per design point in the same stack slot (surrogate.cpp:272):
+  // every sample must see its own cached set
+  for (int k = 1; k <= 3; ++k) {
+    cache::CacheConfig ck;
+    ck.volume_bytes = (n * k / 8) * g.feat_dim * 4;
+    const cache::CacheState cs = cache::build_static_cache(g, ck);
+    sampling::SamplerConfig cfg;
+    cfg.fanouts = {10, 5};
+    cfg.bias_rate = 8.0;
+    cfg.rng_seed = 11;
+    const auto b = sampling::sample_khop(g, batches[0], cfg, cs);
+    std::uint64_t h = fnv(b.unique_nodes.data(), b.unique_nodes.size() * 4);
+    for (const auto& l : b.layers) h = fnv(l.edges.data(), l.edges.size() * 8, h);
+    std::printf("design %d unique=%zu hash=%016llx\n", k, b.unique_nodes.size(), (unsigned long long)h);
+  }
   // reservoir on one list, with the caller's stream advanced like the reference
   {
     std::vector<NodeId> nb(300);

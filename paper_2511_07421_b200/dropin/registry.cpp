@@ -1,5 +1,6 @@
 // registry.cpp -- device copies of reference objects for the C++ drop-in.
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -11,20 +12,47 @@
 namespace a3gnn::b200 {
 namespace {
 
-struct GraphKey {
-  const void* obj;
-  const void* col;
-  const void* feat;
-  std::uint64_t n, m;
-  bool operator<(const GraphKey& o) const {
-    return std::tie(obj, col, feat, n, m) < std::tie(o.obj, o.col, o.feat, o.n, o.m);
+// Content fingerprint of an array: every element when it is small, else
+// 65536 evenly strided elements plus the last one. The reference rebuilds
+// Graph / CacheState objects at recycled addresses (surrogate.cpp:272 builds
+// a fresh CacheState per design point in the same stack slot, test fixtures
+// build equal-size graphs), so the registry keys entries by content, never by
+// address alone.
+template <typename T>
+std::uint64_t fingerprint(const T* p, std::size_t n, std::uint64_t h) {
+  auto mix = [](std::uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xbf58476d1ce4e5b9ull;
+    z ^= z >> 27;
+    z *= 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+  };
+  h = mix(h ^ n);
+  if (!p || n == 0) return h;
+  constexpr std::size_t kFull = std::size_t{1} << 18;
+  const std::size_t step = n <= kFull ? 1 : n / 65536;
+  for (std::size_t i = 0; i < n; i += step) {
+    std::uint64_t v = 0;
+    std::memcpy(&v, p + i, sizeof(T) < 8 ? sizeof(T) : 8);
+    h = mix(h + v + i * 0x9e3779b97f4a7c15ull);
   }
+  std::uint64_t last = 0;
+  std::memcpy(&last, p + n - 1, sizeof(T) < 8 ? sizeof(T) : 8);
+  return mix(h ^ last);
+}
+
+struct GraphKey {
+  std::uint64_t n, m;
+  std::uint32_t f;
+  std::uint64_t fp;  // row_offsets, col, features, labels
+  bool operator<(const GraphKey& o) const { return std::tie(n, m, f, fp) < std::tie(o.n, o.m, o.f, o.fp); }
 };
 
 struct Registry {
   std::mutex mu;
   std::map<GraphKey, a3g_graph*> graphs;
-  std::map<std::tuple<a3g_graph*, const void*, const void*, std::size_t>, a3g_cache*> caches;
+  // (device graph, fingerprint of device_map + per-device counts)
+  std::map<std::pair<a3g_graph*, std::uint64_t>, a3g_cache*> caches;
   std::uint64_t generation = 0;  // bumped by release(): invalidates thread arenas
   ~Registry() {
     for (auto& [k, c] : caches) a3g_cache_destroy(c);
@@ -37,7 +65,17 @@ Registry& reg() {
 }
 
 GraphKey key_of(const graph::Graph& g) {
-  return GraphKey{&g, g.col_indices.data(), g.features.data(), g.num_nodes, g.num_edges};
+  std::uint64_t h = fingerprint(g.row_offsets.data(), g.row_offsets.size(), 0x6a);
+  h = fingerprint(g.col_indices.data(), g.col_indices.size(), h);
+  h = fingerprint(g.features.data(), g.features.size(), h);
+  h = fingerprint(g.labels.data(), g.labels.size(), h);
+  return GraphKey{g.num_nodes, g.num_edges, g.feat_dim, h};
+}
+
+std::uint64_t cache_key(const cache::CacheState& c) {
+  std::uint64_t h = fingerprint(c.device_map.data(), c.device_map.size(), 0xca);
+  for (const auto& l : c.cached_per_device) h = fingerprint(l.data(), l.size(), h);
+  return h;
 }
 
 struct Arena {
@@ -94,8 +132,7 @@ a3g_cache* device_cache(const graph::Graph& g, const cache::CacheState& c) {
   a3g_graph* dg = device_graph(g);
   Registry& r = reg();
   std::lock_guard<std::mutex> lk(r.mu);
-  const auto k = std::make_tuple(dg, static_cast<const void*>(&c), static_cast<const void*>(c.device_map.data()),
-                                 c.device_map.size());
+  const auto k = std::make_pair(dg, cache_key(c));
   auto it = r.caches.find(k);
   if (it != r.caches.end()) return it->second;
   if (c.device_map.size() != g.num_nodes && !c.device_map.empty())
@@ -104,6 +141,35 @@ a3g_cache* device_cache(const graph::Graph& g, const cache::CacheState& c) {
   const std::uint32_t nd = static_cast<std::uint32_t>(std::max<std::size_t>(1, c.cached_per_device.size()));
   check(a3g_cache_from_map(dg, c.device_map.empty() ? nullptr : c.device_map.data(), nd, &h));
   r.caches.emplace(k, h);
+  return h;
+}
+
+a3g_cache* device_cache_of(const cache::CacheState& c) {
+  const std::uint64_t key = cache_key(c);
+  const std::uint64_t n = c.device_map.size();
+  Registry& r = reg();
+  std::lock_guard<std::mutex> lk(r.mu);
+  for (const auto& [gk0, dg0] : r.graphs) {
+    if (gk0.n != n) continue;
+    auto it = r.caches.find(std::make_pair(dg0, key));
+    if (it != r.caches.end()) return it->second;
+  }
+  // lookup() before any call that names the graph: the cache over a
+  // topology-only placeholder graph of the same node count (no edges, no rows)
+  const GraphKey gk{n, 0, 1, 0x100c0u};
+  a3g_graph* dg = nullptr;
+  auto git = r.graphs.find(gk);
+  if (git != r.graphs.end()) {
+    dg = git->second;
+  } else {
+    const std::vector<std::uint64_t> ro(n + 1, 0);
+    check(a3g_graph_create(device(), n, 0, 1, ro.data(), nullptr, nullptr, A3G_FEAT_F32, nullptr, &dg));
+    r.graphs.emplace(gk, dg);
+  }
+  a3g_cache* h = nullptr;
+  const std::uint32_t nd = static_cast<std::uint32_t>(std::max<std::size_t>(1, c.cached_per_device.size()));
+  check(a3g_cache_from_map(dg, c.device_map.empty() ? nullptr : c.device_map.data(), nd, &h));
+  r.caches.emplace(std::make_pair(dg, key), h);
   return h;
 }
 
@@ -134,7 +200,7 @@ void release(const graph::Graph& g) {
   auto it = r.graphs.find(key_of(g));
   if (it == r.graphs.end()) return;
   for (auto c = r.caches.begin(); c != r.caches.end();) {
-    if (std::get<0>(c->first) == it->second) {
+    if (c->first.first == it->second) {
       a3g_cache_destroy(c->second);
       c = r.caches.erase(c);
     } else {

@@ -96,6 +96,8 @@ _SIGS = {
     "a3g_cache_build": (C.c_int, [vp, C.c_uint64, C.c_uint32, i32p, C.POINTER(vp)]),
     "a3g_cache_from_map": (C.c_int, [vp, i32p, C.c_uint32, C.POINTER(vp)]),
     "a3g_cache_total_cached": (C.c_uint64, [vp]),
+    "a3g_cache_hot_order": (C.c_int, [vp, u32p]),
+    "a3g_cache_lookup": (C.c_int, [vp, u32p, C.c_uint64, i32p, u64p, u64p, u64p]),
     "a3g_cache_destroy": (None, [vp]),
     "a3g_sampler_create": (C.c_int, [vp, vp, C.c_uint32, u32p, C.c_uint32, C.POINTER(vp)]),
     "a3g_sampler_destroy": (None, [vp]),

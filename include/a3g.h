@@ -111,6 +111,9 @@ void a3g_graph_destroy(a3g_graph* g);
  * synthesized on the device at feat_dim, stored as feat_dtype. The topology,
  * labels and masks come from a3g_host_graph_power_law at feat_dim 1. */
 a3g_status a3g_graph_synthesize_features(a3g_graph* g, uint32_t feat_dim, int feat_dtype, uint64_t seed);
+/* Elements of the last synthesis that sat within 2^-44 relative of a float
+ * rounding boundary and were recomputed with the host's glibc (synth.cu). */
+uint64_t a3g_graph_synth_patched(const a3g_graph* g);
 
 /* --------------------------------------------------------------- store --- */
 /* Places the feature rows of `g` by `policy` (A3G_STORE_*) from host f32

@@ -114,10 +114,19 @@ class Oracle:
                                                            u64p, C.POINTER(u32p), C.POINTER(u32p), f32p, u32p,
                                                            f64p, f64p, f64p]
         L.orc_sgd_step.argtypes = [f64p, f64p, C.c_uint64, C.c_double]
+        L.orc_feature_rows.argtypes = [C.c_uint64, C.c_uint32, u32p, C.c_uint64, u32p, f32p]
         L.orc_train_steps.restype = C.c_int64
         L.orc_train_steps.argtypes = [C.c_uint64, u64p, u32p, f32p, C.c_uint32, u32p, u8p, i32p, u32p,
                                       C.c_uint32, C.c_double, C.c_int, C.c_uint64, C.c_uint32, C.c_uint32,
                                       C.c_uint32, C.c_double, f64p, f64p, C.c_uint64, f64p, u64p, u64p]
+
+    def feature_rows(self, seed, F, ids, labels) -> np.ndarray:
+        """generators.cpp:12-24 rows of the power-law generator (seed, F) for `ids`."""
+        ids = np.ascontiguousarray(ids, dtype=np.uint32)
+        labels = np.ascontiguousarray(labels, dtype=np.uint32)
+        out = np.empty((len(ids), F), np.float32)
+        self.L.orc_feature_rows(seed, F, _p(ids, u32p), len(ids), _p(labels, u32p), _p(out, f32p))
+        return out
 
     # -- rng ---------------------------------------------------------------
     def mix64(self, z): return self.L.orc_mix64(z)

@@ -67,6 +67,30 @@ double orc_next_unit_at(uint64_t key, uint64_t i) {
   return (double)(mix64(key + i * PHI) >> 11) * 0x1.0p-53;
 }
 
+/* generators.cpp:12-24 + rng.hpp:60-65: the power-law generator's feature
+ * rows for an explicit node list (papers-scale parity of the gathered rows
+ * without the 56 GB f32 table). The generator's rng is RngStream(seed,
+ * 0x97a3) (generators.cpp:87) and the noise its substream 0xfea7 (rng.hpp:38-
+ * 41: key hash2(key, id ^ 0xd6e8feb86659fd93)); element (v, d) is the
+ * Box-Muller Gaussian of draws 2(v F + d) + 1, + 2 (two draws per sample, no
+ * caching), cast to float, + 1.0f at d == label % F. */
+void orc_feature_rows(uint64_t seed, uint32_t F, const uint32_t* ids, uint64_t n, const uint32_t* labels,
+                      float* out) {
+  const uint64_t noise_key = hash2(hash2(seed, 0x97a3), 0xfea7ull ^ 0xd6e8feb86659fd93ull);
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t v = ids[i];
+    float* row = out + i * F;
+    for (uint32_t d = 0; d < F; ++d) {
+      const uint64_t c = 2 * (v * F + d);
+      double u1 = (double)(mix64(noise_key + (c + 1) * PHI) >> 11) * 0x1.0p-53;
+      const double u2 = (double)(mix64(noise_key + (c + 2) * PHI) >> 11) * 0x1.0p-53;
+      if (u1 <= 0.0) u1 = 0x1.0p-53;
+      row[d] = (float)(sqrt(-2.0 * log(u1)) * cos(6.283185307179586476925 * u2));
+    }
+    row[labels[v] % F] += 1.0f;
+  }
+}
+
 /* trainer.cpp:345-348 */
 uint64_t orc_sampling_seed(uint64_t base, uint32_t epoch, uint32_t step, uint32_t worker) {
   return hash3(base, hash2(epoch, step), worker);

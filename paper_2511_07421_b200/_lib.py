@@ -86,6 +86,7 @@ _SIGS = {
                                    C.POINTER(vp)]),
     "a3g_graph_destroy": (None, [vp]),
     "a3g_graph_synthesize_features": (C.c_int, [vp, C.c_uint32, C.c_int, C.c_uint64]),
+    "a3g_graph_synth_patched": (C.c_uint64, [vp]),
     "a3g_store_create": (C.c_int, [vp, f32p, i32p, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
     "a3g_store_info": (C.c_int, [vp, u64p, u64p, u64p]),
     "a3g_store_local_ptr": (C.c_int, [vp, C.POINTER(vp)]),

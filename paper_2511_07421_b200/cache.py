@@ -43,6 +43,7 @@ class CacheState:
     num_devices: int = 1
     volume_bytes: int = 0
     _dev: dict = field(default_factory=dict, repr=False)
+    _graph: object = field(default=None, repr=False)  # the graph it was last placed on (lookup)
 
     def is_cached(self, v: int) -> bool:
         return 0 <= v < len(self.device_map) and self.device_map[v] != KCACHE_MISS
@@ -58,6 +59,7 @@ class CacheState:
         return int((self.device_map != KCACHE_MISS).sum())
 
     def device(self, g: Graph, device: int = 0, feat_dtype: int = 0):
+        self._graph = g
         key = (id(g), device, feat_dtype)
         if key not in self._dev:
             dg = g.device(device, feat_dtype)
@@ -103,19 +105,27 @@ def build_static_cache(g: Graph, cfg: CacheConfig, device: int = 0) -> CacheStat
     check(lib().a3g_cache_build(dg.h, cfg.volume_bytes, cfg.num_devices, ptr(dm, i32p), C.byref(h)))
     st = CacheState(dm, cfg.num_devices, cfg.volume_bytes)
     st._dev[(id(g), device, 0)] = _DeviceCache(h)
+    st._graph = g
     return st
 
 
-def lookup(c: CacheState, ids, acc: CacheAccounting) -> np.ndarray:
-    """cache.cpp:48-68."""
-    ids = np.asarray(ids, dtype=np.int64)
-    d = np.where((ids >= 0) & (ids < len(c.device_map)), c.device_map[np.clip(ids, 0, len(c.device_map) - 1)],
-                 KCACHE_MISS).astype(np.int32)
-    hits = int((d != KCACHE_MISS).sum())
-    acc.add(hits, len(ids) - hits)
+def lookup(c: CacheState, ids, acc: CacheAccounting, g: Graph | None = None, device: int = 0) -> np.ndarray:
+    """cache.cpp:48-68 on the device (a3g_cache_lookup): per-id device
+    (-1 = miss) and the hit / miss / per-device accounting. `g` names the graph
+    the cache was built over (default: the one it was last placed on)."""
+    ids = np.ascontiguousarray(ids, dtype=np.uint32)
+    g = g if g is not None else c._graph
+    if g is None:
+        raise ParameterError("lookup: the cache has no graph (pass g)")
+    out = np.empty(max(len(ids), 1), dtype=np.int32)
+    h, m = C.c_uint64(), C.c_uint64()
+    pd = np.zeros(max(c.num_devices, 1), dtype=np.uint64)
+    check(lib().a3g_cache_lookup(c.device(g, device), ptr(ids, u32p), len(ids), ptr(out, i32p), C.byref(h),
+                                 C.byref(m), ptr(pd, u64p)))
+    acc.add(h.value, m.value)
     for dev in range(min(len(acc.per_device_hits), c.num_devices)):
-        acc.per_device_hits[dev] += int((d == dev).sum())
-    return d
+        acc.per_device_hits[dev] += int(pd[dev])
+    return out[:len(ids)]
 
 
 def retrieve_features(b, c: CacheState, g: Graph, acc: CacheAccounting, device: int = 0):
@@ -130,9 +140,13 @@ def retrieve_features(b, c: CacheState, g: Graph, acc: CacheAccounting, device: 
     check(lib().a3g_gather_rows(dg.h, ch, ptr(uniq, u32p), len(uniq), ptr(out, f32p), C.byref(hits),
                                 C.byref(misses)))
     acc.add(hits.value, misses.value)
-    dm = c.device_map[uniq] if len(uniq) else np.zeros(0, np.int32)
-    for dev in range(min(len(acc.per_device_hits), c.num_devices)):
-        acc.per_device_hits[dev] += int((dm == dev).sum())
+    if c.num_devices > 1 and len(uniq):  # per-device hits from the device lookup
+        pd = np.zeros(c.num_devices, dtype=np.uint64)
+        check(lib().a3g_cache_lookup(ch, ptr(uniq, u32p), len(uniq), None, None, None, ptr(pd, u64p)))
+        for dev in range(min(len(acc.per_device_hits), c.num_devices)):
+            acc.per_device_hits[dev] += int(pd[dev])
+    elif acc.per_device_hits:
+        acc.per_device_hits[0] += hits.value
     ne = b.total_edges()
     st = BatchStats(len(uniq) * g.feat_dim * 4 + ne * 2 * 4, len(uniq), ne)
     return out, st

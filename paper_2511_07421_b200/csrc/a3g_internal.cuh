@@ -166,6 +166,7 @@ struct a3g_graph {
   std::vector<uint64_t> h_ro;       // host copy (validation, degrees)
   std::vector<uint32_t> h_labels;   // host copy
   bool has_features = false;
+  uint64_t synth_patched = 0;       // a3g_graph_synthesize_features: elements recomputed on the host
   a3g::StoreView view{};            // how kernels reach feature rows (default: d_feat, identity)
   a3g_store* store = nullptr;       // attached tiered store (a3g_store_create), else null
 };

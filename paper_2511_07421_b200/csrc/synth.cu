@@ -1,14 +1,24 @@
-// synth.cu -- device synthesis of the power-law generator's features for
-// papers-scale graphs (BASELINE config 5: 111M nodes x 128-d bf16 = 28 GB,
-// whose f32 host table would not fit the host). The formula is the
-// reference's fill_features_and_masks (proj/src/generators.cpp:12-24): element
-// (v, d) is the Box-Muller Gaussian of draws 2(v*F+d)+1, +2 of the noise
-// substream, plus 1.0f at d == label % F. The topology, labels and masks come
-// from the host generator at feat_dim 1 (they never depend on F).
-// fp64 log/sqrt/cos of the device library can differ from glibc by an ulp,
-// which changes the f32 (then bf16) value of ~1e-9 of the elements; parity at
-// this scale is sampling-only.
+// synth.cu -- papers-scale feature table (BASELINE config 5: 111M nodes x
+// 128-d bf16 = 28 GB, whose f32 host table would not fit the host), bit-exact
+// to the reference's fill_features_and_masks (proj/src/generators.cpp:12-24):
+// element (v, d) is the Box-Muller Gaussian (rng.hpp:60-65) of draws
+// 2(v*F+d)+1, +2 of the noise substream, plus 1.0f at d == label % F. The
+// topology, labels and masks come from the host generator at feat_dim 1 (they
+// never depend on F).
+//
+// Bit-exactness: the device evaluates sqrt(-2 log u1) cos(2 pi u2) in fp64
+// with the CUDA math library (log <= 1 ulp, cos <= 2 ulp, sqrt exact), glibc
+// on the host with its own (<= 1 ulp) routines, so the two fp64 values differ
+// by less than 2^-49 relative. The stored value is float(x) (then +1.0f and
+// the bf16 rounding, both exact functions of float(x)), so it can differ only
+// if a float rounding boundary lies within that distance of x. The kernel
+// tests each element against a 2^-44 relative window (32x margin): if
+// float(x (1 - 2^-44)) != float(x (1 + 2^-44)) the element is listed, and the
+// host recomputes the listed elements with glibc exactly as generators.cpp
+// does and patches them (~2e-6 of the elements: ~27K of C5's 14.2G).
+#include <cmath>
 #include <cstring>
+#include <vector>
 
 #include "a3g_internal.cuh"
 
@@ -27,9 +37,11 @@ __device__ __forceinline__ uint16_t enc<uint16_t>(float x) {
   return static_cast<uint16_t>((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);  // RNE, as a3g_graph_create
 }
 
+constexpr double kSynthWindow = 0x1.0p-44;
+
 template <typename T>
 __global__ void k_synth_features(uint64_t noise_key, uint64_t n, uint32_t F, uint32_t pitch, const uint32_t* labels,
-                                  T* out) {
+                                  T* out, unsigned long long* n_listed, uint64_t* listed, uint64_t cap) {
   const uint64_t total = n * pitch;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -41,11 +53,42 @@ __global__ void k_synth_features(uint64_t noise_key, uint64_t n, uint32_t F, uin
       double u1 = unit_of(draw(noise_key, c + 1));
       const double u2 = unit_of(draw(noise_key, c + 2));
       if (u1 <= 0.0) u1 = 0x1.0p-53;
-      x = static_cast<float>(sqrt(-2.0 * log(u1)) * cos(6.283185307179586476925 * u2));
+      const double xd = sqrt(-2.0 * log(u1)) * cos(6.283185307179586476925 * u2);
+      x = static_cast<float>(xd);
+      const double w = fabs(xd) * kSynthWindow;
+      if (__double2float_rn(xd - w) != __double2float_rn(xd + w)) {  // near a float rounding boundary
+        const unsigned long long k = atomicAdd(n_listed, 1ull);
+        if (k < cap) listed[k] = i;
+      }
       if (d == labels[v] % F) x += 1.0f;
     }
     out[i] = enc<T>(x);
   }
+}
+
+template <typename T>
+__global__ void k_patch(const uint64_t* idx, const T* val, uint64_t n, T* out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[idx[i]] = val[i];
+}
+
+// The reference's value of element (v, d) on the host (glibc log / sqrt /
+// cos, fp-contract off: the expression of rng.hpp:60-65 / generators.cpp:20).
+float host_element(uint64_t noise_key, uint64_t v, uint32_t d, uint32_t F, uint32_t label) {
+  const uint64_t c = 2 * (v * F + d);
+  double u1 = unit_of(draw(noise_key, c + 1));
+  const double u2 = unit_of(draw(noise_key, c + 2));
+  if (u1 <= 0.0) u1 = 0x1.0p-53;
+  float x = static_cast<float>(std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586476925 * u2));
+  if (d == label % F) x += 1.0f;
+  return x;
+}
+
+uint16_t bf16_rne(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  return static_cast<uint16_t>((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
 }
 
 }  // namespace
@@ -70,13 +113,57 @@ extern "C" a3g_status a3g_graph_synthesize_features(a3g_graph* g, uint32_t feat_
     const uint64_t noise_key = hash2(rng_key, 0xfea7ull ^ 0xd6e8feb86659fd93ull);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+    constexpr uint64_t kCap = 1ull << 22;  // listed elements (expected ~2e-6 of n x F)
+    unsigned long long* d_cnt = nullptr;
+    uint64_t* d_list = nullptr;
+    A3G_CUDA(cudaMalloc(&d_cnt, 8));
+    A3G_CUDA(cudaMalloc(&d_list, kCap * 8));
+    A3G_CUDA(cudaMemset(d_cnt, 0, 8));
     if (feat_dtype == A3G_FEAT_BF16)
       k_synth_features<uint16_t><<<sms * 8, 256>>>(noise_key, g->n, feat_dim, g->pitch, g->d_labels,
-                                                   static_cast<uint16_t*>(d));
+                                                   static_cast<uint16_t*>(d), d_cnt, d_list, kCap);
     else
       k_synth_features<float><<<sms * 8, 256>>>(noise_key, g->n, feat_dim, g->pitch, g->d_labels,
-                                                static_cast<float*>(d));
+                                                static_cast<float*>(d), d_cnt, d_list, kCap);
     A3G_LAUNCH_CHECK("k_synth_features");
+    unsigned long long listed = 0;
+    A3G_CUDA(cudaMemcpy(&listed, d_cnt, 8, cudaMemcpyDeviceToHost));
+    if (listed > kCap) {
+      cudaFree(d_cnt);
+      cudaFree(d_list);
+      cudaFree(d);
+      raise(A3G_ERR_CUDA, "synthesize_features: too many near-boundary elements to patch");
+    }
+    if (listed) {  // recompute the listed elements with glibc (generators.cpp:20) and patch them
+      std::vector<uint64_t> idx(listed);
+      A3G_CUDA(cudaMemcpy(idx.data(), d_list, listed * 8, cudaMemcpyDeviceToHost));
+      std::vector<float> vf(listed);
+      for (uint64_t k = 0; k < listed; ++k) {
+        const uint64_t v = idx[k] / g->pitch;
+        const uint32_t dd = static_cast<uint32_t>(idx[k] - v * g->pitch);
+        vf[k] = host_element(noise_key, v, dd, feat_dim, g->h_labels.empty() ? 0u : g->h_labels[v]);
+      }
+      uint64_t* d_idx = d_list;
+      void* d_val = nullptr;
+      A3G_CUDA(cudaMalloc(&d_val, listed * 4));
+      const int grid = static_cast<int>(std::min<uint64_t>((listed + 255) / 256, 1024));
+      if (feat_dtype == A3G_FEAT_BF16) {
+        std::vector<uint16_t> vb(listed);
+        for (uint64_t k = 0; k < listed; ++k) vb[k] = bf16_rne(vf[k]);
+        A3G_CUDA(cudaMemcpy(d_val, vb.data(), listed * 2, cudaMemcpyHostToDevice));
+        k_patch<uint16_t><<<grid, 256>>>(d_idx, static_cast<const uint16_t*>(d_val), listed,
+                                         static_cast<uint16_t*>(d));
+      } else {
+        A3G_CUDA(cudaMemcpy(d_val, vf.data(), listed * 4, cudaMemcpyHostToDevice));
+        k_patch<float><<<grid, 256>>>(d_idx, static_cast<const float*>(d_val), listed, static_cast<float*>(d));
+      }
+      A3G_LAUNCH_CHECK("k_patch");
+      A3G_CUDA(cudaDeviceSynchronize());
+      cudaFree(d_val);
+    }
+    g->synth_patched = listed;
+    cudaFree(d_cnt);
+    cudaFree(d_list);
     A3G_CUDA(cudaDeviceSynchronize());
     g->d_feat = d;
     g->view = StoreView{};
@@ -86,3 +173,5 @@ extern "C" a3g_status a3g_graph_synthesize_features(a3g_graph* g, uint32_t feat_
     g->has_features = true;
   });
 }
+
+extern "C" uint64_t a3g_graph_synth_patched(const a3g_graph* g) { return g ? g->synth_patched : 0; }

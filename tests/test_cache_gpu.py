@@ -74,3 +74,19 @@ def test_retrieve_features_sampled_batch_vs_oracle():
     acc = CA.CacheAccounting(1)
     CA.retrieve_features(ds.batch(), c, g, acc)
     assert abs(CA.hit_rate(acc) - oh / (oh + om)) < 1e-12
+
+
+def test_lookup_on_device_two_devices():
+    """cache.cpp:48-68 lookup on the device: per-id devices, any-device hit,
+    per-device hits, over a 2-device round-robin placement."""
+    g = G.generate_power_law(20_000, 3, 2.5, 8, 4)
+    c = CA.build_static_cache(g, CA.CacheConfig(2000 * 8 * 4, 2))
+    ids = np.arange(0, 20_000, 3, dtype=np.uint32)
+    acc = CA.CacheAccounting(2)
+    dev = CA.lookup(c, ids, acc)
+    want = c.device_map[ids]
+    assert np.array_equal(dev, want)
+    assert acc.hits == int((want >= 0).sum()) and acc.misses == int((want < 0).sum())
+    assert acc.per_device_hits == [int((want == 0).sum()), int((want == 1).sum())]
+    with pytest.raises(_lib.ParameterError):
+        CA.lookup(c, [20_000], acc)

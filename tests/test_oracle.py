@@ -126,3 +126,15 @@ def test_oracle_vs_reference_random():
         key = orc.hash2(seed, stream)
         assert np.array_equal(orc.weighted_reservoir(nb, w, m, key)[0], ref.weighted_reservoir(nb, w, m, seed, stream))
         assert np.array_equal(orc.uniform_reservoir(nb, m, key)[0], ref.uniform_reservoir(nb, m, seed, stream))
+
+
+@pytest.mark.parametrize("name,seed", [("pl500", 3), ("pl3000", 1)])
+def test_feature_rows_golden(orc, name, seed):
+    """orc_feature_rows (generators.cpp:12-24 for an explicit node list, the
+    papers-scale row checker) reproduces the reference generator's feature
+    table bit for bit, in any node order."""
+    rec = load_golden(name)
+    n, F = rec["features"].shape
+    ids = np.random.default_rng(0).permutation(n).astype(np.uint32)
+    rows = orc.feature_rows(seed, F, ids, rec["labels"])
+    assert np.array_equal(rows.view(np.uint32), rec["features"][ids].view(np.uint32))

@@ -206,16 +206,20 @@ def test_nccl_gradient_sync_world1(c1):
 @pytest.mark.parametrize("feat_dtype", [0, 1])
 def test_device_feature_synthesis_matches_generator(feat_dtype):
     """Papers-scale inputs: features synthesized on the device from the
-    generator's streams (generators.cpp:12-24) equal the host generator's
-    (bf16: after the same RNE rounding), up to rare 1-ulp libm differences."""
+    generator's streams (generators.cpp:12-24) are BIT-IDENTICAL to the host
+    generator's (bf16: after the same RNE rounding). Elements whose fp64 value
+    sits near a float rounding boundary are recomputed with glibc (synth.cu);
+    200K x 64 elements list a few dozen of them."""
     import ctypes as C
     from paper_2511_07421_b200._lib import check, f32p, lib, ptr, u32p, vp
-    n, F = 20000, 24
+    n, F = 200_000, 64
     full = G.generate_power_law(n, 3, 2.5, F, 7)
     topo = G.generate_power_law(n, 3, 2.5, 1, 7)
     assert np.array_equal(full.col_indices, topo.col_indices) and np.array_equal(full.labels, topo.labels)
     dg = G.DeviceGraph(topo, 0, feat_dtype, upload_features=False)
     check(lib().a3g_graph_synthesize_features(dg.h, F, feat_dtype, 7))
+    patched = lib().a3g_graph_synth_patched(dg.h)
+    assert 0 < patched < 1e-4 * n * F, patched
     hc = vp()
     check(lib().a3g_cache_from_map(dg.h, None, 1, C.byref(hc)))
     ids = np.arange(n, dtype=np.uint32)
@@ -227,9 +231,7 @@ def test_device_feature_synthesis_matches_generator(feat_dtype):
     if feat_dtype == 1:
         u = want.view(np.uint32).astype(np.uint64)
         want = (((u + 0x7fff + ((u >> 16) & 1)) >> 16) << 16).astype(np.uint32).view(np.float32)
-    diff = out != want
-    assert diff.mean() < 1e-5, diff.sum()
-    np.testing.assert_allclose(out, want, rtol=1e-2 if feat_dtype else 1e-6, atol=1e-6)
+    assert np.array_equal(out.view(np.uint32), want.view(np.uint32)), int((out != want).sum())
 
 
 def test_pipeline_shapes_bit_identical(c1):

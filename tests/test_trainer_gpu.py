@@ -1,7 +1,8 @@
 """Device 2-layer mean-GCN step vs the fp64 oracle. Tolerance (fp32 device vs
 fp64 reference): norm-wise relative error <= 1e-3 for loss, logits, gradients
-and intermediates (BASELINE.json north_star); bf16 feature mode is checked
-against the oracle fed the same bf16-rounded features at 2e-3."""
+and intermediates (BASELINE.json north_star). bf16 feature mode has the same
+stated tolerance, 1e-3, against the fp64 oracle fed the same bf16-rounded
+features (the rows are exact; only the fp32 accumulation differs)."""
 import numpy as np
 import pytest
 
@@ -143,7 +144,7 @@ def test_bf16_features(orc, c1):
     g = c1
     cache = CA.build_static_cache(g, CA.CacheConfig(int(0.2 * g.num_nodes) * g.feat_dim * 4, 1))
     seeds = np.arange(0, 60_000, 59, dtype=np.uint32)
-    _grad_case(orc, g, cache, seeds, [10, 5], 8.0, 0, 21, feat_dtype=1, tol=2e-3)
+    _grad_case(orc, g, cache, seeds, [10, 5], 8.0, 0, 21, feat_dtype=1, tol=TOL)
 
 
 @pytest.mark.parametrize("name", ["pl3000"])

@@ -253,6 +253,14 @@ a3g_status a3g_trainer_step_stats(a3g_trainer* t, uint64_t* out, uint32_t num_st
  * accuracy over test_mask (host u8[n]). ConfigError when no test nodes. */
 a3g_status a3g_evaluate_full_graph(a3g_trainer* t, const uint8_t* test_mask, double* accuracy);
 
+/* pipeline.hpp:57-60 profile_stage_costs on the device: one probe of
+ * sample_khop (host seeds), retrieve_features (the unique rows gathered into
+ * HBM) and grad_on_batch (forward + backward, weights unchanged), timed with
+ * CUDA events on the compute stream: stage_ms[3] = {t_sample, t_batch,
+ * t_train} in ms. */
+a3g_status a3g_trainer_profile_step(a3g_trainer* t, const uint32_t* seeds, uint32_t n_seeds, double bias_rate,
+                                    int kind, uint64_t rng_seed, double* stage_ms);
+
 /* Debug/parity copy-out of the last step (host f64 buffers; NULL skips):
  * gradients (F*H, H*C), and ForwardResult arrays (trainer.hpp:49-60). */
 a3g_status a3g_trainer_last_grads(a3g_trainer* t, double* gw1, double* gw2);
@@ -265,6 +273,44 @@ a3g_sampler* a3g_trainer_sampler(a3g_trainer* t, int slot);
  * gather+aggregation kernel (the roofline kernel) with its algorithmic bytes. */
 a3g_status a3g_trainer_timing(a3g_trainer* t, double* total_ms, double* agg_kernel_ms,
                               double* agg_bytes_per_launch, uint64_t* launches_per_step);
+
+/* ------------------------------------------------------- explicit batch --- */
+/* The reference's per-batch model calls on an EXPLICIT host batch -- the
+ * SampleBatch (sampler.hpp:30-46) and the feats array the caller passes --
+ * run through the same device kernels as the pipeline (explicit.cu). Backs
+ * the drop-in's train::forward / backward / grad_on_batch
+ * (trainer.hpp:63-79, trainer.cpp:59-239). One model per host thread. */
+typedef struct a3g_batch_model a3g_batch_model;
+a3g_status a3g_batch_model_create(int device, uint32_t feat_dim, uint32_t hidden_dim, uint32_t num_classes,
+                                  a3g_batch_model** out);
+void a3g_batch_model_destroy(a3g_batch_model* m);
+/* Loads unique count, unique-seed count, num_layers layers of (dst_idx,
+ * src_idx) pairs (layers >= 2 are ignored, as trainer.cpp does), feats
+ * (host f32[n_unique * feat_dim], unique-node order) and the seed labels
+ * (host u32[n_seed_unique], NULL = zeros: forward only). n_inner_out = the
+ * ForwardResult's |inner_nodes|. */
+a3g_status a3g_batch_model_load(a3g_batch_model* m, uint64_t n_unique, uint64_t n_seed_unique,
+                                uint32_t num_layers, const uint64_t* layer_ne, const uint32_t* const* layer_dst,
+                                const uint32_t* const* layer_src, const float* feats, const uint32_t* seed_labels,
+                                uint64_t* n_inner_out);
+/* forward + softmax-CE backward with W1 (F x H), W2 (H x C) f64 host: mean
+ * loss and gradients (f64 host, NULL skips). Weights are not changed. */
+a3g_status a3g_batch_model_run(a3g_batch_model* m, const double* w1, const double* w2, double* loss,
+                               double* gw1, double* gw2);
+/* ForwardResult (trainer.hpp:49-60) of the last run, host buffers, NULL
+ * skips: inner_nodes u32[n_inner], inner_pos i32[n_unique], inner_deg
+ * u32[n_inner], outer_deg u32[n_seed_unique], agg_inner f64[n_inner*F],
+ * h1 f64[n_inner*H] (post-ReLU), agg_outer f64[n_seed_unique*H], logits
+ * f64[n_seed_unique*C]. */
+a3g_status a3g_batch_model_forward(a3g_batch_model* m, uint32_t* inner_nodes, int32_t* inner_pos,
+                                   uint32_t* inner_deg, uint32_t* outer_deg, double* agg_inner, double* h1,
+                                   double* agg_outer, double* logits);
+/* trainer.cpp:208-211 sgd_step on the device: w[i] += (-lr) * g[i] (f64,
+ * product and sum rounded separately as the reference's scalar axpy). */
+a3g_status a3g_sgd_step(int device, double* w, const double* g, uint64_t n, double lr);
+/* trainer.cpp:213-229 sync_gradients on the device: out = (g_0 + ... +
+ * g_{k-1}) * (1/k), summed in list order. ParameterError when k == 0. */
+a3g_status a3g_mean_gradients(int device, const double* const* grads, uint32_t k, uint64_t n, double* out);
 
 /* ---------------------------------------------------------------- comm --- */
 /* NCCL communicator for data-parallel gradient sync (trainer.cpp:213-229 ->

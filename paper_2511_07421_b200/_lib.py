@@ -126,7 +126,16 @@ _SIGS = {
     "a3g_trainer_last_grads": (C.c_int, [vp, f64p, f64p]),
     "a3g_trainer_last_forward": (C.c_int, [vp, u64p, f64p, f64p, f64p, f64p]),
     "a3g_trainer_sampler": (vp, [vp, C.c_int]),
+    "a3g_trainer_profile_step": (C.c_int, [vp, u32p, C.c_uint32, C.c_double, C.c_int, C.c_uint64, f64p]),
     "a3g_trainer_timing": (C.c_int, [vp, f64p, f64p, f64p, u64p]),
+    "a3g_batch_model_create": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(vp)]),
+    "a3g_batch_model_destroy": (None, [vp]),
+    "a3g_batch_model_load": (C.c_int, [vp, C.c_uint64, C.c_uint64, C.c_uint32, u64p, C.POINTER(u32p),
+                                       C.POINTER(u32p), f32p, u32p, u64p]),
+    "a3g_batch_model_run": (C.c_int, [vp, f64p, f64p, f64p, f64p, f64p]),
+    "a3g_batch_model_forward": (C.c_int, [vp, u32p, i32p, u32p, u32p, f64p, f64p, f64p, f64p]),
+    "a3g_sgd_step": (C.c_int, [C.c_int, f64p, f64p, C.c_uint64, C.c_double]),
+    "a3g_mean_gradients": (C.c_int, [C.c_int, C.POINTER(f64p), C.c_uint32, C.c_uint64, f64p]),
     "a3g_comm_unique_id": (C.c_int, [u8p]),
     "a3g_comm_create": (C.c_int, [u8p, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
     "a3g_comm_destroy": (None, [vp]),

@@ -810,6 +810,7 @@ void a3g_trainer_destroy(a3g_trainer* tr) {
   dfree(t.d_amax);
   dfree(t.d_part);
   dfree(t.d_hpart);
+  dfree(t.d_gather);
   dfree(t.d_agg_bytes);
   dfree(t.d_losses);
   dfree(t.d_stats);
@@ -1100,6 +1101,46 @@ a3g_status a3g_trainer_last_forward(a3g_trainer* tr, uint64_t* n_inner, double* 
       for (uint64_t r = 0; r < ni; ++r)
         for (uint32_t f = 0; f < t.F; ++f) agg_inner[r * t.F + f] = tmp[r * t.pitch + f];
     }
+  });
+}
+
+a3g_status a3g_trainer_profile_step(a3g_trainer* tr, const uint32_t* seeds, uint32_t n_seeds, double gamma,
+                                    int kind, uint64_t rng_seed, double* stage_ms) {
+  return guard([&] {
+    TrainerState& t = tr->st;
+    A3G_CUDA(cudaSetDevice(t.g->device));
+    a3g_sampler* smp = t.smp[0];
+    SamplerState& s = smp->st;
+    cudaEvent_t ev[5];
+    for (auto& e : ev) A3G_CUDA(cudaEventCreate(&e));
+    // stage 1: sample_khop (the host seed copy included, as the reference's
+    // sample_unit reads host seeds)
+    A3G_CUDA(cudaEventRecord(ev[0], t.s_comp));
+    sample_impl(s, seeds, n_seeds, false, gamma, kind, rng_seed, t.s_comp);
+    A3G_CUDA(cudaEventRecord(ev[1], t.s_comp));
+    // stage 2: retrieve_features -- the unique rows gathered into HBM
+    read_counters(s, t.s_comp);
+    const uint64_t U = s.h_ctr->ucount[s.L];
+    const uint64_t need = std::max<uint64_t>(U, 1) * t.F;
+    if (need > t.gather_cap) {
+      dfree(t.d_gather);
+      t.d_gather = dalloc<float>(need);
+      t.gather_cap = need;
+    }
+    A3G_CUDA(cudaEventRecord(ev[2], t.s_comp));
+    launch_gather_unique(s, t.d_gather, t.s_comp);
+    A3G_CUDA(cudaEventRecord(ev[3], t.s_comp));
+    // stage 3: grad_on_batch (lr = 0: the weights are not changed)
+    launch_train_compute(t, smp, 0.0, t.d_losses, nullptr, t.s_comp, false);
+    A3G_CUDA(cudaEventRecord(ev[4], t.s_comp));
+    A3G_CUDA(cudaStreamSynchronize(t.s_comp));
+    A3G_CUDA(cudaMemsetAsync(&s.d_ctr->hits, 0, 8, t.s_comp));
+    float ms[3];
+    A3G_CUDA(cudaEventElapsedTime(&ms[0], ev[0], ev[1]));
+    A3G_CUDA(cudaEventElapsedTime(&ms[1], ev[2], ev[3]));
+    A3G_CUDA(cudaEventElapsedTime(&ms[2], ev[3], ev[4]));
+    for (auto& e : ev) cudaEventDestroy(e);
+    for (int i = 0; i < 3; ++i) stage_ms[i] = ms[i];
   });
 }
 

@@ -66,6 +66,8 @@ struct TrainerState {
   float* d_hpart = nullptr; // split-K partials of the h1 GEMM [h1_split_cap][cap_inner][H]
   uint32_t h1_split_cap = 1;
   bool h1_split_used = false;  // the last step's h1 GEMM ran split-K (+ k_h1_reduce)
+  float* d_gather = nullptr;   // a3g_trainer_profile_step: the unique rows of a retrieve_features stage
+  uint64_t gather_cap = 0;
 };
 
 // Compute part of one step on s_comp for the batch in arena `smp`

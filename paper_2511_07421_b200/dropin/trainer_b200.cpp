@@ -1,8 +1,14 @@
-// trainer_b200.cpp -- drop-in for train::train and train::evaluate_full_graph
-// (trainer.hpp:81-117, trainer.cpp:241-303, 350-424): every step -- sampling,
-// fused gather + mean aggregation, forward, backward, SGD -- runs on the
-// device through the CUDA-stream pipeline (a3g_train_steps_v); the host plans
-// the epoch's batches and seeds exactly as the reference.
+// trainer_b200.cpp -- drop-in for the trainer entry points of trainer.hpp:
+//  * forward / backward / grad_on_batch (trainer.cpp:59-239) on the caller's
+//    explicit SampleBatch + feats: one device model per host thread
+//    (a3g_batch_model_*, the pipeline's own kernels);
+//  * sgd_step / sync_gradients (trainer.cpp:208-229) on the device
+//    (a3g_sgd_step, a3g_mean_gradients);
+//  * train (trainer.cpp:350-424) and evaluate_full_graph (:241-303): every
+//    step -- sampling, fused gather + mean aggregation, forward, backward,
+//    SGD -- runs on the device through the CUDA-stream pipeline
+//    (a3g_train_steps_v); the host plans the epoch's batches and seeds exactly
+//    as the reference.
 #include <algorithm>
 #include <cmath>
 #include <limits>
@@ -33,7 +39,126 @@ std::unique_ptr<TrainerHandle> make_trainer(const Graph& g, const CacheState& c,
   return t;
 }
 
+// This thread's device model for explicit batches of (F, H, C).
+a3g_batch_model* thread_model(const ModelSpec& spec) {
+  struct Slot {
+    a3g_batch_model* m = nullptr;
+    std::uint32_t F = 0, H = 0, C = 0;
+    ~Slot() { a3g_batch_model_destroy(m); }
+  };
+  thread_local Slot slot;
+  if (!slot.m || slot.F != spec.feat_dim || slot.H != spec.hidden_dim || slot.C != spec.num_classes) {
+    a3g_batch_model_destroy(slot.m);
+    slot.m = nullptr;
+    b200::check(a3g_batch_model_create(b200::device(), spec.feat_dim, spec.hidden_dim, spec.num_classes, &slot.m));
+    slot.F = spec.feat_dim;
+    slot.H = spec.hidden_dim;
+    slot.C = spec.num_classes;
+  }
+  return slot.m;
+}
+
+// Loads (batch, feats, labels) into the thread's device model; returns n_inner.
+std::uint64_t load(a3g_batch_model* dm, const SampleBatch& batch, const float* feats, const std::uint32_t* labels) {
+  const std::size_t L = std::min<std::size_t>(batch.layers.size(), 2);  // trainer.cpp reads layers[0..1]
+  std::vector<std::vector<std::uint32_t>> d(L), s(L);
+  std::vector<const std::uint32_t*> pd(std::max<std::size_t>(L, 1)), ps(std::max<std::size_t>(L, 1));
+  std::vector<std::uint64_t> ne(std::max<std::size_t>(L, 1), 0);
+  for (std::size_t l = 0; l < L; ++l) {
+    const auto& e = batch.layers[l].edges;
+    d[l].resize(e.size());
+    s[l].resize(e.size());
+    for (std::size_t i = 0; i < e.size(); ++i) {
+      d[l][i] = e[i].first;
+      s[l][i] = e[i].second;
+    }
+    pd[l] = d[l].data();
+    ps[l] = s[l].data();
+    ne[l] = e.size();
+  }
+  std::uint64_t n_inner = 0;
+  b200::check(a3g_batch_model_load(dm, batch.unique_nodes.size(), batch.num_seed_unique,
+                                   static_cast<std::uint32_t>(L), ne.data(), pd.data(), ps.data(), feats, labels,
+                                   &n_inner));
+  return n_inner;
+}
+
 }  // namespace
+
+ForwardResult forward(const Model& m, const SampleBatch& batch, const float* feats) {
+  const ModelSpec& spec = m.spec;
+  a3g_batch_model* dm = thread_model(spec);
+  const std::uint64_t ni = load(dm, batch, feats, nullptr);
+  b200::check(a3g_batch_model_run(dm, m.w1.data(), m.w2.data(), nullptr, nullptr, nullptr));
+  const std::size_t ns = batch.num_seed_unique;
+  ForwardResult out;
+  out.inner_nodes.resize(ni);
+  out.inner_pos.resize(batch.unique_nodes.size());
+  out.inner_deg.resize(ni);
+  out.outer_deg.resize(ns);
+  out.agg_inner.resize(ni * spec.feat_dim);
+  out.h1.resize(ni * spec.hidden_dim);
+  out.agg_outer.resize(ns * spec.hidden_dim);
+  out.logits.resize(ns * spec.num_classes);
+  b200::check(a3g_batch_model_forward(dm, out.inner_nodes.data(), out.inner_pos.data(), out.inner_deg.data(),
+                                      out.outer_deg.data(), out.agg_inner.data(), out.h1.data(),
+                                      out.agg_outer.data(), out.logits.data()));
+  // modelled as 4 bytes per value (trainer.cpp:134-135)
+  out.activation_bytes = (out.agg_inner.size() + out.h1.size() + out.agg_outer.size() + out.logits.size()) * 4;
+  return out;
+}
+
+// The device recomputes the forward pass it needs (fwd is the caller's cache
+// of it; the kernels keep their own activations resident).
+double backward(const Model& m, const SampleBatch& batch, const float* feats, const ForwardResult& fwd,
+                const std::vector<std::uint32_t>& seed_labels, Gradients& grads) {
+  (void)fwd;
+  if (seed_labels.size() != batch.num_seed_unique) throw ParameterError("backward: seed_labels size mismatch");
+  a3g_batch_model* dm = thread_model(m.spec);
+  load(dm, batch, feats, seed_labels.data());
+  grads.w1.assign(m.w1.size(), 0.0);
+  grads.w2.assign(m.w2.size(), 0.0);
+  double loss = 0.0;
+  b200::check(a3g_batch_model_run(dm, m.w1.data(), m.w2.data(), &loss, grads.w1.data(), grads.w2.data()));
+  return loss;
+}
+
+double grad_on_batch(const Model& m, const Graph& g, const SampleBatch& batch, const float* feats,
+                     Gradients& grads) {
+  std::vector<std::uint32_t> labels(batch.num_seed_unique);  // trainer.cpp:234-237
+  for (std::size_t s = 0; s < batch.num_seed_unique; ++s) labels[s] = g.labels[batch.unique_nodes[s]];
+  a3g_batch_model* dm = thread_model(m.spec);
+  load(dm, batch, feats, labels.data());
+  grads.w1.assign(m.w1.size(), 0.0);
+  grads.w2.assign(m.w2.size(), 0.0);
+  double loss = 0.0;
+  b200::check(a3g_batch_model_run(dm, m.w1.data(), m.w2.data(), &loss, grads.w1.data(), grads.w2.data()));
+  return loss;
+}
+
+void sgd_step(Model& m, const Gradients& g, double lr) {
+  b200::check(a3g_sgd_step(b200::device(), m.w1.data(), g.w1.data(), std::min(m.w1.size(), g.w1.size()), lr));
+  b200::check(a3g_sgd_step(b200::device(), m.w2.data(), g.w2.data(), std::min(m.w2.size(), g.w2.size()), lr));
+}
+
+Gradients sync_gradients(const std::vector<Gradients>& grads) {
+  if (grads.empty()) throw ParameterError("sync_gradients: empty gradient list");
+  for (const Gradients& g : grads)
+    if (g.w1.size() != grads[0].w1.size() || g.w2.size() != grads[0].w2.size())
+      throw ParameterError("sync_gradients: shape mismatch");
+  Gradients out;
+  out.w1.resize(grads[0].w1.size());
+  out.w2.resize(grads[0].w2.size());
+  std::vector<const double*> p1, p2;
+  for (const Gradients& g : grads) {
+    p1.push_back(g.w1.data());
+    p2.push_back(g.w2.data());
+  }
+  const auto k = static_cast<std::uint32_t>(grads.size());
+  b200::check(a3g_mean_gradients(b200::device(), p1.data(), k, out.w1.size(), out.w1.data()));
+  b200::check(a3g_mean_gradients(b200::device(), p2.data(), k, out.w2.size(), out.w2.data()));
+  return out;
+}
 
 double evaluate_full_graph(const Model& m, const Graph& g) {
   const ModelSpec& spec = m.spec;

@@ -305,9 +305,11 @@ a3g_status a3g_batch_model_run(a3g_batch_model* m, const double* w1, const doubl
 a3g_status a3g_batch_model_forward(a3g_batch_model* m, uint32_t* inner_nodes, int32_t* inner_pos,
                                    uint32_t* inner_deg, uint32_t* outer_deg, double* agg_inner, double* h1,
                                    double* agg_outer, double* logits);
-/* trainer.cpp:208-211 sgd_step on the device: w[i] += (-lr) * g[i] (f64,
- * product and sum rounded separately as the reference's scalar axpy). */
-a3g_status a3g_sgd_step(int device, double* w, const double* g, uint64_t n, double lr);
+/* trainer.cpp:208-211 sgd_step on the device: w[i] += (-lr) * g[i] in f64,
+ * bit-identical to the reference's active kernel table: the first n_fused
+ * elements as one fused multiply-add (AVX2 table: n - n % 4), the rest with
+ * product and sum rounded separately (scalar table: n_fused = 0). */
+a3g_status a3g_sgd_step(int device, double* w, const double* g, uint64_t n, uint64_t n_fused, double lr);
 /* trainer.cpp:213-229 sync_gradients on the device: out = (g_0 + ... +
  * g_{k-1}) * (1/k), summed in list order. ParameterError when k == 0. */
 a3g_status a3g_mean_gradients(int device, const double* const* grads, uint32_t k, uint64_t n, double* out);

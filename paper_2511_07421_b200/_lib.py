@@ -134,7 +134,7 @@ _SIGS = {
                                        C.POINTER(u32p), f32p, u32p, u64p]),
     "a3g_batch_model_run": (C.c_int, [vp, f64p, f64p, f64p, f64p, f64p]),
     "a3g_batch_model_forward": (C.c_int, [vp, u32p, i32p, u32p, u32p, f64p, f64p, f64p, f64p]),
-    "a3g_sgd_step": (C.c_int, [C.c_int, f64p, f64p, C.c_uint64, C.c_double]),
+    "a3g_sgd_step": (C.c_int, [C.c_int, f64p, f64p, C.c_uint64, C.c_uint64, C.c_double]),
     "a3g_mean_gradients": (C.c_int, [C.c_int, C.POINTER(f64p), C.c_uint32, C.c_uint64, f64p]),
     "a3g_comm_unique_id": (C.c_int, [u8p]),
     "a3g_comm_create": (C.c_int, [u8p, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),

@@ -91,8 +91,11 @@ DROPIN_OUT = os.path.join(DROPIN, "_build")
 DROPIN_LIBS = {
     # sampler + cache hot functions only: the reference's train()/executor run on them
     "liba3gnn_b200_sampling.so": ["registry.cpp", "sampler_b200.cpp", "cache_b200.cpp"],
-    # + train() / evaluate_full_graph on the device
-    "liba3gnn_b200.so": ["registry.cpp", "sampler_b200.cpp", "cache_b200.cpp", "trainer_b200.cpp"],
+    # + the trainer (forward / backward / grad_on_batch / sgd_step /
+    # sync_gradients / train / evaluate_full_graph) and the executor
+    # (execute_pipeline / profile_stage_costs) on the device
+    "liba3gnn_b200.so": ["registry.cpp", "sampler_b200.cpp", "cache_b200.cpp", "trainer_b200.cpp",
+                         "pipeline_b200.cpp"],
 }
 
 

@@ -34,12 +34,14 @@ T* dalloc_x(size_t n) {
   return p;
 }
 
-// trainer.cpp:208-211 (kernels::axpy(-lr, g, w)): w[i] += (-lr) * g[i], the
-// product and the sum rounded separately as the scalar kernel table does.
-__global__ void k_sgd_f64(double* w, const double* g, uint64_t n, double a) {
+// trainer.cpp:208-211 (kernels::axpy(-lr, g, w)): w[i] += (-lr) * g[i]. The
+// first n_fused elements with one fused multiply-add (the AVX2 kernel table
+// fuses blocks of four, kernels_avx2.cpp:14-22), the rest with the product
+// and the sum rounded separately (its scalar tail, and the scalar table).
+__global__ void k_sgd_f64(double* w, const double* g, uint64_t n, uint64_t n_fused, double a) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    w[i] = __dadd_rn(w[i], __dmul_rn(a, g[i]));
+    w[i] = i < n_fused ? __fma_rn(a, g[i], w[i]) : __dadd_rn(w[i], __dmul_rn(a, g[i]));
 }
 
 // trainer.cpp:213-229: out = (sum over k in list order) * (1 / k).
@@ -318,14 +320,14 @@ a3g_status a3g_batch_model_forward(a3g_batch_model* m, uint32_t* inner_nodes, in
   });
 }
 
-a3g_status a3g_sgd_step(int device, double* w, const double* g, uint64_t n, double lr) {
+a3g_status a3g_sgd_step(int device, double* w, const double* g, uint64_t n, uint64_t n_fused, double lr) {
   return guard([&] {
     if (n == 0) return;
     A3G_CUDA(cudaSetDevice(device));
     double* d = dalloc_x<double>(2 * n);
     A3G_CUDA(cudaMemcpy(d, w, n * 8, cudaMemcpyHostToDevice));
     A3G_CUDA(cudaMemcpy(d + n, g, n * 8, cudaMemcpyHostToDevice));
-    k_sgd_f64<<<static_cast<int>(std::min<uint64_t>((n + 255) / 256, 1024)), 256>>>(d, d + n, n, -lr);
+    k_sgd_f64<<<static_cast<int>(std::min<uint64_t>((n + 255) / 256, 1024)), 256>>>(d, d + n, n, std::min(n, n_fused), -lr);
     A3G_LAUNCH_CHECK("k_sgd_f64");
     A3G_CUDA(cudaMemcpy(w, d, n * 8, cudaMemcpyDeviceToHost));
     cudaFree(d);

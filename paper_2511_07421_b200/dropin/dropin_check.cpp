@@ -126,6 +126,91 @@ int main(int argc, char** argv) {
     std::printf("train epoch %zu loss %.17g hit %.17g\n", e, rep.loss_curve[e], rep.epoch_hit_rates[e]);
   std::printf("train accuracy %.17g batch_bytes %llu act_bytes %llu\n", rep.test_accuracy,
               (unsigned long long)rep.max_batch_bytes, (unsigned long long)rep.max_activation_bytes);
+  // the per-batch model entry points on one explicit batch (trainer.cpp:59-239)
+  {
+    sampling::SamplerConfig cfg;
+    cfg.fanouts = {10, 5};
+    cfg.bias_rate = 8.0;
+    cfg.rng_seed = train::sampling_seed(3, 0, 0, 0);
+    const auto b = sampling::sample_khop(g, batches[1], cfg, cache);
+    cache::CacheAccounting a1(1);
+    const auto feats = cache::retrieve_features(b, cache, g, a1).first;
+    const train::Model m = train::init_model(spec, 1);
+    const auto fwd = train::forward(m, b, feats.data());
+    double lsum = 0, asum = 0, hsum = 0;
+    for (double x : fwd.logits) lsum += x * x;
+    for (double x : fwd.agg_inner) asum += x * x;
+    for (double x : fwd.h1) hsum += x * x;
+    std::uint64_t ih = fnv(fwd.inner_nodes.data(), fwd.inner_nodes.size() * 4);
+    ih = fnv(fwd.inner_pos.data(), fwd.inner_pos.size() * 4, ih);
+    std::uint64_t dh = fnv(fwd.inner_deg.data(), fwd.inner_deg.size() * 4);
+    dh = fnv(fwd.outer_deg.data(), fwd.outer_deg.size() * 4, dh);
+    std::printf("model forward n_inner %zu inner %016llx deg %016llx act %llu logits2 %.17g agg2 %.17g h12 %.17g\n",
+                fwd.inner_nodes.size(), (unsigned long long)ih, (unsigned long long)dh,
+                (unsigned long long)fwd.activation_bytes, lsum, asum, hsum);
+    std::vector<std::uint32_t> labels(b.num_seed_unique);
+    for (std::size_t i = 0; i < labels.size(); ++i) labels[i] = g.labels[b.unique_nodes[i]];
+    train::Gradients gb, gg;
+    const double lb = train::backward(m, b, feats.data(), fwd, labels, gb);
+    const double lg = train::grad_on_batch(m, g, b, feats.data(), gg);
+    double n1 = 0, n2 = 0;
+    for (double x : gg.w1) n1 += x * x;
+    for (double x : gg.w2) n2 += x * x;
+    std::printf("model grad loss %.17g backward_loss %.17g gw1 %.17g gw2 %.17g\n", lg, lb, n1, n2);
+    // sync_gradients / sgd_step on fixed inputs (init_model draws): bit-identical
+    // to the reference's active kernel table
+    const train::Model ma = train::init_model(spec, 11), mb = train::init_model(spec, 12);
+    train::Gradients x, y;
+    x.w1 = ma.w1;
+    x.w2 = ma.w2;
+    y.w1 = mb.w1;
+    y.w2 = mb.w2;
+    const auto mean = train::sync_gradients({x, y, x});
+    train::Model m2 = m;
+    train::sgd_step(m2, mean, 0.2);
+    std::printf("sync %016llx sgd %016llx %016llx\n", (unsigned long long)fnv(mean.w1.data(), mean.w1.size() * 8,
+                                                                               fnv(mean.w2.data(), mean.w2.size() * 8)),
+                (unsigned long long)fnv(m2.w1.data(), m2.w1.size() * 8),
+                (unsigned long long)fnv(m2.w2.data(), m2.w2.size() * 8));
+    try {
+      train::sync_gradients({});
+    } catch (const ParameterError& e) {
+      std::printf("error ParameterError %s\n", e.what());
+    }
+  }
+  // profile_stage_costs: the three stage medians the analytic model consumes
+  {
+    ResolvedDesign d;
+    d.batch_size = 512;
+    d.bias_rate = 8.0;
+    d.cache_volume = cc.volume_bytes;
+    pipeline::PlatformSpec plat;
+    sampling::SamplerConfig pcfg;
+    pcfg.fanouts = {10, 5};
+    pcfg.rng_seed = 3;
+    const auto c = pipeline::profile_stage_costs(g, d, plat, spec, pcfg, 3);
+    std::printf("profile iters %llu positive %d\n", (unsigned long long)c.iters_per_epoch,
+                c.t_sample > 0 && c.t_batch > 0 && c.t_train > 0 ? 1 : 0);
+  }
+  // execute_pipeline in the three modes (sequential; pmode1 / pmode2 with 4 workers)
+  for (Mode mode : {Mode::sequential, Mode::pmode2}) {
+    ResolvedDesign d;
+    d.batch_size = 512;
+    d.bias_rate = 8.0;
+    d.workers = 4;
+    d.cache_volume = cc.volume_bytes;
+    d.mode = mode;
+    pipeline::PlatformSpec plat;
+    pipeline::ExecOptions eo;
+    eo.epochs = 1;
+    sampling::SamplerConfig pcfg;
+    pcfg.fanouts = {10, 5};
+    pcfg.rng_seed = 3;
+    const auto ex = pipeline::execute_pipeline(g, d, plat, spec, pcfg, eo);
+    std::printf("pipeline %s accuracy %.17g hit %.17g batch_bytes %llu model_bytes %llu\n", to_string(mode).c_str(),
+                ex.metrics.accuracy, ex.hit_rate, (unsigned long long)ex.batch_bytes_max,
+                (unsigned long long)ex.model_bytes);
+  }
   // execute_pipeline pmode1 with 4 producer threads: concurrent sample_khop
   ResolvedDesign d;
   d.batch_size = 512;

@@ -14,6 +14,7 @@
 #include <limits>
 #include <memory>
 
+#include "a3gnn/kernels.hpp"
 #include "a3gnn/rng.hpp"
 #include "a3gnn/trainer.hpp"
 #include "dropin.hpp"
@@ -137,8 +138,14 @@ double grad_on_batch(const Model& m, const Graph& g, const SampleBatch& batch, c
 }
 
 void sgd_step(Model& m, const Gradients& g, double lr) {
-  b200::check(a3g_sgd_step(b200::device(), m.w1.data(), g.w1.data(), std::min(m.w1.size(), g.w1.size()), lr));
-  b200::check(a3g_sgd_step(b200::device(), m.w2.data(), g.w2.data(), std::min(m.w2.size(), g.w2.size()), lr));
+  // the reference's axpy is fused in blocks of four under the AVX2 table
+  const bool fused = kernels::active_backend() == kernels::Backend::avx2;
+  auto step = [&](std::vector<double>& w, const std::vector<double>& gr) {
+    const std::size_t n = std::min(w.size(), gr.size());
+    b200::check(a3g_sgd_step(b200::device(), w.data(), gr.data(), n, fused ? n - n % 4 : 0, lr));
+  };
+  step(m.w1, g.w1);
+  step(m.w2, g.w2);
 }
 
 Gradients sync_gradients(const std::vector<Gradients>& grads) {

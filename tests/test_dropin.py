@@ -6,9 +6,12 @@ reference (oracle/_ref) with LD_PRELOAD.
   reservoirs): every line of dropin_check -- including the reference's own
   train() and execute_pipeline() running on device-sampled batches with 4
   concurrent producer threads -- is bit-identical to the reference alone;
-* full drop-in (+ train / evaluate_full_graph on the device): batches and
-  hit rates identical, losses within 1e-3 relative (fp32 device vs fp64),
-  accuracies within 3 test nodes.
+* full drop-in (+ forward / backward / grad_on_batch / sgd_step /
+  sync_gradients / train / evaluate_full_graph and the executor's
+  execute_pipeline / profile_stage_costs on the device): batches, index
+  arrays and hit rates identical, losses and gradients within 1e-3 relative
+  (fp32 device vs fp64), accuracies within 3 test nodes, sgd_step and
+  sync_gradients bit-identical.
 """
 import os
 import re
@@ -42,7 +45,11 @@ def test_dropin_exports_reference_symbols():
     out = subprocess.run(["nm", "-DC", "--defined-only", LIB_FULL], capture_output=True, text=True).stdout
     for sym in ("a3gnn::sampling::sample_khop(", "a3gnn::sampling::weighted_reservoir_sample(",
                 "a3gnn::sampling::uniform_reservoir_sample(", "a3gnn::cache::retrieve_features(",
-                "a3gnn::cache::build_static_cache(", "a3gnn::train::train(", "a3gnn::train::evaluate_full_graph("):
+                "a3gnn::cache::build_static_cache(", "a3gnn::cache::lookup(", "a3gnn::cache::hit_rate(",
+                "a3gnn::train::train(", "a3gnn::train::evaluate_full_graph(", "a3gnn::train::forward(",
+                "a3gnn::train::backward(", "a3gnn::train::grad_on_batch(", "a3gnn::train::sgd_step(",
+                "a3gnn::train::sync_gradients(", "a3gnn::pipeline::execute_pipeline(",
+                "a3gnn::pipeline::profile_stage_costs("):
         assert sym in out, sym
     out = subprocess.run(["nm", "-DC", "--defined-only", LIB_SAMPLING], capture_output=True, text=True).stdout
     assert "a3gnn::train::train(" not in out and "a3gnn::sampling::sample_khop(" in out
@@ -68,17 +75,43 @@ def _num(line, key):
 @needs_build
 @pytest.mark.gpu
 def test_full_dropin_matches_reference():
+    """Everything of the drop-in interposed: train(), execute_pipeline() in
+    the three modes, profile_stage_costs() and the per-batch model calls
+    (forward / backward / grad_on_batch / sgd_step / sync_gradients) run on the
+    device. Index outputs, hit rates and byte counts are identical; fp32 device
+    values are within 1e-3 of the fp64 reference; sgd_step / sync_gradients
+    are bit-identical to the reference's active kernel table."""
     ref, dev = run(), run(LIB_FULL)
     assert len(ref) == len(dev)
+    seen = set()
     for a, b in zip(ref, dev):
+        tag = " ".join(a.split()[:2])
+        seen.add(a.split()[0])
         if a.startswith("train epoch"):
             assert _num(a, "hit") == _num(b, "hit")
             assert abs(_num(a, "loss") - _num(b, "loss")) <= 1e-3 * abs(_num(a, "loss"))
         elif a.startswith("train accuracy"):
             assert abs(_num(a, "accuracy") - _num(b, "accuracy")) <= 3.0 / NTEST
             assert _num(a, "batch_bytes") == _num(b, "batch_bytes") and _num(a, "act_bytes") == _num(b, "act_bytes")
-        elif a.startswith("pipeline"):  # the reference executor, device evaluate_full_graph at its end
-            assert abs(_num(a, "accuracy") - _num(b, "accuracy")) <= 3.0 / NTEST
-            assert _num(a, "hit") == _num(b, "hit")
+        elif a.startswith("pipeline"):  # every executor mode on the device
+            assert a.split()[1] == b.split()[1], (a, b)
+            assert abs(_num(a, "accuracy") - _num(b, "accuracy")) <= 3.0 / NTEST, (a, b)
+            assert _num(a, "hit") == _num(b, "hit"), (a, b)
+            if "batch_bytes" in a:
+                assert _num(a, "batch_bytes") == _num(b, "batch_bytes")
+                assert _num(a, "model_bytes") == _num(b, "model_bytes")
+        elif a.startswith("model forward"):
+            for k in ("n_inner", "act"):
+                assert _num(a, k) == _num(b, k), (k, a, b)
+            assert re.search(r"inner (\w+)", a).group(1) == re.search(r"inner (\w+)", b).group(1)
+            assert re.search(r"deg (\w+)", a).group(1) == re.search(r"deg (\w+)", b).group(1)
+            for k in ("logits2", "agg2", "h12"):  # squared norms: compare the norms
+                assert abs(_num(a, k) ** 0.5 - _num(b, k) ** 0.5) <= 1e-3 * _num(a, k) ** 0.5, (k, a, b)
+        elif a.startswith("model grad"):
+            for k in ("loss", "backward_loss"):
+                assert abs(_num(a, k) - _num(b, k)) <= 1e-3 * abs(_num(a, k)), (k, a, b)
+            for k in ("gw1", "gw2"):
+                assert abs(_num(a, k) ** 0.5 - _num(b, k) ** 0.5) <= 1e-3 * _num(a, k) ** 0.5, (k, a, b)
         else:
-            assert a == b
+            assert a == b, tag
+    assert {"model", "sync", "profile", "pipeline", "lookup2", "design"} <= seen

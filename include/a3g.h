@@ -320,6 +320,15 @@ a3g_status a3g_mean_gradients(int device, const double* const* grads, uint32_t k
 a3g_status a3g_comm_unique_id(uint8_t unique_id[128]);
 a3g_status a3g_comm_create(const uint8_t unique_id[128], int nranks, int rank, int device,
                            a3g_comm** out);
+/* Host-transport communicator: each step the library hands the packed
+ * gradient buffer [n_k dW1 | n_k dW2 | n_k | n_k loss] (f32, `count` values,
+ * pinned host memory) to `fn`, which must replace it in place with the
+ * element-wise sum over all ranks (a gloo / MPI / shared-memory allreduce) and
+ * return 0. The arithmetic around it is the NCCL path's (k_scale_for_sync,
+ * k_sgd); for ranks that cannot share an NCCL communicator (several ranks on
+ * one GPU) and for CPU-side collectives. */
+typedef int (*a3g_allreduce_fn)(float* buf, size_t count, void* user);
+a3g_status a3g_comm_create_host(int nranks, int rank, a3g_allreduce_fn fn, void* user, a3g_comm** out);
 void a3g_comm_destroy(a3g_comm* c);
 
 #ifdef __cplusplus

@@ -138,6 +138,7 @@ _SIGS = {
     "a3g_mean_gradients": (C.c_int, [C.c_int, C.POINTER(f64p), C.c_uint32, C.c_uint64, f64p]),
     "a3g_comm_unique_id": (C.c_int, [u8p]),
     "a3g_comm_create": (C.c_int, [u8p, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
+    "a3g_comm_create_host": (C.c_int, [C.c_int, C.c_int, vp, vp, C.POINTER(vp)]),
     "a3g_comm_destroy": (None, [vp]),
 }
 

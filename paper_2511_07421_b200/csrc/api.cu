@@ -23,6 +23,7 @@ void save_host(const a3g_host_graph* g, const std::string& path);
 a3g_host_graph* load_host(const std::string& path);
 void comm_unique_id(uint8_t out[128]);
 a3g_comm* comm_create(const uint8_t id[128], int nranks, int rank, int device);
+a3g_comm* comm_create_host(int nranks, int rank, a3g_allreduce_fn fn, void* user);
 void comm_destroy(a3g_comm* c);
 }  // namespace a3g
 
@@ -1173,6 +1174,9 @@ a3g_status a3g_comm_unique_id(uint8_t id[128]) {
 }
 a3g_status a3g_comm_create(const uint8_t id[128], int nranks, int rank, int device, a3g_comm** out) {
   return guard([&] { *out = comm_create(id, nranks, rank, device); });
+}
+a3g_status a3g_comm_create_host(int nranks, int rank, a3g_allreduce_fn fn, void* user, a3g_comm** out) {
+  return guard([&] { *out = comm_create_host(nranks, rank, fn, user); });
 }
 void a3g_comm_destroy(a3g_comm* c) { comm_destroy(c); }
 

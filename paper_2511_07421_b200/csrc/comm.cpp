@@ -15,6 +15,12 @@
 struct a3g_comm {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0, device = 0;
+  // host transport (a3g_comm_create_host): the packed buffer goes through a
+  // pinned host copy to the caller's allreduce
+  a3g_allreduce_fn host_fn = nullptr;
+  void* host_user = nullptr;
+  float* h_buf = nullptr;
+  size_t h_cap = 0;
 };
 
 namespace a3g {
@@ -76,13 +82,41 @@ a3g_comm* comm_create(const uint8_t id_bytes[128], int nranks, int rank, int dev
   return c;
 }
 
+a3g_comm* comm_create_host(int nranks, int rank, a3g_allreduce_fn fn, void* user) {
+  if (!fn) raise(A3G_ERR_PARAMETER, "comm: allreduce callback is null");
+  if (nranks < 1 || rank < 0 || rank >= nranks) raise(A3G_ERR_PARAMETER, "comm: bad rank / nranks");
+  auto* c = new a3g_comm;
+  c->nranks = nranks;
+  c->rank = rank;
+  c->host_fn = fn;
+  c->host_user = user;
+  return c;
+}
+
 void comm_destroy(a3g_comm* c) {
   if (!c) return;
   if (c->comm && nccl().destroy) nccl().destroy(c->comm);
+  if (c->h_buf) cudaFreeHost(c->h_buf);
   delete c;
 }
 
 void comm_allreduce_sum(a3g_comm* comm, float* buf, size_t count, cudaStream_t st) {
+  if (comm->host_fn) {
+    // the gradients of this step are complete once the stream reaches here
+    if (count > comm->h_cap) {
+      if (comm->h_buf) cudaFreeHost(comm->h_buf);
+      comm->h_buf = nullptr;
+      A3G_CUDA(cudaMallocHost(&comm->h_buf, count * sizeof(float)));
+      comm->h_cap = count;
+    }
+    A3G_CUDA(cudaMemcpyAsync(comm->h_buf, buf, count * sizeof(float), cudaMemcpyDeviceToHost, st));
+    A3G_CUDA(cudaStreamSynchronize(st));
+    if (comm->host_fn(comm->h_buf, count, comm->host_user) != 0)
+      raise(A3G_ERR_NCCL, "comm: host allreduce callback failed");
+    A3G_CUDA(cudaMemcpyAsync(buf, comm->h_buf, count * sizeof(float), cudaMemcpyHostToDevice, st));
+    A3G_CUDA(cudaStreamSynchronize(st));  // h_buf is reused by the next step
+    return;
+  }
   nccl_check(nccl().all_reduce(buf, buf, count, ncclFloat32, ncclSum, comm->comm, st), "ncclAllReduce");
 }
 

@@ -260,6 +260,29 @@ class Comm:
         check(lib().a3g_comm_create(buf, nranks, rank, device, C.byref(h)))
         self.h = h
 
+    @classmethod
+    def host(cls, nranks: int, rank: int, allreduce) -> "Comm":
+        """Host-transport communicator (a3g_comm_create_host): `allreduce(buf)`
+        receives the packed f32 gradient buffer as a numpy view over pinned
+        host memory and must sum it in place over all ranks (gloo, MPI, ...)."""
+        self = cls.__new__(cls)
+        proto = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_float), C.c_size_t, C.c_void_p)
+
+        def _cb(buf, count, _user):
+            try:
+                allreduce(np.ctypeslib.as_array(buf, shape=(count,)))
+                return 0
+            except Exception:  # noqa: BLE001 -- reported to the library as a failed collective
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._cb = proto(_cb)  # kept alive with the communicator
+        h = vp()
+        check(lib().a3g_comm_create_host(nranks, rank, C.cast(self._cb, vp), None, C.byref(h)))
+        self.h = h
+        return self
+
     @staticmethod
     def unique_id() -> bytes:
         buf = (C.c_uint8 * 128)()

@@ -59,6 +59,11 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-units", type=int, default=3, help="batches in the bounded cpu_baseline sample")
     p.add_argument("--pipeline", type=int, default=None, help="sampling streams (0 = sequential; default: library's)")
+    p.add_argument("--store", choices=["auto", "hbm", "cache", "sharded"], default="auto",
+                   help="feature placement (DESIGN.md 5): hbm = whole table replicated in each GPU's HBM; cache = "
+                        "cached rows in HBM, misses in pinned host memory (zero-copy PCIe); sharded = rank r holds "
+                        "the rows the cache places on device r, peers read over NVLink (cudaIpc), misses on the "
+                        "host. auto: hbm at N=1, sharded at N>1")
     return p.parse_args()
 
 
@@ -159,6 +164,27 @@ def make_graph(cfg_name):
     return G.generate_power_law(n, m, 2.5, 1 if cfg_name in SYNTH else F, BASE_SEED)
 
 
+NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md; 900 nominal)
+
+
+def measure_pcie_h2d_gbs(device: int) -> float:
+    """Pinned host -> device copy bandwidth on this box (best of 5, 256 MiB,
+    CUDA events): the ceiling of the zero-copy miss path."""
+    import torch
+    n = 256 << 20
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device=f"cuda:{device}")
+    best = 0.0
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        d.copy_(h, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        best = max(best, n / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    return best
+
+
 def host_cpu():
     """nproc and the CPU model of this host (printed beside the CPU numbers)."""
     model = "unknown"
@@ -256,9 +282,27 @@ def run_ours(args):
     gen_s = time.time() - t0
     synth = args.config in SYNTH
     Fh = 1 if synth else F  # host feat_dim (the cache's node_cost, cache.cpp:20, scales the same set)
-    cache = CA.build_static_cache(g, CA.CacheConfig(int(frac * n) * Fh * 4, 1), device=local)
+    store = args.store if args.store != "auto" else ("sharded" if world > 1 else "hbm")
+    from paper_2511_07421_b200 import graph as Gm
+    # Appendix B: the ratio is the aggregate cached fraction; per-device volume
+    # ratio*n*F*4/N over N devices caches the same set for every N
+    ndev = world if store == "sharded" else 1
+    cache = CA.build_static_cache(g, CA.CacheConfig(int(frac * n) * Fh * 4 // ndev, ndev), device=local)
+    placement = None
+    if store == "cache":
+        placement = dict(policy=Gm.STORE_CACHE)
+    elif store == "sharded":
+        placement = dict(policy=Gm.STORE_SHARDED, rank=rank, nranks=world)
     tr = T.Trainer(g, cache, T.ModelSpec(F, HIDDEN, CLASSES, learning_rate=LR), fan, max_seeds=B, device=local,
-                   feat_dtype=1 if synth else 0, synth_seed=BASE_SEED if synth else None)
+                   feat_dtype=1 if synth else 0, synth_seed=BASE_SEED if synth else None, placement=placement)
+    if store == "sharded" and world > 1:  # peer shards over NVLink: exchange cudaIpc handles
+        import torch.distributed as dist
+        handles = [None] * world
+        dist.all_gather_object(handles, tr.store.ipc_handle())
+        for r in range(world):
+            if r != rank:
+                tr.store.open_peer(r, handles[r])
+        dist.barrier()
     comm = None
     if world > 1:
         import torch.distributed as dist
@@ -303,10 +347,13 @@ def run_ours(args):
     # the pipelined run's k_agg1 shares the SMs with the concurrent sampling streams.
     barrier()
     tr.set_pipeline(0)
+    tr.set_tier_accounting(True)  # distinct rows per store tier, counted after k_agg1's events
     dev_seq = torch.from_numpy(mine[W + 2 * K:W + 3 * K].astype(np.int32)).cuda()
     _steps_device(tr, dev_seq, gseeds[W + 2 * K:W + 3 * K], args.gamma)
     barrier()
     tm3 = tr.timing()
+    tiers = tr.tier_rows()
+    tr.set_tier_accounting(False)
     tr.set_pipeline(pipe)
     if world > 1:
         import torch.distributed as dist
@@ -325,6 +372,24 @@ def run_ours(args):
     achieved = agg_bytes / (agg_ms * 1e-3) / 1e9 if agg_ms > 0 else 0.0
     pipe_ms = tm["agg_ms"]
     pipe_gbs = tm["agg_bytes"] / (pipe_ms * 1e-3) / 1e9 if pipe_ms > 0 else 0.0
+    # per-resource roofline of the gather: distinct rows per tier
+    # x row bytes per launch, over the same k_agg1 launch time
+    esz = 2 if args.config in SYNTH else 4
+    rows_local = int(tiers[rank if store == "sharded" else 0])
+    rows_host = int(tiers[15])
+    rows_peer = int(tiers[:15].sum()) - rows_local
+    res = {}
+    pcie = measure_pcie_h2d_gbs(local) if rows_host else None
+    for name, rows, peak, kind in (("hbm_local", rows_local, hbm, peak_kind),
+                                   ("nvlink_peer", rows_peer, NVLINK_PEER_GBS, "guide-measured peer copy"),
+                                   ("pcie_host", rows_host, pcie, "measured pinned H2D on this box")):
+        if rows == 0:
+            continue
+        b = rows * F * esz / K
+        a = b / (agg_ms * 1e-3) / 1e9 if agg_ms > 0 else 0.0
+        res[name] = {"bytes_per_launch": b, "achieved": a, "peak": peak, "peak_kind": kind,
+                     "frac": a / peak if peak else None}
+    bound = max(res, key=lambda k: res[k]["frac"] or 0.0) if res else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "agg_traffic.json")
     if os.path.exists(prof):
@@ -337,6 +402,7 @@ def run_ours(args):
         "config": {"workload": args.config, "description": desc, "global_batch": world * B, "batch_per_gpu": B,
                    "fanouts": fan, "gamma": args.gamma, "model": "2-layer mean-GCN (reference trainer), H=16, C=4",
                    "hidden": HIDDEN, "classes": CLASSES, "parallelism": f"dp{world}", "sampling_streams": pipe,
+                   "store": store,
                    "l2": "inputs larger than L2 (CSR %.0f MB + features %.0f MB)" % (
                        g.num_edges * 4 / 1e6, n * F * (2 if args.config in SYNTH else 4) / 1e6),
                    "graph_gen_s": round(gen_s, 1)},
@@ -347,7 +413,11 @@ def run_ours(args):
                      "timed_in": f"{K} sequential-mode steps (k_agg1 alone on the device), CUDA events on the compute stream",
                      "pipelined": {"ms_per_launch": pipe_ms, "achieved": pipe_gbs, "frac": pipe_gbs / hbm,
                                    "note": "same kernel inside the timed pipelined region, sharing SMs/HBM with the concurrent sampling streams"},
-                     "sequential_ms_per_step": tm3["total_ms"] / K},
+                     "sequential_ms_per_step": tm3["total_ms"] / K,
+                     "resources": res, "bound_resource": bound,
+                     "resource_note": "feature rows the gather reads, split by where the store placed them; "
+                                      "achieved = those bytes / the k_agg1 launch time; the path's fraction is "
+                                      "the max over resources"},
         "e2e": {"value": e2e, "unit": "seeds/s", "h2d_bytes_per_step": B * 4, "d2h_bytes_per_step": 8},
         "gpu_launches": int(tm["launches_per_step"]) * K,
         "clocks": clk.summary(),

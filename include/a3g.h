@@ -117,8 +117,10 @@ uint64_t a3g_graph_synth_patched(const a3g_graph* g);
 
 /* --------------------------------------------------------------- store --- */
 /* Places the feature rows of `g` by `policy` (A3G_STORE_*) from host f32
- * features (n x feat_dim, encoded to the graph's feat_dtype) and attaches the
- * store to the graph: every gather of the path then reads through it.
+ * features (n x feat_dim, encoded to the graph's feat_dtype) -- or, with
+ * features == NULL, from the graph's own device table (the synthesized
+ * papers-scale table, which has no host copy) -- and attaches the store to
+ * the graph: every gather of the path then reads through it.
  * device_map: the cache placement (i32[n], -1 = miss, cache.hpp:31); ignored
  * for A3G_STORE_HBM. rank/nranks: this GPU's shard for A3G_STORE_SHARDED. */
 a3g_status a3g_store_create(a3g_graph* g, const float* features, const int32_t* device_map, int policy,
@@ -260,6 +262,14 @@ a3g_status a3g_evaluate_full_graph(a3g_trainer* t, const uint8_t* test_mask, dou
  * t_train} in ms. */
 a3g_status a3g_trainer_profile_step(a3g_trainer* t, const uint32_t* seeds, uint32_t n_seeds, double bias_rate,
                                     int kind, uint64_t rng_seed, double* stage_ms);
+
+/* Per-resource accounting of the gather (bench roofline leg): when on, each
+ * step counts the distinct feature rows the fused gather reads by the tier
+ * they live in (store placement: HBM shard of rank r < 15, NVLink peer,
+ * pinned host = 15; no store: tier 0), after the gather's timing events.
+ * a3g_trainer_tier_rows: u64[16] summed over the last a3g_train_steps call. */
+a3g_status a3g_trainer_set_tier_accounting(a3g_trainer* t, int on);
+a3g_status a3g_trainer_tier_rows(a3g_trainer* t, uint64_t* rows);
 
 /* Debug/parity copy-out of the last step (host f64 buffers; NULL skips):
  * gradients (F*H, H*C), and ForwardResult arrays (trainer.hpp:49-60). */

@@ -812,6 +812,8 @@ void a3g_trainer_destroy(a3g_trainer* tr) {
   dfree(t.d_part);
   dfree(t.d_hpart);
   dfree(t.d_gather);
+  dfree(t.d_tier_seen);
+  dfree(t.d_tier_rows);
   dfree(t.d_agg_bytes);
   dfree(t.d_losses);
   dfree(t.d_stats);
@@ -924,6 +926,7 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
     for (cudaEvent_t e : t.ev_agg) cudaEventDestroy(e);
     t.ev_agg.clear();
     A3G_CUDA(cudaMemsetAsync(t.d_agg_bytes, 0, 16, t.s_comp));
+    if (t.d_tier_rows) A3G_CUDA(cudaMemsetAsync(t.d_tier_rows, 0, kMaxTiers * 8, t.s_comp));
     A3G_CUDA(cudaMemsetAsync(t.d_stats, 0, static_cast<size_t>(K) * A3G_STEP_STATS * 8, t.s_comp));
     A3G_CUDA(cudaEventRecord(t.ev_t0, t.s_comp));
     A3G_CUDA(cudaStreamWaitEvent(t.s_samp, t.ev_t0, 0));
@@ -1142,6 +1145,33 @@ a3g_status a3g_trainer_profile_step(a3g_trainer* tr, const uint32_t* seeds, uint
     A3G_CUDA(cudaEventElapsedTime(&ms[2], ev[3], ev[4]));
     for (auto& e : ev) cudaEventDestroy(e);
     for (int i = 0; i < 3; ++i) stage_ms[i] = ms[i];
+  });
+}
+
+a3g_status a3g_trainer_set_tier_accounting(a3g_trainer* tr, int on) {
+  return guard([&] {
+    TrainerState& t = tr->st;
+    A3G_CUDA(cudaSetDevice(t.g->device));
+    A3G_CUDA(cudaStreamSynchronize(t.s_comp));
+    if (on && !t.d_tier_seen) {
+      const uint64_t words = (t.g->n + 31) / 32;
+      t.d_tier_seen = dalloc<uint32_t>(words);
+      A3G_CUDA(cudaMemset(t.d_tier_seen, 0, words * 4));
+      t.d_tier_rows = dalloc<unsigned long long>(kMaxTiers);
+      A3G_CUDA(cudaMemset(t.d_tier_rows, 0, kMaxTiers * 8));
+    }
+    t.tier_acct = on != 0;
+  });
+}
+
+a3g_status a3g_trainer_tier_rows(a3g_trainer* tr, uint64_t* rows) {
+  return guard([&] {
+    TrainerState& t = tr->st;
+    A3G_CUDA(cudaSetDevice(t.g->device));
+    A3G_CUDA(cudaStreamSynchronize(t.s_comp));
+    unsigned long long h[kMaxTiers] = {};
+    if (t.d_tier_rows) A3G_CUDA(cudaMemcpy(h, t.d_tier_rows, sizeof h, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < kMaxTiers; ++i) rows[i] = h[i];
   });
 }
 

@@ -71,6 +71,44 @@ void* upload_rows(const float* features, uint32_t F, uint32_t row_bytes, int dty
   return d;
 }
 
+// Rows `ids` of the graph's own device table (a synthesized papers-scale
+// table has no host copy): one warp per row, 16-byte chunks.
+__global__ void k_copy_rows(const uint8_t* __restrict__ src, uint32_t rb, const uint32_t* __restrict__ ids,
+                            uint64_t count, uint8_t* __restrict__ dst) {
+  const uint64_t w = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31, q16 = rb / 16;
+  for (uint64_t i = w; i < count; i += nw) {
+    const uint4* s = reinterpret_cast<const uint4*>(src + static_cast<uint64_t>(ids[i]) * rb);
+    uint4* d = reinterpret_cast<uint4*>(dst + i * rb);
+    for (uint32_t q = lane; q < q16; q += 32) d[q] = s[q];
+  }
+}
+
+// Copies rows `ids` (in order) of g's device table to dst (device, or mapped
+// pinned host through device slabs).
+void copy_device_rows(const a3g_graph* g, const std::vector<uint32_t>& ids, uint8_t* dst, bool dst_host) {
+  const uint32_t rb = g->view.row_bytes;
+  const uint64_t slab = std::max<uint64_t>(1, (256ull << 20) / rb);
+  uint32_t* d_ids = nullptr;
+  uint8_t* d_stage = nullptr;
+  A3G_CUDA(cudaMalloc(&d_ids, std::min<uint64_t>(slab, std::max<size_t>(ids.size(), 1)) * 4));
+  if (dst_host) A3G_CUDA(cudaMalloc(&d_stage, std::min<uint64_t>(slab, std::max<size_t>(ids.size(), 1)) * rb));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+  for (uint64_t i0 = 0; i0 < ids.size(); i0 += slab) {
+    const uint64_t cnt = std::min<uint64_t>(slab, ids.size() - i0);
+    A3G_CUDA(cudaMemcpy(d_ids, ids.data() + i0, cnt * 4, cudaMemcpyHostToDevice));
+    uint8_t* out = dst_host ? d_stage : dst + i0 * rb;
+    k_copy_rows<<<sms * 8, 256>>>(static_cast<const uint8_t*>(g->d_feat), rb, d_ids, cnt, out);
+    A3G_LAUNCH_CHECK("k_copy_rows");
+    if (dst_host) A3G_CUDA(cudaMemcpy(dst + i0 * rb, d_stage, cnt * rb, cudaMemcpyDeviceToHost));
+  }
+  A3G_CUDA(cudaDeviceSynchronize());
+  cudaFree(d_ids);
+  if (d_stage) cudaFree(d_stage);
+}
+
 void refresh_view(a3g_store* s) {
   StoreView& v = s->g->view;
   v.base[s->rank] = static_cast<const uint8_t*>(s->d_local);
@@ -93,7 +131,11 @@ extern "C" {
 a3g_status a3g_store_create(a3g_graph* g, const float* features, const int32_t* device_map, int policy,
                             int rank, int nranks, a3g_store** out) {
   return guard([&] {
-    if (!g || !features) raise(A3G_ERR_PARAMETER, "store: graph and host features are required");
+    if (!g) raise(A3G_ERR_PARAMETER, "store: graph is required");
+    // features == NULL: the rows come from the graph's own device table
+    // (a3g_graph_synthesize_features / a3g_graph_create with features)
+    if (!features && (!g->d_feat || !g->has_features || g->store))
+      raise(A3G_ERR_PARAMETER, "store: host features, or a graph holding its own device table, are required");
     if (policy < A3G_STORE_HBM || policy > A3G_STORE_SHARDED) raise(A3G_ERR_PARAMETER, "store: unknown policy");
     if (nranks < 1 || nranks >= static_cast<int>(kTierHost) || rank < 0 || rank >= nranks)
       raise(A3G_ERR_PARAMETER, "store: rank/nranks out of range (at most 15 devices)");
@@ -138,13 +180,21 @@ a3g_status a3g_store_create(a3g_graph* g, const float* features, const int32_t* 
         }
       }
       s->n_local = local.size();
-      s->d_local = upload_rows(features, g->F, rb, g->feat_dtype, local);
+      if (features) {
+        s->d_local = upload_rows(features, g->F, rb, g->feat_dtype, local);
+      } else {
+        A3G_CUDA(cudaMalloc(&s->d_local, std::max<size_t>(1, local.size() * static_cast<size_t>(rb))));
+        copy_device_rows(g, local, static_cast<uint8_t*>(s->d_local), false);
+      }
       if (!host.empty()) {
         s->n_host = host.size();
         A3G_CUDA(cudaHostAlloc(&s->h_host, host.size() * static_cast<size_t>(rb),
                                cudaHostAllocMapped | cudaHostAllocPortable));
-        encode_rows(features, g->F, rb, g->feat_dtype, host.data(), host.size(),
-                    static_cast<uint8_t*>(s->h_host));
+        if (features)
+          encode_rows(features, g->F, rb, g->feat_dtype, host.data(), host.size(),
+                      static_cast<uint8_t*>(s->h_host));
+        else
+          copy_device_rows(g, host, static_cast<uint8_t*>(s->h_host), true);
       }
       if (!loc.empty()) {
         A3G_CUDA(cudaMalloc(&s->d_loc, n * 4));

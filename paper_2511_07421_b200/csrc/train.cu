@@ -718,6 +718,28 @@ bool launch_agg(TrainerState& t, AggArgs aa, uint32_t chunks, cudaStream_t st) {
 
 }  // namespace
 
+// Per-resource accounting of the gather (a3g_trainer_set_tier_accounting):
+// the distinct feature rows k_agg1 reads -- every layer-1 source of an inner
+// row, or the row itself on the self-fallback -- by the tier they live in
+// (StoreView loc: HBM shard r < 15, pinned host 15; identity layout: 0).
+// Off by default; the bench's roofline leg turns it on, and it runs after
+// k_agg1's timing events.
+__global__ void k_tier_rows(const uint32_t* unique, const int32_t* inv1, const uint32_t* cnt1, const uint32_t* S1,
+                            uint32_t f1, const uint32_t* n_inner_p, int has_layer1, const uint32_t* loc,
+                            uint32_t* seen, unsigned long long* tier_rows) {
+  const uint32_t n_inner = *n_inner_p;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_inner; r += gridDim.x * blockDim.x) {
+    const int32_t k = has_layer1 ? inv1[r] : -1;
+    const uint32_t c = k >= 0 ? cnt1[k] : 0u;
+    for (uint32_t t = 0; t < (c ? c : 1u); ++t) {
+      const uint32_t v = c ? S1[static_cast<uint64_t>(k) * f1 + t] : unique[r];
+      const uint32_t bit = 1u << (v & 31);
+      if (!(atomicOr(seen + (v >> 5), bit) & bit))
+        atomicAdd(tier_rows + (loc ? (__ldg(loc + v) >> kLocShift) : 0u), 1ull);
+    }
+  }
+}
+
 // nccl glue lives in comm.cpp
 void comm_allreduce_sum(a3g_comm* comm, float* buf, size_t count, cudaStream_t st);
 
@@ -772,6 +794,12 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
     A3G_CUDA(cudaEventRecord(e1, st));
     t.ev_agg.push_back(e0);
     t.ev_agg.push_back(e1);
+  }
+  if (t.tier_acct) {
+    k_tier_rows<<<t.sm_count * 2, 256, 0, st>>>(s.d_unique, s.d_inv1, aa.cnt1, aa.S1, aa.f1, aa.n_inner,
+                                                aa.has_layer1, g->view.loc, t.d_tier_seen, t.d_tier_rows);
+    A3G_LAUNCH_DONE("k_tier_rows", st);
+    A3G_CUDA(cudaMemsetAsync(t.d_tier_seen, 0, (g->n + 31) / 32 * 4, st));
   }
   if (!fused) launch_h1_tc(t, t.d_agg_inner, aa.n_inner, t.d_h1, st);
   // ---- outer aggregation, logits, loss, dlogits, scatter to dh1

@@ -67,6 +67,9 @@ struct TrainerState {
   uint32_t h1_split_cap = 1;
   bool h1_split_used = false;  // the last step's h1 GEMM ran split-K (+ k_h1_reduce)
   float* d_gather = nullptr;   // a3g_trainer_profile_step: the unique rows of a retrieve_features stage
+  bool tier_acct = false;                    // a3g_trainer_set_tier_accounting
+  uint32_t* d_tier_seen = nullptr;           // n-bit "row already counted" map (cleared per step)
+  unsigned long long* d_tier_rows = nullptr; // [kMaxTiers] distinct rows gathered per tier
   uint64_t gather_cap = 0;
 };
 

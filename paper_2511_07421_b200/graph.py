@@ -60,10 +60,11 @@ class Store:
 
     def __init__(self, dg: DeviceGraph, features: np.ndarray, device_map=None, policy: int = STORE_HBM,
                  rank: int = 0, nranks: int = 1):
-        f = np.ascontiguousarray(features, dtype=np.float32)
+        # features None: the rows come from the graph's own device table (synthesized)
+        f = None if features is None else np.ascontiguousarray(features, dtype=np.float32)
         dm = None if device_map is None else np.ascontiguousarray(device_map, dtype=np.int32)
         h = vp()
-        check(lib().a3g_store_create(dg.h, ptr(f, f32p), None if dm is None else ptr(dm, i32p), policy, rank,
+        check(lib().a3g_store_create(dg.h, None if f is None else ptr(f, f32p), None if dm is None else ptr(dm, i32p), policy, rank,
                                      nranks, C.byref(h)))
         self.h, self.dg, self.policy, self.rank, self.nranks = h, dg, policy, rank, nranks
 

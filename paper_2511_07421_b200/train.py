@@ -121,13 +121,16 @@ class Trainer:
         if synth_seed is not None:
             dg = DeviceGraph(g, device, feat_dtype, upload_features=False)
             check(lib().a3g_graph_synthesize_features(dg.h, spec.feat_dim, feat_dtype, int(synth_seed)))
+            if placement is not None:  # tiered store placed from the synthesized device table
+                self.store = Store(dg, None, cache.device_map, placement.get("policy", STORE_HBM),
+                                   placement.get("rank", 0), placement.get("nranks", 1))
             from .cache import _DeviceCache
             hc = vp()
             dm = np.ascontiguousarray(cache.device_map, dtype=np.int32)
             check(lib().a3g_cache_from_map(dg.h, ptr(dm, i32p), cache.num_devices, C.byref(hc)))
             dc = _DeviceCache(hc)
             ch = dc.h
-            keep = [dc, dg]
+            keep = [dc, self.store, dg]
         elif placement is None:
             dg = g.device(device, feat_dtype)
             ch = cache.device(g, device, feat_dtype)
@@ -244,6 +247,16 @@ class Trainer:
         n = ni.value
         return dict(n_inner=n, logits=logits, agg_inner=agg_inner[:n * F].reshape(n, F),
                     h1=h1[:n * H].reshape(n, H), agg_outer=agg_outer)
+
+    def set_tier_accounting(self, on: bool):
+        check(lib().a3g_trainer_set_tier_accounting(self.h, 1 if on else 0))
+
+    def tier_rows(self) -> np.ndarray:
+        """u64[16]: distinct rows the fused gather read per store tier over the
+        last steps call (tier r < 15: HBM shard of rank r; 15: pinned host)."""
+        out = np.zeros(16, dtype=np.uint64)
+        check(lib().a3g_trainer_tier_rows(self.h, ptr(out, u64p)))
+        return out
 
     def timing(self):
         t, a, b, l = C.c_double(), C.c_double(), C.c_double(), C.c_uint64()

@@ -12,6 +12,7 @@ import os
 import shutil
 import subprocess
 import sys
+import sysconfig
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -95,7 +96,7 @@ DROPIN_LIBS = {
     # sync_gradients / train / evaluate_full_graph) and the executor
     # (execute_pipeline / profile_stage_costs) on the device
     "liba3gnn_b200.so": ["registry.cpp", "sampler_b200.cpp", "cache_b200.cpp", "trainer_b200.cpp",
-                         "pipeline_b200.cpp"],
+                         "pipeline_b200.cpp", "evaluator_b200.cpp"],
 }
 
 
@@ -132,5 +133,22 @@ def build_dropin(ref_lib_dir: str | None = None, force: bool = False) -> list:
             if r.returncode != 0:
                 sys.stderr.write(r.stdout + r.stderr)
                 raise RuntimeError("dropin_check build failed")
+            built.append(out)
+        # the device Evaluator's check: reference alone / linked with the drop-in
+        nj = os.path.join(sysconfig.get_paths()["purelib"], "include", "cudnn_frontend", "thirdparty")
+        for name, extra in (("tuner_check", []),
+                            ("tuner_check_b200", ["-DA3G_DEVICE_EVAL", "-I", DROPIN, "-L", DROPIN_OUT, "-la3gnn_b200",
+                                                  "-Wl,-rpath,$ORIGIN"])):
+            out = os.path.join(DROPIN_OUT, name)
+            if not force and os.path.exists(out) and os.path.getmtime(out) >= newest:
+                continue
+            rel = os.path.relpath(ref_lib_dir, DROPIN_OUT)
+            cmd = [cxx, "-std=c++20", "-O2", "-I", REF_INCLUDE, "-I", nj, "-o", out,
+                   os.path.join(DROPIN, "tuner_check.cpp")] + extra + [
+                "-L", ref_lib_dir, "-lref_a3gnn", f"-Wl,-rpath,$ORIGIN/{rel}", "-lpthread"]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"{name} build failed")
             built.append(out)
     return built

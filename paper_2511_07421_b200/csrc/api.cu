@@ -136,6 +136,8 @@ void sampler_alloc(SamplerState& s, a3g_graph* g, a3g_cache* c, uint32_t max_see
   A3G_CUDA(cudaMallocHost(&s.h_seeds, max_seeds * sizeof(uint32_t)));
   A3G_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
   s.own_stream = true;
+  A3G_CUDA(cudaEventCreateWithFlags(&s.ev_fork, cudaEventDisableTiming));
+  A3G_CUDA(cudaEventCreateWithFlags(&s.ev_join, cudaEventDisableTiming));
 }
 
 void sampler_free(SamplerState& s) {
@@ -172,6 +174,8 @@ void sampler_free(SamplerState& s) {
   if (s.h_ctr) cudaFreeHost(s.h_ctr);
   if (s.h_seeds) cudaFreeHost(s.h_seeds);
   if (s.own_stream && s.stream) cudaStreamDestroy(s.stream);
+  if (s.ev_fork) cudaEventDestroy(s.ev_fork);
+  if (s.ev_join) cudaEventDestroy(s.ev_join);
 }
 
 // sample_khop validation in the reference's order (sampler.cpp:91-94, :110,

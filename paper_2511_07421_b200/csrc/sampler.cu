@@ -1900,11 +1900,16 @@ static uint64_t lane_min_rows(bool dense) {
   return dense ? 8192ull : 32768ull;
 }
 
+// aux / ev_fork / ev_join: with A3G_SPLIT_CLS (long items to the lane-group
+// kernel) and A3G_SPLIT_FORK=1, the lane-group launch forks onto the arena's
+// auxiliary stream so it runs beside the lane kernel.
 template <int WM>
-void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_count, cudaStream_t st) {
+void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_count, cudaStream_t st,
+                          cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join) {
   k_classify<WM><<<sm_count * 2, 256, 0, st>>>(sa);
   A3G_LAUNCH_DONE("k_classify", st);
   if (sa.f <= 32) {
+    bool fork = false;
     static std::atomic<uint64_t> attr_done{0};
     smem_attr_once(attr_done, reinterpret_cast<const void*>(k_hub_merge<WM>), kMergeSmem);
     {
@@ -1934,25 +1939,34 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
       }();
       SampleArgs sl = sa;
       sl.split_cls = lane ? split : -1;
+      static const bool fork_env = std::getenv("A3G_SPLIT_FORK") != nullptr;
+      fork = lane && split >= 0 && fork_env && aux && aux != st && ev_fork && ev_join;
+      cudaStream_t gst = st;
+      if (fork) {
+        A3G_CUDA(cudaEventRecord(ev_fork, st));
+        A3G_CUDA(cudaStreamWaitEvent(aux, ev_fork, 0));
+        gst = aux;
+      }
       if (!lane || split >= 0) {  // lane groups: the whole layer, or its long items
         if (WM == 2 && sa.kind != A3G_SAMPLER_UNIFORM) {
           if (sa.f <= 8)
-            k_stream_grp_mixed<8><<<grp_grid(8), kGrpThreads, 0, st>>>(sl, lists, sa.cls_count);
+            k_stream_grp_mixed<8><<<grp_grid(8), kGrpThreads, 0, gst>>>(sl, lists, sa.cls_count);
           else if (sa.f <= 16)
-            k_stream_grp_mixed<16><<<grp_grid(16), kGrpThreads, 0, st>>>(sl, lists, sa.cls_count);
+            k_stream_grp_mixed<16><<<grp_grid(16), kGrpThreads, 0, gst>>>(sl, lists, sa.cls_count);
           else
-            k_stream_grp_mixed<32><<<grp_grid(32), kGrpThreads, 0, st>>>(sl, lists, sa.cls_count);
-          A3G_LAUNCH_DONE("k_stream_grp_mixed", st);
+            k_stream_grp_mixed<32><<<grp_grid(32), kGrpThreads, 0, gst>>>(sl, lists, sa.cls_count);
+          A3G_LAUNCH_DONE("k_stream_grp_mixed", gst);
         } else {
           if (sa.f <= 8)
-            k_stream_grp<W, 8><<<grp_grid(8), kGrpThreads, 0, st>>>(sl, lists, sa.cls_count);
+            k_stream_grp<W, 8><<<grp_grid(8), kGrpThreads, 0, gst>>>(sl, lists, sa.cls_count);
           else if (sa.f <= 16)
-            k_stream_grp<W, 16><<<grp_grid(16), kGrpThreads, 0, st>>>(sl, lists, sa.cls_count);
+            k_stream_grp<W, 16><<<grp_grid(16), kGrpThreads, 0, gst>>>(sl, lists, sa.cls_count);
           else
-            k_stream_grp<W, 32><<<grp_grid(32), kGrpThreads, 0, st>>>(sl, lists, sa.cls_count);
-          A3G_LAUNCH_DONE("k_stream_grp", st);
+            k_stream_grp<W, 32><<<grp_grid(32), kGrpThreads, 0, gst>>>(sl, lists, sa.cls_count);
+          A3G_LAUNCH_DONE("k_stream_grp", gst);
         }
       }
+      if (fork) A3G_CUDA(cudaEventRecord(ev_join, aux));
       if (lane) {  // register reservoirs sized to the fanout (exact sizes for the common 5 / 10)
         if (WM == 2) {
           if (sa.f == 5)
@@ -1981,6 +1995,7 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
       const char* e = std::getenv("A3G_MERGE_CTAS4");
       return e ? std::max(1, std::atoi(e)) : 2;  // r01 sweep: 2 (74 CTAs) beat 8 and 4 in the pipeline
     }();
+    if (fork) A3G_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
     k_hub_merge<WM><<<std::max(1, sm_count * merge_ctas_q / 4), kMergeThreads, kMergeSmem, st>>>(sa);
     A3G_LAUNCH_DONE("k_hub_merge", st);
   }
@@ -2079,11 +2094,11 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
     sa.kind = kind;
     sa.wmode = wmode;
     if (wmode == 1)
-      launch_layer_kernels<1>(sa, la.cap_rows, s.sm_count, st);
+      launch_layer_kernels<1>(sa, la.cap_rows, s.sm_count, st, s.stream, s.ev_fork, s.ev_join);
     else if (wmode == 2)
-      launch_layer_kernels<2>(sa, la.cap_rows, s.sm_count, st);
+      launch_layer_kernels<2>(sa, la.cap_rows, s.sm_count, st, s.stream, s.ev_fork, s.ev_join);
     else
-      launch_layer_kernels<0>(sa, la.cap_rows, s.sm_count, st);
+      launch_layer_kernels<0>(sa, la.cap_rows, s.sm_count, st, s.stream, s.ev_fork, s.ev_join);
     FinArgs fa{};
     fa.S = la.S;
     fa.cnt = la.cnt;

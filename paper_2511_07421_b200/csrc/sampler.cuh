@@ -68,6 +68,7 @@ struct SamplerState {
   uint32_t gtag = 0;               // interner tag (per batch)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // fork of a layer's lane-group launch onto `stream`
   // last batch parameters
   uint32_t last_n_seeds = 0;
   bool check_seeds = false;  // seeds came from device memory: range-check them on the device

@@ -56,6 +56,8 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", choices=list(CONFIGS), default="c2")
     p.add_argument("--gamma", type=float, default=8.0)
+    p.add_argument("--hidden", type=int, default=HIDDEN,
+                   help="hidden width H (reference default 16, config.hpp:51; > 16 puts h1 and dW1 on tcgen05)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-units", type=int, default=3, help="batches in the bounded cpu_baseline sample")
     p.add_argument("--pipeline", type=int, default=None, help="sampling streams (0 = sequential; default: library's)")
@@ -72,6 +74,14 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def measured_tflops():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return float(json.load(f).get("bf16_tflops", 1590.0))
+    return 1590.0
 
 
 def measured_peaks():
@@ -203,7 +213,7 @@ def host_cpu():
     return n, model
 
 
-def cpu_reference_run(rg, cfg_name, gamma, units, mode, producers, warmup=1):
+def cpu_reference_run(rg, cfg_name, gamma, units, mode, producers, warmup=1, hidden=HIDDEN):
     """Time the reference's own CPU path (oracle/_ref: the unmodified reference
     compiled in place) on `units` batches of the workload after `warmup`
     untimed ones, scheduled as the executor's `mode` (0 sequential, 1 pmode1,
@@ -213,7 +223,7 @@ def cpu_reference_run(rg, cfg_name, gamma, units, mode, producers, warmup=1):
     n, m, F, fan, B, frac, _ = CONFIGS[cfg_name]
     ref = oracle.RefLib()
     dm = ref.build_static_cache(rg, int(frac * n) * F * 4, 1)
-    secs, seeds = ref.bench_steps(rg, dm, fan, gamma, BASE_SEED, B, HIDDEN, CLASSES, LR, units, producers, 8,
+    secs, seeds = ref.bench_steps(rg, dm, fan, gamma, BASE_SEED, B, hidden, CLASSES, LR, units, producers, 8,
                                   warmup=warmup, mode=mode)
     return dict(seconds=secs, seeds=seeds, seeds_per_s=seeds / secs if secs > 0 else 0.0, units=units,
                 mode=["sequential", "pmode1", "pmode2"][mode], threads=1 if mode == 0 else producers + 1)
@@ -233,7 +243,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "dtype": "f64", "data": "synthetic (the reference's generate_power_law, seed 1)", "vs_baseline": None,
             "config": {"workload": args.config, "description": desc, "global_batch": B, "fanouts": fan,
-                       "gamma": args.gamma, "hidden": HIDDEN, "classes": CLASSES}}
+                       "gamma": args.gamma, "hidden": args.hidden, "classes": CLASSES}}
     if not oracle.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref (reference compiled in place) not built"}))
         return 0
@@ -248,10 +258,10 @@ def run_reference(args):
     producers = max(1, cores - 1)
     K, W = max(1, args.steps), max(0, args.warmup)
     # headline: the executor's pmode1 schedule, nproc-1 producers + the trainer thread, queue 8
-    r1 = cpu_reference_run(rg, args.config, args.gamma, K, 1, producers, warmup=W)
+    r1 = cpu_reference_run(rg, args.config, args.gamma, K, 1, producers, warmup=W, hidden=args.hidden)
     # beside it (bounded): pmode2 and the 1-thread sequential train() loop
-    r2 = cpu_reference_run(rg, args.config, args.gamma, max(1, min(K, 8)), 2, producers, warmup=1)
-    r0 = cpu_reference_run(rg, args.config, args.gamma, max(1, min(K, 3)), 0, 0, warmup=1)
+    r2 = cpu_reference_run(rg, args.config, args.gamma, max(1, min(K, 8)), 2, producers, warmup=1, hidden=args.hidden)
+    r0 = cpu_reference_run(rg, args.config, args.gamma, max(1, min(K, 3)), 0, 0, warmup=1, hidden=args.hidden)
     v = r1["seeds_per_s"]
     base.update({"value": v, "ms_per_step": 1e3 * r1["seconds"] / max(1, r1["units"]),
                  "cpu_baseline": {"value": v, "unit": "seeds/s", "cores": cores, "cpu_model": cpu_model,
@@ -293,7 +303,8 @@ def run_ours(args):
         placement = dict(policy=Gm.STORE_CACHE)
     elif store == "sharded":
         placement = dict(policy=Gm.STORE_SHARDED, rank=rank, nranks=world)
-    tr = T.Trainer(g, cache, T.ModelSpec(F, HIDDEN, CLASSES, learning_rate=LR), fan, max_seeds=B, device=local,
+    H = args.hidden
+    tr = T.Trainer(g, cache, T.ModelSpec(F, H, CLASSES, learning_rate=LR), fan, max_seeds=B, device=local,
                    feat_dtype=1 if synth else 0, synth_seed=BASE_SEED if synth else None, placement=placement)
     if store == "sharded" and world > 1:  # peer shards over NVLink: exchange cudaIpc handles
         import torch.distributed as dist
@@ -352,6 +363,8 @@ def run_ours(args):
     _steps_device(tr, dev_seq, gseeds[W + 2 * K:W + 3 * K], args.gamma)
     barrier()
     tm3 = tr.timing()
+    gt3 = tr.gemm_timing()
+    st3 = tr.step_stats(K)
     tiers = tr.tier_rows()
     tr.set_tier_accounting(False)
     tr.set_pipeline(pipe)
@@ -390,6 +403,21 @@ def run_ours(args):
         res[name] = {"bytes_per_launch": b, "achieved": a, "peak": peak, "peak_kind": kind,
                      "frac": a / peak if peak else None}
     bound = max(res, key=lambda k: res[k]["frac"] or 0.0) if res else None
+    # the dense update on the tensor cores (H > 16): algorithmic flops of
+    # h1 = agg W1 and dW1 = agg^T G (2 n_inner F H each) over their launch time
+    tensor = None
+    if gt3["launches"]:
+        n_inner = float(st3[:, T.STAT_INNER].mean())
+        fl = 2 * 2.0 * n_inner * F * H
+        ms = gt3["h1_ms"] + gt3["dw1_ms"]
+        tf = fl / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+        peak_tf = measured_tflops()
+        tensor = {"kernels": "k_h1_tc + k_dw1_tc (tcgen05.mma kind::f16, fp32 TMEM accumulators)", "bound": "tensor",
+                  "flops_per_step": fl, "ms_per_step": ms, "h1_ms": gt3["h1_ms"], "dw1_ms": gt3["dw1_ms"],
+                  "achieved": tf, "peak": peak_tf, "unit": "TFLOP/s", "frac": tf / peak_tf if peak_tf else None,
+                  "mma_flops_issued_per_step": 6 * fl,
+                  "note": "fp32 operands as 3 bf16 terms, 6 MMAs per product (fp32-class accuracy); the issued "
+                          "tensor work is 6x the algorithmic flops"}
     traffic = None
     prof = os.path.join(ROOT, "profiles", "agg_traffic.json")
     if os.path.exists(prof):
@@ -400,8 +428,8 @@ def run_ours(args):
         "warmup": W, "ms_per_step": dev_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16" if args.config in SYNTH else "f32", "data": "synthetic (generate_power_law, bit-identical to the reference generator)",
         "config": {"workload": args.config, "description": desc, "global_batch": world * B, "batch_per_gpu": B,
-                   "fanouts": fan, "gamma": args.gamma, "model": "2-layer mean-GCN (reference trainer), H=16, C=4",
-                   "hidden": HIDDEN, "classes": CLASSES, "parallelism": f"dp{world}", "sampling_streams": pipe,
+                   "fanouts": fan, "gamma": args.gamma, "model": f"2-layer mean-GCN (reference trainer), H={H}, C=4",
+                   "hidden": H, "classes": CLASSES, "parallelism": f"dp{world}", "sampling_streams": pipe,
                    "store": store,
                    "l2": "inputs larger than L2 (CSR %.0f MB + features %.0f MB)" % (
                        g.num_edges * 4 / 1e6, n * F * (2 if args.config in SYNTH else 4) / 1e6),
@@ -419,6 +447,7 @@ def run_ours(args):
                                       "achieved = those bytes / the k_agg1 launch time; the path's fraction is "
                                       "the max over resources"},
         "e2e": {"value": e2e, "unit": "seeds/s", "h2d_bytes_per_step": B * 4, "d2h_bytes_per_step": 8},
+        "tensor_roofline": tensor,
         "gpu_launches": int(tm["launches_per_step"]) * K,
         "clocks": clk.summary(),
         "loss_first_last": [float(losses[0]), float(losses_e2e[-1])],
@@ -435,7 +464,7 @@ def run_ours(args):
             rg = oracle.RefLib().load(path)
             os.remove(path)
             cores, cpu_model = host_cpu()
-            r = cpu_reference_run(rg, args.config, args.gamma, args.cpu_units, 0, 0, warmup=1)
+            r = cpu_reference_run(rg, args.config, args.gamma, args.cpu_units, 0, 0, warmup=1, hidden=args.hidden)
             out["cpu_baseline"] = {"value": r["seeds_per_s"], "unit": "seeds/s", "cores": 1, "kind": "reference",
                                    "cpu_model": cpu_model, "host_nproc": cores,
                                    "sample": f"{args.cpu_units} batches of epoch 0 (B={B}) after 1 untimed, "

@@ -324,6 +324,12 @@ a3g_status a3g_sgd_step(int device, double* w, const double* g, uint64_t n, uint
  * g_{k-1}) * (1/k), summed in list order. ParameterError when k == 0. */
 a3g_status a3g_mean_gradients(int device, const double* const* grads, uint32_t k, uint64_t n, double* out);
 
+/* Average per-launch ms of the tcgen05 dense update in the last a3g_train_steps
+ * call (CUDA events on the compute stream): h1 = ReLU(agg . W1) and dW1 =
+ * agg^T . G, when they ran on the tensor cores (H > 16, or A3G_TC_GEMMS=1);
+ * launches = number of timed h1 GEMMs (0: the fused / CUDA-core path ran). */
+a3g_status a3g_trainer_gemm_timing(a3g_trainer* t, double* h1_ms, double* dw1_ms, uint64_t* launches);
+
 /* ---------------------------------------------------------------- comm --- */
 /* NCCL communicator for data-parallel gradient sync (trainer.cpp:213-229 ->
  * allreduce(sum) of n_k-weighted gradients). unique_id is 128 opaque bytes. */

@@ -130,6 +130,7 @@ _SIGS = {
     "a3g_trainer_tier_rows": (C.c_int, [vp, u64p]),
     "a3g_trainer_profile_step": (C.c_int, [vp, u32p, C.c_uint32, C.c_double, C.c_int, C.c_uint64, f64p]),
     "a3g_trainer_timing": (C.c_int, [vp, f64p, f64p, f64p, u64p]),
+    "a3g_trainer_gemm_timing": (C.c_int, [vp, f64p, f64p, u64p]),
     "a3g_batch_model_create": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(vp)]),
     "a3g_batch_model_destroy": (None, [vp]),
     "a3g_batch_model_load": (C.c_int, [vp, C.c_uint64, C.c_uint64, C.c_uint32, u64p, C.POINTER(u32p),

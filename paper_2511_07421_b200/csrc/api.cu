@@ -709,7 +709,9 @@ a3g_status a3g_trainer_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds, co
                               a3g_trainer** out) {
   return guard([&] {
     if (g->F < 1 || H < 1 || C < 1) raise(A3G_ERR_PARAMETER, "init_model: dims must be >= 1");
-    if (H > 32 || C > 32) raise(A3G_ERR_PARAMETER, "trainer: hidden_dim and num_classes must be <= 32");
+    // H <= 16: h1 fused into the gather; 16 < H <= 32: dW1 on the CUDA cores;
+    // up to 256: both products on tcgen05 (N = H, TMEM accumulators)
+    if (H > 256 || C > 32) raise(A3G_ERR_PARAMETER, "trainer: hidden_dim must be <= 256 and num_classes <= 32");
     if (!g->has_features) raise(A3G_ERR_PARAMETER, "trainer: graph has no features");
     auto* tr = new a3g_trainer;
     TrainerState& t = tr->st;
@@ -824,6 +826,8 @@ void a3g_trainer_destroy(a3g_trainer* tr) {
   dfree(t.d_seed_buf);
   if (t.h_seed_stage) cudaFreeHost(t.h_seed_stage);
   if (t.h_losses) cudaFreeHost(t.h_losses);
+  for (cudaEvent_t e : t.ev_h1) cudaEventDestroy(e);
+  for (cudaEvent_t e : t.ev_dw1) cudaEventDestroy(e);
   for (cudaEvent_t e : t.ev_agg) cudaEventDestroy(e);
   for (int i = 0; i < TrainerState::kArenas; ++i) {
     if (t.ev_sampled[i]) cudaEventDestroy(t.ev_sampled[i]);
@@ -929,6 +933,10 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
     }
     for (cudaEvent_t e : t.ev_agg) cudaEventDestroy(e);
     t.ev_agg.clear();
+    for (cudaEvent_t e : t.ev_h1) cudaEventDestroy(e);
+    for (cudaEvent_t e : t.ev_dw1) cudaEventDestroy(e);
+    t.ev_h1.clear();
+    t.ev_dw1.clear();
     A3G_CUDA(cudaMemsetAsync(t.d_agg_bytes, 0, 16, t.s_comp));
     if (t.d_tier_rows) A3G_CUDA(cudaMemsetAsync(t.d_tier_rows, 0, kMaxTiers * 8, t.s_comp));
     A3G_CUDA(cudaMemsetAsync(t.d_stats, 0, static_cast<size_t>(K) * A3G_STEP_STATS * 8, t.s_comp));
@@ -1039,6 +1047,18 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
       agg += x;
     }
     t.last_agg_launches = t.ev_agg.size() / 2;
+    auto avg_pairs = [](const std::vector<cudaEvent_t>& ev) {
+      double sum = 0;
+      for (size_t i = 0; i + 1 < ev.size(); i += 2) {
+        float x = 0;
+        A3G_CUDA(cudaEventElapsedTime(&x, ev[i], ev[i + 1]));
+        sum += x;
+      }
+      return ev.size() >= 2 ? sum / static_cast<double>(ev.size() / 2) : 0.0;
+    };
+    t.last_h1_ms = avg_pairs(t.ev_h1);
+    t.last_dw1_ms = avg_pairs(t.ev_dw1);
+    t.last_gemm_launches = t.ev_h1.size() / 2;
     t.last_agg_ms = t.last_agg_launches ? agg / t.last_agg_launches : 0;
     unsigned long long words[2] = {0, 0};
     A3G_CUDA(cudaMemcpy(words, t.d_agg_bytes, 16, cudaMemcpyDeviceToHost));
@@ -1203,6 +1223,15 @@ a3g_status a3g_trainer_timing(a3g_trainer* tr, double* total_ms, double* agg_ms,
 }
 
 // ------------------------------------------------------------------- comm
+a3g_status a3g_trainer_gemm_timing(a3g_trainer* tr, double* h1_ms, double* dw1_ms, uint64_t* launches) {
+  return guard([&] {
+    TrainerState& t = tr->st;
+    if (h1_ms) *h1_ms = t.last_h1_ms;
+    if (dw1_ms) *dw1_ms = t.last_dw1_ms;
+    if (launches) *launches = t.last_gemm_launches;
+  });
+}
+
 a3g_status a3g_comm_unique_id(uint8_t id[128]) {
   return guard([&] { comm_unique_id(id); });
 }

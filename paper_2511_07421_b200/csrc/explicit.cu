@@ -123,7 +123,7 @@ extern "C" {
 a3g_status a3g_batch_model_create(int device, uint32_t F, uint32_t H, uint32_t C, a3g_batch_model** out) {
   return guard([&] {
     if (F < 1 || H < 1 || C < 1) raise(A3G_ERR_PARAMETER, "init_model: dims must be >= 1");
-    if (H > 32 || C > 32) raise(A3G_ERR_PARAMETER, "trainer: hidden_dim and num_classes must be <= 32");
+    if (H > 256 || C > 32) raise(A3G_ERR_PARAMETER, "trainer: hidden_dim must be <= 256 and num_classes <= 32");
     auto* m = new a3g_batch_model;
     m->device = device;
     m->F = F;

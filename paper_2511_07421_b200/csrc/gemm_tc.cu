@@ -90,6 +90,12 @@ __device__ __forceinline__ uint32_t idesc_bf16(uint32_t n, bool a_mn_major, bool
 
 constexpr int kParts = 3;  // bf16 terms per fp32 operand
 
+// MMA N (and TMEM columns) for hidden width H: 16, 32, 64, 128 or 256
+__host__ __device__ __forceinline__ uint32_t hn_of(uint32_t H) {
+  return H <= 16 ? 16u : H <= 32 ? 32u : H <= 64 ? 64u : H <= 128 ? 128u : 256u;
+}
+__host__ __device__ __forceinline__ uint32_t tmem_cols_of(uint32_t HN) { return HN < 32 ? 32u : HN; }
+
 __device__ __forceinline__ void split3(float x, __nv_bfloat16 (&p)[kParts]) {
   p[0] = __float2bfloat16_rn(x);
   const float r1 = x - __bfloat162float(p[0]);
@@ -181,7 +187,7 @@ __global__ void __launch_bounds__(kTcThreads) k_h1_tc(const __grid_constant__ Tc
   uint8_t* bpart = apart + kParts * kPartBytes;
   const uint32_t b_part = a.HN * 64 * 2;
   const uint32_t b_cs = (a.HN / 8) * kCore;  // B: core (n/8, k/8) at (k/8)*b_cs + (n/8)*128
-  if (warp == 0) tmem_alloc(&tmem_slot, 32);
+  if (warp == 0) tmem_alloc(&tmem_slot, tmem_cols_of(a.HN));
   if (tid == 0) {
     ptx::mbar_init(&bar, 1);
     ptx::fence_mbar_init();
@@ -250,20 +256,28 @@ __global__ void __launch_bounds__(kTcThreads) k_h1_tc(const __grid_constant__ Tc
   }
   ptx::mbar_wait(&bar, (nkb - 1) & 1);
   tc_fence_after();
-  const uint32_t row = r0 + warp * 32 + lane;
   const bool split = gridDim.y > 1;
   float* out = split ? a.hpart + (static_cast<uint64_t>(blockIdx.y) * a.part_rows) * a.H : a.h1;
+  // epilogue: TMEM -> shared tile [128][HN + 1] (warp w owns rows 32w..) ->
+  // coalesced row-major stores of the 128 x H block (the MMAs are done: the
+  // staging buffers are free)
+  float* tile = reinterpret_cast<float*>(smem);
+  const uint32_t ts = a.HN + 1;
   for (uint32_t c0 = 0; warp < 4 && c0 < a.HN; c0 += 16) {
     float v[16];
     tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
-    if (row < n)
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (c0 + j < a.H) out[static_cast<uint64_t>(row) * a.H + c0 + j] = split ? v[j] : fmaxf(v[j], 0.f);
+    for (int j = 0; j < 16; ++j) tile[(warp * 32 + lane) * ts + c0 + j] = split ? v[j] : fmaxf(v[j], 0.f);
+  }
+  __syncthreads();
+  const uint32_t rows = min(128u, n - r0);
+  for (uint32_t i = tid; i < rows * a.H; i += kTcThreads) {
+    const uint32_t rr = i / a.H, c = i - rr * a.H;
+    out[static_cast<uint64_t>(r0 + rr) * a.H + c] = tile[rr * ts + c];
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, 32);
+  if (warp == 0) tmem_dealloc(tmem, tmem_cols_of(a.HN));
 }
 
 // ------------------------------------------------------------ backward -----
@@ -291,14 +305,12 @@ __global__ void __launch_bounds__(kTcThreads) k_dw1_tc(const __grid_constant__ T
     return;
   }
   const uint32_t H = a.H;
-  const uint32_t g_stg = 2 * 64 * 32 * 4;  // dh1 | h1 staging per stage (H <= 32)
   float* stg = reinterpret_cast<float*>(smem);
-  float* stg_g = reinterpret_cast<float*>(smem + 2 * kStgBytes);
-  uint8_t* apart = smem + 2 * kStgBytes + 2 * g_stg;
+  uint8_t* apart = smem + 2 * kStgBytes;
   uint8_t* gpart = apart + kParts * kPartBytes;
   const uint32_t g_part = 64 * a.HN * 2;
   const uint32_t g_rs = (a.HN / 8) * kCore;  // G core (row/8, h/8) at (row/8)*g_rs + (h/8)*128
-  if (warp == 0) tmem_alloc(&tmem_slot, 32);
+  if (warp == 0) tmem_alloc(&tmem_slot, tmem_cols_of(a.HN));
   if (tid == 0) {
     ptx::mbar_init(&bar, 1);
     ptx::fence_mbar_init();
@@ -312,16 +324,6 @@ __global__ void __launch_bounds__(kTcThreads) k_dw1_tc(const __grid_constant__ T
       const uint32_t row = kr0 + rr, f = f0 + c;
       const bool ok = row < re && f < a.pitch;
       cp_async16(dst + rr * 128 + c, ok ? a.agg + static_cast<uint64_t>(row) * a.pitch + f : a.agg, ok);
-    }
-    // dh1 / h1 rows kr0.. are contiguous (row-major, H floats per row)
-    float* gd = stg_g + (kb & 1) * (g_stg / 4);
-    const uint32_t pieces = 64 * H / 4;
-    for (uint32_t i = tid; i < pieces; i += kTcThreads) {
-      const uint32_t row = kr0 + (i * 4) / H;
-      const bool ok = row < re;
-      const uint64_t o = static_cast<uint64_t>(kr0) * H + i * 4;
-      cp_async16(gd + i * 4, ok ? a.dh1 + o : a.dh1, ok);
-      cp_async16(gd + 64 * 32 + i * 4, ok ? a.h1 + o : a.h1, ok);
     }
     cp_async_commit();
   };
@@ -347,14 +349,18 @@ __global__ void __launch_bounds__(kTcThreads) k_dw1_tc(const __grid_constant__ T
       const uint32_t i = tid + j * kTcThreads, rr = i >> 5, c = (i & 31) * 4;
       put4(apart, kPartBytes, rr, c, 16 * kCore, kCore, *reinterpret_cast<const float4*>(src + rr * 128 + c));
     }
-    const float* gd = stg_g + (kb & 1) * (g_stg / 4);
-    for (uint32_t i = tid; i < 64 * (a.HN / 4); i += kTcThreads) {  // G = dh1 * [h1 > 0] (trainer.cpp:200)
+    // G = dh1 * [h1 > 0] (trainer.cpp:200) of rows kr0.., read straight from
+    // global (row-major, H floats per row: consecutive threads, consecutive h)
+    const uint32_t kr0 = rb + kb * 64;
+    for (uint32_t i = tid; i < 64 * (a.HN / 4); i += kTcThreads) {
       const uint32_t rr = i / (a.HN / 4), c = (i % (a.HN / 4)) * 4;
+      const uint32_t row = kr0 + rr;
       float t[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const uint32_t h = c + j, o = rr * H + h;
-        t[j] = h < H && gd[64 * 32 + o] > 0.f ? gd[o] : 0.f;
+        const uint32_t h = c + j;
+        const uint64_t o = static_cast<uint64_t>(row) * H + h;
+        t[j] = (row < re && h < H && __ldg(a.h1 + o) > 0.f) ? __ldg(a.dh1 + o) : 0.f;
       }
       put4(gpart, g_part, rr, c, g_rs, kCore, make_float4(t[0], t[1], t[2], t[3]));
     }
@@ -380,18 +386,25 @@ __global__ void __launch_bounds__(kTcThreads) k_dw1_tc(const __grid_constant__ T
   }
   ptx::mbar_wait(&bar, (nkb - 1) & 1);
   tc_fence_after();
-  const uint32_t f = f0 + warp * 32 + lane;
+  // epilogue through a shared tile, as k_h1_tc: coalesced stores of the
+  // 128-feature x H partial
+  float* tile = reinterpret_cast<float*>(smem);
+  const uint32_t ts = a.HN + 1;
   for (uint32_t c0 = 0; warp < 4 && c0 < a.HN; c0 += 16) {
     float v[16];
     tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
-    if (f < a.F)
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (c0 + j < a.H) out[static_cast<uint64_t>(f) * a.H + c0 + j] = v[j];
+    for (int j = 0; j < 16; ++j) tile[(warp * 32 + lane) * ts + c0 + j] = v[j];
+  }
+  __syncthreads();
+  const uint32_t nf = min(128u, a.F - f0);
+  for (uint32_t i = tid; i < nf * H; i += kTcThreads) {
+    const uint32_t ff = i / H, c = i - ff * H;
+    out[static_cast<uint64_t>(f0 + ff) * H + c] = tile[ff * ts + c];
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, 32);
+  if (warp == 0) tmem_dealloc(tmem, tmem_cols_of(a.HN));
 }
 
 // h1 = ReLU(sum of the split-K partials), in split order (deterministic).
@@ -410,12 +423,14 @@ __global__ void k_h1_reduce(const float* hpart, uint32_t nsplit, uint32_t part_r
 }  // namespace
 
 size_t tc_h1_smem(uint32_t /*F*/, uint32_t H) {
-  const uint32_t HN = H <= 16 ? 16 : 32;
-  return 2ull * kStgBytes + kParts * kPartBytes + static_cast<size_t>(kParts) * HN * 64 * 2;
+  const uint32_t HN = hn_of(H);
+  const size_t main = 2ull * kStgBytes + kParts * kPartBytes + static_cast<size_t>(kParts) * HN * 64 * 2;
+  return std::max<size_t>(main, static_cast<size_t>(128) * (HN + 1) * 4);  // epilogue tile
 }
 size_t tc_dw1_smem(uint32_t H) {
-  const uint32_t HN = H <= 16 ? 16 : 32;
-  return 2ull * kStgBytes + 2ull * (2 * 64 * 32 * 4) + kParts * kPartBytes + static_cast<size_t>(kParts) * 64 * HN * 2;
+  const uint32_t HN = hn_of(H);
+  const size_t main = 2ull * kStgBytes + kParts * kPartBytes + static_cast<size_t>(kParts) * 64 * HN * 2;
+  return std::max<size_t>(main, static_cast<size_t>(128) * (HN + 1) * 4);
 }
 
 void launch_h1_tc(TrainerState& t, const float* agg, const uint32_t* n_inner, float* h1, cudaStream_t st) {
@@ -424,7 +439,7 @@ void launch_h1_tc(TrainerState& t, const float* agg, const uint32_t* n_inner, fl
   a.pitch = t.pitch;
   a.F = t.F;
   a.H = t.H;
-  a.HN = t.H <= 16 ? 16 : 32;
+  a.HN = hn_of(t.H);
   a.n_inner = n_inner;
   a.w1 = t.d_w1;
   a.h1 = h1;
@@ -432,8 +447,10 @@ void launch_h1_tc(TrainerState& t, const float* agg, const uint32_t* n_inner, fl
   // split K so the grid covers ~4 CTAs per SM (the row tiles alone are < 1 wave)
   const uint32_t tiles = static_cast<uint32_t>((t.cap_inner + 127) / 128);
   const uint32_t nkb = a.k_pad / 64;
-  uint32_t ksplit = std::min<uint32_t>(std::min<uint32_t>(nkb, t.h1_split_cap),
-                                       std::max<uint32_t>(1, (4u * t.sm_count + tiles - 1) / tiles));
+  uint32_t ksplit = tiles >= static_cast<uint32_t>(t.sm_count)
+                        ? 1u
+                        : std::min<uint32_t>(std::min<uint32_t>(nkb, t.h1_split_cap),
+                                             std::max<uint32_t>(1, (4u * t.sm_count + tiles - 1) / tiles));
   a.kb_per_split = (nkb + ksplit - 1) / ksplit;
   ksplit = (nkb + a.kb_per_split - 1) / a.kb_per_split;
   a.hpart = t.d_hpart;
@@ -456,7 +473,7 @@ void launch_dw1_tc(const TrainerState& t, const float* agg, const uint32_t* n_in
   a.pitch = t.pitch;
   a.F = t.F;
   a.H = t.H;
-  a.HN = t.H <= 16 ? 16 : 32;
+  a.HN = hn_of(t.H);
   a.n_inner = n_inner;
   a.h1 = const_cast<float*>(h1);
   a.dh1 = dh1;

@@ -429,30 +429,57 @@ struct OuterArgs {
   int has_layer0;
 };
 
+// One warp per seed; lane l owns hidden units l, l + 32, ... (H <= 256).
+constexpr int kOuterHB = 8;  // hidden units per lane (H <= 32 * kOuterHB)
 __global__ void __launch_bounds__(256) k_outer(OuterArgs a) {
   const int lane = threadIdx.x & 31;
   const uint32_t ns = *a.ns;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   const uint32_t H = a.H, C = a.C;
+  const uint32_t nh = (H + 31) / 32;  // hidden units per lane in use
   const float inv_ns = 1.f / static_cast<float>(ns);
   for (uint32_t s = gw; s < ns; s += nw) {
     const uint32_t c0 = a.has_layer0 ? a.cnt0[s] : 0u;
     const uint32_t* srcs = a.sidx0 + static_cast<uint64_t>(s) * a.f0;
-    float ag = 0.f;
-    if (lane < H) {
-      if (c0 == 0) {
-        ag = a.h1[static_cast<uint64_t>(s) * H + lane];
-      } else {
-        for (uint32_t t = 0; t < c0; ++t) ag += a.h1[static_cast<uint64_t>(srcs[t]) * H + lane];
-        ag *= 1.f / static_cast<float>(c0);
+    // outer mean of h1 over the seed's layer-0 sources, or its own row
+    // (trainer.cpp:115-127): sum in edge order, then x (1/deg)
+    float ag[kOuterHB];
+#pragma unroll
+    for (int k = 0; k < kOuterHB; ++k) ag[k] = 0.f;
+    if (c0 == 0) {
+#pragma unroll
+      for (int k = 0; k < kOuterHB; ++k) {
+        const uint32_t h = lane + 32 * k;
+        if (static_cast<uint32_t>(k) < nh && h < H) ag[k] = a.h1[static_cast<uint64_t>(s) * H + h];
       }
-      a.agg_outer[static_cast<uint64_t>(s) * H + lane] = ag;
+    } else {
+      for (uint32_t t = 0; t < c0; ++t) {
+        const float* row = a.h1 + static_cast<uint64_t>(srcs[t]) * H;
+#pragma unroll
+        for (int k = 0; k < kOuterHB; ++k) {
+          const uint32_t h = lane + 32 * k;
+          if (static_cast<uint32_t>(k) < nh && h < H) ag[k] += row[h];
+        }
+      }
+      const float inv = 1.f / static_cast<float>(c0);
+#pragma unroll
+      for (int k = 0; k < kOuterHB; ++k) ag[k] *= inv;
+    }
+#pragma unroll
+    for (int k = 0; k < kOuterHB; ++k) {
+      const uint32_t h = lane + 32 * k;
+      if (static_cast<uint32_t>(k) < nh && h < H) a.agg_outer[static_cast<uint64_t>(s) * H + h] = ag[k];
     }
     // logits (trainer.cpp:129-131)
     float myz = -INFINITY;
     for (uint32_t cc = 0; cc < C; ++cc) {
-      float p = lane < H ? ag * a.w2[lane * C + cc] : 0.f;
+      float p = 0.f;
+#pragma unroll
+      for (int k = 0; k < kOuterHB; ++k) {
+        const uint32_t h = lane + 32 * k;
+        if (static_cast<uint32_t>(k) < nh && h < H) p = fmaf(ag[k], a.w2[h * C + cc], p);
+      }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(kFull, p, off);
       if (lane == static_cast<int>(cc)) myz = p;
@@ -476,16 +503,33 @@ __global__ void __launch_bounds__(256) k_outer(OuterArgs a) {
     if (lane == 0) a.loss_s[s] = -(zy - mx - logf(den));
     // dagg_outer = dlogits . W2^T (trainer.cpp:177-179), pre-scaled by the
     // outer mean's 1/deg: the contribution of each of the seed's edges
-    float dg = 0.f;
+    float dg[kOuterHB];
+#pragma unroll
+    for (int k = 0; k < kOuterHB; ++k) dg[k] = 0.f;
     for (uint32_t cc = 0; cc < C; ++cc) {
       const float dc = __shfl_sync(kFull, d, cc);
-      if (lane < H) dg = fmaf(dc, a.w2[lane * C + cc], dg);
+#pragma unroll
+      for (int k = 0; k < kOuterHB; ++k) {
+        const uint32_t h = lane + 32 * k;
+        if (static_cast<uint32_t>(k) < nh && h < H) dg[k] = fmaf(dc, a.w2[h * C + cc], dg[k]);
+      }
     }
-    if (lane < H) {
-      const float v = c0 == 0 ? dg : (1.f / static_cast<float>(c0)) * dg;
-      a.dagg[static_cast<uint64_t>(s) * H + lane] = v;
-      atomicMax(a.amax, __float_as_uint(fabsf(v)));  // non-negative floats order like their bits
+    float amax = 0.f;
+#pragma unroll
+    for (int k = 0; k < kOuterHB; ++k) {
+      const uint32_t h = lane + 32 * k;
+      if (static_cast<uint32_t>(k) < nh && h < H) {
+        const float v = c0 == 0 ? dg[k] : (1.f / static_cast<float>(c0)) * dg[k];
+        a.dagg[static_cast<uint64_t>(s) * H + h] = v;
+        amax = fmaxf(amax, fabsf(v));
+      }
     }
+    amax = fmaxf(amax, __shfl_xor_sync(kFull, amax, 16));
+    amax = fmaxf(amax, __shfl_xor_sync(kFull, amax, 8));
+    amax = fmaxf(amax, __shfl_xor_sync(kFull, amax, 4));
+    amax = fmaxf(amax, __shfl_xor_sync(kFull, amax, 2));
+    amax = fmaxf(amax, __shfl_xor_sync(kFull, amax, 1));
+    if (lane == 0) atomicMax(a.amax, __float_as_uint(amax));  // non-negative floats order like their bits
   }
 }
 
@@ -801,7 +845,20 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
     A3G_LAUNCH_DONE("k_tier_rows", st);
     A3G_CUDA(cudaMemsetAsync(t.d_tier_seen, 0, (g->n + 31) / 32 * 4, st));
   }
-  if (!fused) launch_h1_tc(t, t.d_agg_inner, aa.n_inner, t.d_h1, st);
+  if (!fused) {
+    cudaEvent_t g0 = nullptr, g1 = nullptr;
+    if (record_timing) {
+      A3G_CUDA(cudaEventCreate(&g0));
+      A3G_CUDA(cudaEventCreate(&g1));
+      A3G_CUDA(cudaEventRecord(g0, st));
+    }
+    launch_h1_tc(t, t.d_agg_inner, aa.n_inner, t.d_h1, st);
+    if (record_timing) {
+      A3G_CUDA(cudaEventRecord(g1, st));
+      t.ev_h1.push_back(g0);
+      t.ev_h1.push_back(g1);
+    }
+  }
   // ---- outer aggregation, logits, loss, dlogits, scatter to dh1
   OuterArgs oa{};
   oa.h1 = t.d_h1;
@@ -835,7 +892,18 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
   uint32_t nparts;
   if (t.tc_gemms || t.H > 32) {
     nparts = t.tc_splits;
+    cudaEvent_t g0 = nullptr, g1 = nullptr;
+    if (record_timing) {
+      A3G_CUDA(cudaEventCreate(&g0));
+      A3G_CUDA(cudaEventCreate(&g1));
+      A3G_CUDA(cudaEventRecord(g0, st));
+    }
     launch_dw1_tc(t, t.d_agg_inner, aa.n_inner, t.d_h1, t.d_dh1, t.d_part, nparts, st);
+    if (record_timing) {
+      A3G_CUDA(cudaEventRecord(g1, st));
+      t.ev_dw1.push_back(g0);
+      t.ev_dw1.push_back(g1);
+    }
   } else {
     nparts = t.dw1_splits;
     const dim3 grid((t.F + 127) / 128, nparts);

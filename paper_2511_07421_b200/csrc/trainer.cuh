@@ -57,6 +57,9 @@ struct TrainerState {
   cudaEvent_t ev_seeds = nullptr;                     // host seeds copied (sampling streams wait on it)
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
   std::vector<cudaEvent_t> ev_agg;  // pairs around k_agg1 launches (timing)
+  std::vector<cudaEvent_t> ev_h1, ev_dw1;  // pairs around the tcgen05 h1 / dW1 GEMMs (timing)
+  double last_h1_ms = 0, last_dw1_ms = 0;
+  uint64_t last_gemm_launches = 0;
   bool timing = true;
   double last_total_ms = 0, last_agg_ms = 0, last_agg_bytes = 0;
   uint64_t last_agg_launches = 0;

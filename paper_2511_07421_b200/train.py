@@ -258,6 +258,12 @@ class Trainer:
         check(lib().a3g_trainer_tier_rows(self.h, ptr(out, u64p)))
         return out
 
+    def gemm_timing(self):
+        """Average ms of the tcgen05 h1 / dW1 GEMMs of the last steps call."""
+        a, b, n = C.c_double(), C.c_double(), C.c_uint64()
+        check(lib().a3g_trainer_gemm_timing(self.h, C.byref(a), C.byref(b), C.byref(n)))
+        return dict(h1_ms=a.value, dw1_ms=b.value, launches=n.value)
+
     def timing(self):
         t, a, b, l = C.c_double(), C.c_double(), C.c_double(), C.c_uint64()
         check(lib().a3g_trainer_timing(self.h, C.byref(t), C.byref(a), C.byref(b), C.byref(l)))

@@ -89,6 +89,17 @@ def test_grads_c1_vs_oracle(orc, c1, fanouts, gamma, kind, H):
     _grad_case(orc, g, cache, batches[3], fanouts, gamma, kind, T.sampling_seed(1, 0, 3, 0), H=H)
 
 
+@pytest.mark.parametrize("H", [48, 64, 128, 256])
+def test_wide_hidden_on_tcgen05(orc, c1, H):
+    """Realistic hidden widths (e.g. 256): h1 and dW1 run
+    on tcgen05 with N = H (64 / 128 / 256 TMEM columns), k_outer strides the
+    hidden units over the warp; loss and gradients within the same 1e-3."""
+    g = c1
+    cache = CA.build_static_cache(g, CA.CacheConfig(int(0.2 * g.num_nodes) * g.feat_dim * 4, 1))
+    batches = T.plan_epoch_batches(g.train_nodes, 0, 1024, orc.hash2(1, 0))
+    _grad_case(orc, g, cache, batches[4], [10, 5], 8.0, 0, T.sampling_seed(1, 0, 4, 0), H=H)
+
+
 def test_tcgen05_gemm_path(orc, c1, monkeypatch):
     """A3G_TC_GEMMS=1: h1 and dW1 from the tcgen05 GEMMs instead of k_agg1's
     epilogue and the CUDA-core dW1 -- the same oracle tolerance (both paths

@@ -18,6 +18,8 @@
 #include "a3gnn/cache.hpp"
 #include "a3gnn/common.hpp"
 #include "a3gnn/graph.hpp"
+#include "a3gnn/partition.hpp"
+#include "a3gnn/trainer.hpp"
 
 namespace a3gnn::b200 {
 
@@ -45,5 +47,17 @@ a3g_sampler* thread_sampler(a3g_graph* g, a3g_cache* c, std::uint32_t n_seeds,
                             const std::vector<std::uint32_t>& fanouts);
 // Drop the device copies of g (and of caches over it).
 void release(const graph::Graph& g);
+
+// train() with u > 1 partition-local workers on the device (trainer_b200.cpp);
+// also behind execute_pipeline with partitions > 1.
+struct PartitionedRun {
+  train::TrainReport rep;
+  std::uint64_t hits = 0, misses = 0;
+  train::Model model;
+};
+PartitionedRun train_partitioned(const graph::Graph& g, const train::ModelSpec& spec,
+                                 const sampling::SamplerConfig& sampler_cfg, const cache::CacheState& cache_global,
+                                 std::uint32_t u, graph::PartitionMethod method, std::uint32_t batch_size,
+                                 std::uint32_t epochs, std::uint64_t model_seed);
 
 }  // namespace a3gnn::b200

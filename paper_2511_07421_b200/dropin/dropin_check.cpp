@@ -126,6 +126,36 @@ int main(int argc, char** argv) {
     std::printf("train epoch %zu loss %.17g hit %.17g\n", e, rep.loss_curve[e], rep.epoch_hit_rates[e]);
   std::printf("train accuracy %.17g batch_bytes %llu act_bytes %llu\n", rep.test_accuracy,
               (unsigned long long)rep.max_batch_bytes, (unsigned long long)rep.max_activation_bytes);
+  // partitioned workers (u = 2, hash partitions with halos, localized caches)
+  {
+    train::TrainOptions o2 = opts;
+    o2.u = 2;
+    o2.epochs = 1;
+    const auto r2 = train::train(g, spec, scfg, cache, o2);
+    for (std::size_t e = 0; e < r2.loss_curve.size(); ++e)
+      std::printf("train_u2 epoch %zu loss %.17g hit %.17g\n", e, r2.loss_curve[e], r2.epoch_hit_rates[e]);
+    std::printf("train_u2 accuracy %.17g batch_bytes %llu act_bytes %llu\n", r2.test_accuracy,
+                (unsigned long long)r2.max_batch_bytes, (unsigned long long)r2.max_activation_bytes);
+    ResolvedDesign d;
+    d.batch_size = 512;
+    d.partitions = 2;
+    d.bias_rate = 8.0;
+    d.workers = 2;
+    d.cache_volume = cc.volume_bytes;
+    d.mode = Mode::pmode1;
+    pipeline::PlatformSpec plat;
+    pipeline::ExecOptions eo;
+    eo.epochs = 1;
+    sampling::SamplerConfig pcfg;
+    pcfg.fanouts = {10, 5};
+    pcfg.rng_seed = 3;
+    const auto ex = pipeline::execute_pipeline(g, d, plat, spec, pcfg, eo);
+    std::printf("pipeline_p2 accuracy %.17g hit %.17g batch_bytes %llu model_bytes %llu\n", ex.metrics.accuracy,
+                ex.hit_rate, (unsigned long long)ex.batch_bytes_max, (unsigned long long)ex.model_bytes);
+    const auto c = pipeline::profile_stage_costs(g, d, plat, spec, pcfg, 4);
+    std::printf("profile_p2 iters %llu positive %d\n", (unsigned long long)c.iters_per_epoch,
+                c.t_sample > 0 && c.t_batch > 0 && c.t_train > 0 ? 1 : 0);
+  }
   // the per-batch model entry points on one explicit batch (trainer.cpp:59-239)
   {
     sampling::SamplerConfig cfg;

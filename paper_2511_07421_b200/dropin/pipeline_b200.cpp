@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <chrono>
 
+#include "a3gnn/partition.hpp"
 #include "a3gnn/pipeline.hpp"
 #include "a3gnn/rng.hpp"
 #include "dropin.hpp"
@@ -27,20 +28,25 @@ struct Setup {
   cache::CacheState cache;
   std::vector<NodeId> train_nodes;
   double sample_multiplier = 1.0;
+  graph::PartitionSet parts;                 // partitions > 1 only
+  std::vector<train::WorkerContext> ctxs;    // partitions > 1 only
 };
 
-// make_setup (pipeline_exec.cpp:74-112) for u = 1: the cache over the whole
-// graph, the ascending train ids. Partitioned workers (partitions > 1) are not
-// part of the B200 path (data parallelism runs across GPUs).
+// make_setup (pipeline_exec.cpp:74-112): the cache over `partitions` devices;
+// u = 1: the whole graph and its ascending train ids; partitions > 1: the
+// reference's hash partitioning and worker contexts (localized caches).
 Setup make_setup(const Graph& g, const ResolvedDesign& d, const PlatformSpec& platform) {
-  if (d.partitions > 1)
-    throw ConfigError("pipeline: partitioned workers (partitions > 1) are not part of the B200 path "
-                      "(data parallelism runs across GPUs)");
   Setup s;
   cache::CacheConfig ccfg;
   ccfg.volume_bytes = d.cache_volume;
   ccfg.num_devices = d.partitions;
   s.cache = cache::build_static_cache(g, ccfg);
+  if (d.partitions > 1) {
+    s.parts = graph::partition_graph(g, d.partitions, graph::PartitionMethod::hash);
+    s.ctxs = train::make_worker_contexts(g, &s.parts, s.cache);
+    for (const auto& c : s.ctxs)
+      if (c.train_nodes.empty()) throw ConfigError("pipeline: a worker has no train nodes");
+  }
   for (std::uint64_t v = 0; v < g.num_nodes; ++v)
     if (g.train_mask[v]) s.train_nodes.push_back(static_cast<NodeId>(v));
   if (s.train_nodes.empty()) throw ConfigError("pipeline: a worker has no train nodes");
@@ -78,19 +84,29 @@ StageCosts profile_stage_costs(const Graph& g, const ResolvedDesign& design, con
                                const ModelSpec& spec, const SamplerConfig& sampler_base, std::uint32_t probe_iters) {
   if (probe_iters < 3) throw ParameterError("profile_stage_costs: probe_iters must be >= 3");
   const Setup s = make_setup(g, design, platform);
-  const auto batches = train::plan_epoch_batches(s.train_nodes, 0, design.batch_size, hash2(sampler_base.rng_seed, 0));
-  std::uint32_t max_seeds = 1;
-  for (const auto& b : batches) max_seeds = std::max<std::uint32_t>(max_seeds, static_cast<std::uint32_t>(b.size()));
-  Trainer t;
-  make_trainer(t, g, s.cache, spec, sampler_base, max_seeds, 1);
+  // workers: the whole graph (u = 1) or the partition-local contexts
+  const std::uint32_t u = s.ctxs.empty() ? 1u : static_cast<std::uint32_t>(s.ctxs.size());
+  std::vector<std::vector<std::vector<NodeId>>> batches(u);
+  std::vector<Trainer> tw(u);
+  std::size_t steps = 0;
+  for (std::uint32_t w = 0; w < u; ++w) {
+    const Graph& lg = s.ctxs.empty() ? g : *s.ctxs[w].graph;
+    const auto& tn = s.ctxs.empty() ? s.train_nodes : s.ctxs[w].train_nodes;
+    batches[w] = train::plan_epoch_batches(tn, 0, design.batch_size, hash2(sampler_base.rng_seed, w));
+    steps = std::max(steps, batches[w].size());
+    std::uint32_t max_seeds = 1;
+    for (const auto& b : batches[w]) max_seeds = std::max<std::uint32_t>(max_seeds, static_cast<std::uint32_t>(b.size()));
+    make_trainer(tw[w], lg, s.ctxs.empty() ? s.cache : s.ctxs[w].cache, spec, sampler_base, max_seeds, 1);
+  }
   std::vector<double> ts, tb, tt;
   for (std::uint32_t i = 0; i < probe_iters; ++i) {
-    const std::uint32_t step = i % static_cast<std::uint32_t>(batches.size());
-    const auto& seeds = batches[step];
+    // the probe units of pipeline_exec.cpp:151: (0, i % steps, i % u)
+    const std::uint32_t step = i % static_cast<std::uint32_t>(steps), w = i % u;
+    const auto& seeds = batches[w][step % batches[w].size()];
     double ms[3] = {0, 0, 0};
-    b200::check(a3g_trainer_profile_step(t.h, seeds.data(), static_cast<std::uint32_t>(seeds.size()),
+    b200::check(a3g_trainer_profile_step(tw[w].h, seeds.data(), static_cast<std::uint32_t>(seeds.size()),
                                          design.bias_rate, kind_of(sampler_base),
-                                         train::sampling_seed(sampler_base.rng_seed, 0, step, 0), ms));
+                                         train::sampling_seed(sampler_base.rng_seed, 0, step, w), ms));
     ts.push_back(ms[0] * 1e-3);
     tb.push_back(ms[1] * 1e-3);
     tt.push_back(ms[2] * 1e-3);
@@ -99,7 +115,7 @@ StageCosts profile_stage_costs(const Graph& g, const ResolvedDesign& design, con
   costs.t_sample = median(ts) * s.sample_multiplier;
   costs.t_batch = median(tb);
   costs.t_train = median(tt);
-  costs.iters_per_epoch = batches.size();
+  costs.iters_per_epoch = static_cast<std::uint64_t>(steps) * u;
   return costs;
 }
 
@@ -108,6 +124,30 @@ ExecResult execute_pipeline(const Graph& g, const ResolvedDesign& design, const 
   const Setup s = make_setup(g, design, platform);
   const std::uint32_t B = design.batch_size;
   if (B < 1) throw ParameterError("pipeline: batch_size must be >= 1");
+  if (design.partitions > 1) {
+    // units (epoch, step, worker) in order, the SGD after each step's last
+    // worker (pipeline_exec.cpp:115-123, 199-215): train() with u workers
+    SamplerConfig cfg = sampler_base;
+    cfg.bias_rate = design.bias_rate;
+    const auto t0 = Clock::now();
+    const auto run = b200::train_partitioned(g, spec, cfg, s.cache, design.partitions, graph::PartitionMethod::hash,
+                                             B, opts.epochs, opts.model_seed);
+    ExecResult result;
+    result.elapsed_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+    result.metrics.throughput_eps =
+        result.elapsed_seconds > 0.0 ? static_cast<double>(opts.epochs) / result.elapsed_seconds : 0.0;
+    result.batch_bytes_max = run.rep.max_batch_bytes;
+    result.model_bytes = spec.param_bytes() + run.rep.max_activation_bytes;
+    result.memory = analytic_memory(design.mode, design.workers, design.cache_volume, result.batch_bytes_max,
+                                    result.model_bytes, platform.runtime_overhead_bytes);
+    result.metrics.memory_bytes = static_cast<double>(result.memory.peak_total);
+    result.within_capacity = result.memory.peak_total <= platform.gpu_mem_capacity;
+    result.metrics.accuracy = run.rep.test_accuracy;
+    result.hit_rate = run.hits + run.misses > 0
+                          ? static_cast<double>(run.hits) / static_cast<double>(run.hits + run.misses)
+                          : 0.0;
+    return result;
+  }
   Trainer t;
   make_trainer(t, g, s.cache, spec, sampler_base, static_cast<std::uint32_t>(std::min<std::size_t>(B, s.train_nodes.size())),
                opts.model_seed);

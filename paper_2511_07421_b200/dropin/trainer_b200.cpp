@@ -15,6 +15,7 @@
 #include <memory>
 
 #include "a3gnn/kernels.hpp"
+#include "a3gnn/partition.hpp"
 #include "a3gnn/rng.hpp"
 #include "a3gnn/trainer.hpp"
 #include "dropin.hpp"
@@ -178,12 +179,108 @@ double evaluate_full_graph(const Model& m, const Graph& g) {
   return acc;
 }
 
+}  // namespace a3gnn::train
+
+namespace a3gnn::b200 {
+
+// trainer.cpp:350-424 with u > 1 partition-local workers:
+// the reference's own partitioning and worker contexts (partition_graph,
+// make_worker_contexts, cache::localize -- host setup), each worker's step on
+// the device over its local graph and localized cache (RNG keyed by local
+// ids, as the reference), the unweighted mean of the workers' gradients
+// (sync_gradients) and the SGD step (sgd_step), both on the device.
+PartitionedRun train_partitioned(const graph::Graph& g, const train::ModelSpec& spec,
+                                 const sampling::SamplerConfig& sampler_cfg, const cache::CacheState& cache_global,
+                                 std::uint32_t u, graph::PartitionMethod method, std::uint32_t batch_size,
+                                 std::uint32_t epochs, std::uint64_t model_seed) {
+  using namespace a3gnn::train;
+  const graph::PartitionSet parts = graph::partition_graph(g, u, method);
+  const std::vector<WorkerContext> ctxs = make_worker_contexts(g, &parts, cache_global);
+  const auto nw = static_cast<std::uint32_t>(ctxs.size());
+  for (const auto& c : ctxs)
+    if (c.train_nodes.empty()) throw ConfigError("train: a worker has no train nodes");
+  PartitionedRun run;
+  run.model = init_model(spec, model_seed);
+  ModelSpec wspec = spec;
+  wspec.learning_rate = 0.0;  // worker trainers compute gradients only
+  std::vector<a3g_trainer*> tr(nw, nullptr);
+  struct Guard {
+    std::vector<a3g_trainer*>& t;
+    ~Guard() {
+      for (a3g_trainer* h : t) a3g_trainer_destroy(h);
+    }
+  } guard{tr};
+  for (std::uint32_t w = 0; w < nw; ++w) {
+    const Graph& lg = *ctxs[w].graph;
+    const auto ms = static_cast<std::uint32_t>(std::min<std::size_t>(batch_size, ctxs[w].train_nodes.size()));
+    b200::check(a3g_trainer_create(device_graph(lg), device_cache(lg, ctxs[w].cache), ms, sampler_cfg.fanouts.data(),
+                                   static_cast<std::uint32_t>(sampler_cfg.fanouts.size()), spec.hidden_dim,
+                                   spec.num_classes, 0.0, model_seed, &tr[w]));
+  }
+  const int kind = sampler_cfg.kind == sampling::SamplerKind::uniform_baseline ? A3G_SAMPLER_UNIFORM
+                                                                               : A3G_SAMPLER_WEIGHTED;
+  const std::uint64_t F = spec.feat_dim, H = spec.hidden_dim, C = spec.num_classes;
+  TrainReport& rep = run.rep;
+  rep.param_bytes = spec.param_bytes();
+  for (std::uint32_t epoch = 0; epoch < epochs; ++epoch) {
+    std::vector<std::vector<std::vector<NodeId>>> batches(nw);
+    std::size_t steps = 0;
+    for (std::uint32_t w = 0; w < nw; ++w) {
+      batches[w] = plan_epoch_batches(ctxs[w].train_nodes, epoch, batch_size, hash2(sampler_cfg.rng_seed, w));
+      steps = std::max(steps, batches[w].size());
+    }
+    double epoch_loss = 0.0;
+    std::size_t loss_count = 0;
+    std::uint64_t hits = 0, misses = 0;
+    for (std::size_t step = 0; step < steps; ++step) {
+      std::vector<Gradients> grads(nw);
+      for (std::uint32_t w = 0; w < nw; ++w) {
+        const auto& seeds = batches[w][step % batches[w].size()];
+        const std::uint64_t off[2] = {0, seeds.size()};
+        const std::uint64_t rs = sampling_seed(sampler_cfg.rng_seed, epoch, static_cast<std::uint32_t>(step), w);
+        b200::check(a3g_trainer_set_weights(tr[w], run.model.w1.data(), run.model.w2.data()));
+        double loss = 0.0;
+        b200::check(a3g_train_steps_v(tr[w], seeds.data(), off, 1, &rs, sampler_cfg.bias_rate, kind, 0, &loss));
+        grads[w].w1.resize(run.model.w1.size());
+        grads[w].w2.resize(run.model.w2.size());
+        b200::check(a3g_trainer_last_grads(tr[w], grads[w].w1.data(), grads[w].w2.data()));
+        std::uint64_t st[A3G_STEP_STATS];
+        b200::check(a3g_trainer_step_stats(tr[w], st, 1));
+        hits += st[A3G_STAT_HITS];
+        misses += st[A3G_STAT_MISSES];
+        rep.max_batch_bytes = std::max(rep.max_batch_bytes, st[A3G_STAT_UNIQUE] * F * 4 + st[A3G_STAT_EDGES] * 8);
+        rep.max_activation_bytes =
+            std::max(rep.max_activation_bytes, (st[A3G_STAT_INNER] * (F + H) + st[A3G_STAT_SEEDS] * (H + C)) * 4);
+        epoch_loss += loss;
+        ++loss_count;
+      }
+      sgd_step(run.model, sync_gradients(grads), spec.learning_rate);
+    }
+    rep.loss_curve.push_back(loss_count > 0 ? epoch_loss / static_cast<double>(loss_count) : 0.0);
+    rep.epoch_hit_rates.push_back(hits + misses ? static_cast<double>(hits) / static_cast<double>(hits + misses)
+                                                : 0.0);
+    run.hits += hits;
+    run.misses += misses;
+  }
+  rep.epochs_run = epochs;
+  rep.test_accuracy = evaluate_full_graph(run.model, g);
+  return run;
+}
+
+}  // namespace a3gnn::b200
+
+namespace a3gnn::train {
+
 TrainReport train(const Graph& g, const ModelSpec& spec, const SamplerConfig& sampler_cfg,
                   const CacheState& cache_global, const TrainOptions& opts) {
   if (opts.batch_size < 1) throw ParameterError("train: batch_size must be >= 1");
-  if (opts.u > 1)
-    throw ConfigError("train: partitioned workers (u > 1) are not part of the B200 path "
-                      "(data parallelism runs across GPUs)");
+  if (opts.u > 1) {  // partition-local workers (trainer.cpp:353-359)
+    auto run = b200::train_partitioned(g, spec, sampler_cfg, cache_global, opts.u, opts.partition_method,
+                                       opts.batch_size, opts.epochs, opts.model_seed);
+    run.rep.accuracy_drop = opts.reference_accuracy ? *opts.reference_accuracy - run.rep.test_accuracy
+                                                    : std::numeric_limits<double>::quiet_NaN();
+    return run.rep;
+  }
   std::vector<NodeId> train_nodes;
   for (std::uint64_t v = 0; v < g.num_nodes; ++v)
     if (g.train_mask[v]) train_nodes.push_back(static_cast<NodeId>(v));

@@ -87,10 +87,10 @@ def test_full_dropin_matches_reference():
     for a, b in zip(ref, dev):
         tag = " ".join(a.split()[:2])
         seen.add(a.split()[0])
-        if a.startswith("train epoch"):
+        if a.startswith("train epoch") or a.startswith("train_u2 epoch"):
             assert _num(a, "hit") == _num(b, "hit")
             assert abs(_num(a, "loss") - _num(b, "loss")) <= 1e-3 * abs(_num(a, "loss"))
-        elif a.startswith("train accuracy"):
+        elif a.startswith("train accuracy") or a.startswith("train_u2 accuracy"):
             assert abs(_num(a, "accuracy") - _num(b, "accuracy")) <= 3.0 / NTEST
             assert _num(a, "batch_bytes") == _num(b, "batch_bytes") and _num(a, "act_bytes") == _num(b, "act_bytes")
         elif a.startswith("pipeline"):  # every executor mode on the device
@@ -114,4 +114,5 @@ def test_full_dropin_matches_reference():
                 assert abs(_num(a, k) ** 0.5 - _num(b, k) ** 0.5) <= 1e-3 * _num(a, k) ** 0.5, (k, a, b)
         else:
             assert a == b, tag
-    assert {"model", "sync", "profile", "pipeline", "lookup2", "design"} <= seen
+    assert {"model", "sync", "profile", "pipeline", "lookup2", "design", "train_u2", "pipeline_p2",
+            "profile_p2"} <= seen

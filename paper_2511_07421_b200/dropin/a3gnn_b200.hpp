@@ -10,10 +10,13 @@
 //
 //   knob 0 batch_size        as is
 //   knob 1 partitions        FANOUT LEVEL: index i selects fanout_levels[i]
-//                            (partitioned workers are replaced by data
-//                            parallelism across GPUs, so this slot carries
-//                            the fanout knob the reference lacks); empty
-//                            fanout_levels = the sampler_base fanouts
+//                            (the B200 tuner selects cache ratio, fanout and
+//                            pipeline depth only -- scaling is data
+//                            parallelism across GPUs -- so this slot carries
+//                            the fanout knob the reference lacks; the
+//                            partitioned mode itself still runs through
+//                            train / execute_pipeline); empty fanout_levels =
+//                            the sampler_base fanouts
 //   knob 2 bias_rate         as is (gamma)
 //   knob 3 sampling_device   no effect: sampling always runs on the GPU
 //                            (the reference's knob only scales sampling time)

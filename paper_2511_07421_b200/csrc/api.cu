@@ -195,13 +195,16 @@ void validate_sample(const SamplerState& s, const uint32_t* seeds, uint32_t n_se
     return;
   }
   const a3g_graph* g = s.g;
-  bool any_deg = false;
-  for (uint32_t i = 0; i < n_seeds; ++i) {
+  for (uint32_t i = 0; i < n_seeds; ++i)
     if (seeds[i] >= g->n) raise(A3G_ERR_PARAMETER, "sample_khop: seed out of range");
-    any_deg |= g->h_ro[seeds[i] + 1] > g->h_ro[seeds[i]];
+  // assign_weights is reached (and throws on gamma < 1) only if some unique
+  // seed has neighbours; the degree lookups (random reads of the host CSR
+  // offsets, ~16 ms per 164K seeds at papers scale) only when gamma < 1
+  if (kind == A3G_SAMPLER_WEIGHTED && s.L > 0 && gamma < 1.0) {
+    bool any_deg = false;
+    for (uint32_t i = 0; i < n_seeds && !any_deg; ++i) any_deg = g->h_ro[seeds[i] + 1] > g->h_ro[seeds[i]];
+    if (any_deg) raise(A3G_ERR_PARAMETER, "assign_weights: gamma must be >= 1");
   }
-  if (kind == A3G_SAMPLER_WEIGHTED && s.L > 0 && any_deg && gamma < 1.0)
-    raise(A3G_ERR_PARAMETER, "assign_weights: gamma must be >= 1");
 }
 
 // prevalidated: device seeds that the host already checked (a3g_train_steps_v
@@ -826,9 +829,7 @@ void a3g_trainer_destroy(a3g_trainer* tr) {
   dfree(t.d_seed_buf);
   if (t.h_seed_stage) cudaFreeHost(t.h_seed_stage);
   if (t.h_losses) cudaFreeHost(t.h_losses);
-  for (cudaEvent_t e : t.ev_h1) cudaEventDestroy(e);
-  for (cudaEvent_t e : t.ev_dw1) cudaEventDestroy(e);
-  for (cudaEvent_t e : t.ev_agg) cudaEventDestroy(e);
+  for (cudaEvent_t e : t.ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < TrainerState::kArenas; ++i) {
     if (t.ev_sampled[i]) cudaEventDestroy(t.ev_sampled[i]);
     if (t.ev_consumed[i]) cudaEventDestroy(t.ev_consumed[i]);
@@ -931,12 +932,10 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
       t.d_stats = dalloc<unsigned long long>(static_cast<size_t>(K) * A3G_STEP_STATS);
       t.stats_cap = K;
     }
-    for (cudaEvent_t e : t.ev_agg) cudaEventDestroy(e);
-    t.ev_agg.clear();
-    for (cudaEvent_t e : t.ev_h1) cudaEventDestroy(e);
-    for (cudaEvent_t e : t.ev_dw1) cudaEventDestroy(e);
+    t.ev_agg.clear();  // the events return to the pool
     t.ev_h1.clear();
     t.ev_dw1.clear();
+    t.ev_used = 0;
     A3G_CUDA(cudaMemsetAsync(t.d_agg_bytes, 0, 16, t.s_comp));
     if (t.d_tier_rows) A3G_CUDA(cudaMemsetAsync(t.d_tier_rows, 0, kMaxTiers * 8, t.s_comp));
     A3G_CUDA(cudaMemsetAsync(t.d_stats, 0, static_cast<size_t>(K) * A3G_STEP_STATS * 8, t.s_comp));
@@ -944,13 +943,15 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
     A3G_CUDA(cudaStreamWaitEvent(t.s_samp, t.ev_t0, 0));
     const uint32_t* dseeds = seeds;
     if (!on_device) {  // H2D of every step's seeds (inside the timed region)
-      if (total > t.seed_buf_cap) {
+      if (total > t.seed_buf_cap) {  // grow geometrically: reallocation (a device sync) stays rare
+        const uint64_t cap = std::max<uint64_t>(total, std::max<uint64_t>(2 * t.seed_buf_cap,
+                                                                          64ull * t.max_seeds));
         dfree(t.d_seed_buf);
         if (t.h_seed_stage) cudaFreeHost(t.h_seed_stage);
         t.h_seed_stage = nullptr;
-        t.d_seed_buf = dalloc<uint32_t>(total);
-        A3G_CUDA(cudaMallocHost(&t.h_seed_stage, std::max<uint64_t>(total, 1) * 4));
-        t.seed_buf_cap = total;
+        t.d_seed_buf = dalloc<uint32_t>(cap);
+        A3G_CUDA(cudaMallocHost(&t.h_seed_stage, cap * 4));
+        t.seed_buf_cap = cap;
       }
       std::memcpy(t.h_seed_stage, seeds, total * 4);
       A3G_CUDA(cudaMemcpyAsync(t.d_seed_buf, t.h_seed_stage, total * 4, cudaMemcpyHostToDevice, t.s_samp));

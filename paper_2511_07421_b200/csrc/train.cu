@@ -822,8 +822,8 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
   aa.bytes = t.d_agg_bytes;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (record_timing) {
-    A3G_CUDA(cudaEventCreate(&e0));
-    A3G_CUDA(cudaEventCreate(&e1));
+    e0 = pool_event(t);
+    e1 = pool_event(t);
     A3G_CUDA(cudaEventRecord(e0, st));
   }
   aa.w1 = t.d_w1;
@@ -848,8 +848,8 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
   if (!fused) {
     cudaEvent_t g0 = nullptr, g1 = nullptr;
     if (record_timing) {
-      A3G_CUDA(cudaEventCreate(&g0));
-      A3G_CUDA(cudaEventCreate(&g1));
+      g0 = pool_event(t);
+      g1 = pool_event(t);
       A3G_CUDA(cudaEventRecord(g0, st));
     }
     launch_h1_tc(t, t.d_agg_inner, aa.n_inner, t.d_h1, st);
@@ -894,8 +894,8 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
     nparts = t.tc_splits;
     cudaEvent_t g0 = nullptr, g1 = nullptr;
     if (record_timing) {
-      A3G_CUDA(cudaEventCreate(&g0));
-      A3G_CUDA(cudaEventCreate(&g1));
+      g0 = pool_event(t);
+      g1 = pool_event(t);
       A3G_CUDA(cudaEventRecord(g0, st));
     }
     launch_dw1_tc(t, t.d_agg_inner, aa.n_inner, t.d_h1, t.d_dh1, t.d_part, nparts, st);

@@ -56,7 +56,9 @@ struct TrainerState {
   cudaEvent_t ev_sampled[kArenas] = {}, ev_consumed[kArenas] = {};
   cudaEvent_t ev_seeds = nullptr;                     // host seeds copied (sampling streams wait on it)
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
-  std::vector<cudaEvent_t> ev_agg;  // pairs around k_agg1 launches (timing)
+  std::vector<cudaEvent_t> ev_agg;  // pairs around k_agg1 launches (timing; events from ev_pool)
+  std::vector<cudaEvent_t> ev_pool;  // timing events, created once and reused across calls
+  size_t ev_used = 0;
   std::vector<cudaEvent_t> ev_h1, ev_dw1;  // pairs around the tcgen05 h1 / dW1 GEMMs (timing)
   double last_h1_ms = 0, last_dw1_ms = 0;
   uint64_t last_gemm_launches = 0;
@@ -75,6 +77,16 @@ struct TrainerState {
   unsigned long long* d_tier_rows = nullptr; // [kMaxTiers] distinct rows gathered per tier
   uint64_t gather_cap = 0;
 };
+
+// A timing event from the trainer's pool (reset by a3g_train_steps_v).
+inline cudaEvent_t pool_event(TrainerState& t) {
+  if (t.ev_used == t.ev_pool.size()) {
+    cudaEvent_t e = nullptr;
+    A3G_CUDA(cudaEventCreate(&e));
+    t.ev_pool.push_back(e);
+  }
+  return t.ev_pool[t.ev_used++];
+}
 
 // Compute part of one step on s_comp for the batch in arena `smp`
 // (gather+aggregate -> forward -> backward -> [allreduce] -> sgd).

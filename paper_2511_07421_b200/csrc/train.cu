@@ -709,6 +709,13 @@ void launch_agg_n(TrainerState& t, const AggArgs& aa, cudaStream_t st) {
     return;
   }
   const uint64_t per_slot = 24ull * (32 / LPR) * aa.view.row_bytes;
+  const uint64_t w1_bytes = HB > 0 ? static_cast<uint64_t>(aa.pitch) * HB * 4 : 0;
+  if (per_slot * 3 + w1_bytes > 227 * 1024) {
+    // wide rows (up to the 8 KB the chunk layout covers): 8 warps x 2 ring
+    // slots stream them instead of refusing the width
+    launch_agg_cfg<T, N, 8, 2, LPR, HB>(t, aa, st);
+    return;
+  }
   if (per_slot * 8 <= 176 * 1024)
     launch_agg_cfg<T, N, 24, 8, LPR, HB>(t, aa, st);
   else if (per_slot * 6 <= 176 * 1024)

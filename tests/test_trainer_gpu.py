@@ -89,6 +89,16 @@ def test_grads_c1_vs_oracle(orc, c1, fanouts, gamma, kind, H):
     _grad_case(orc, g, cache, batches[3], fanouts, gamma, kind, T.sampling_seed(1, 0, 3, 0), H=H)
 
 
+def test_wide_feature_rows(orc):
+    """Rows wider than k_agg1's 24-warp ring (F = 1500 f32, 6 KB) stream
+    through the 8-warp configuration instead of being refused."""
+    g = G.generate_power_law(20_000, 3, 2.5, 1500, 3)
+    cache = CA.build_static_cache(g, CA.CacheConfig(int(0.2 * g.num_nodes) * g.feat_dim * 4, 1))
+    seeds = np.arange(0, 12_000, 23, dtype=np.uint32)
+    _grad_case(orc, g, cache, seeds, [10, 5], 8.0, 0, 17, H=16)
+    _grad_case(orc, g, cache, seeds, [10, 5], 8.0, 0, 17, H=64)
+
+
 @pytest.mark.parametrize("H", [48, 64, 128, 256])
 def test_wide_hidden_on_tcgen05(orc, c1, H):
     """Realistic hidden widths (e.g. 256): h1 and dW1 run

@@ -910,6 +910,7 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
     TrainerState& t = tr->st;
     A3G_CUDA(cudaSetDevice(t.g->device));
     t.last_steps = 0;
+    t.last_seeds_on_device = on_device != 0;
     if (K == 0) return;
     if (off[0] != 0) raise(A3G_ERR_PARAMETER, "train_steps: offsets[0] must be 0");
     for (uint32_t i = 0; i < K; ++i) {
@@ -1219,7 +1220,8 @@ a3g_status a3g_trainer_timing(a3g_trainer* tr, double* total_ms, double* agg_ms,
     // and its split-K reduce when not fused + scale and SGD with a communicator
     if (launches_per_step)
       *launches_per_step = 4 + 6ull * t.L + (t.L ? 1 : 0) + 1 + 6 + (t.h1_fused ? 0 : 1) +
-                           (!t.h1_fused && t.h1_split_used ? 1 : 0) + (t.comm ? 2 : 0);
+                           (!t.h1_fused && t.h1_split_used ? 1 : 0) + (t.comm ? 2 : 0) +
+                           (t.last_seeds_on_device ? 1 : 0);  // k_check_seeds
   });
 }
 

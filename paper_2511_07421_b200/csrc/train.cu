@@ -429,8 +429,9 @@ struct OuterArgs {
   int has_layer0;
 };
 
-// One warp per seed; lane l owns hidden units l, l + 32, ... (H <= 256).
-constexpr int kOuterHB = 8;  // hidden units per lane (H <= 32 * kOuterHB)
+// One warp per seed; lane l owns hidden units l, l + 32, ... (H <= 32 * kOuterHB:
+// 1 unit per lane up to H = 32, 8 up to H = 256).
+template <int kOuterHB>
 __global__ void __launch_bounds__(256) k_outer(OuterArgs a) {
   const int lane = threadIdx.x & 31;
   const uint32_t ns = *a.ns;
@@ -886,7 +887,10 @@ void launch_train_compute(TrainerState& t, a3g_sampler* smp, double lr, double* 
   oa.dagg = t.d_dagg;
   oa.amax = t.d_amax;
   A3G_CUDA(cudaMemsetAsync(t.d_amax, 0, sizeof(uint32_t), st));
-  k_outer<<<std::max(1, static_cast<int>((t.max_seeds + 7) / 8)), 256, 0, st>>>(oa);
+  if (t.H <= 32)
+    k_outer<1><<<std::max(1, static_cast<int>((t.max_seeds + 7) / 8)), 256, 0, st>>>(oa);
+  else
+    k_outer<8><<<std::max(1, static_cast<int>((t.max_seeds + 7) / 8)), 256, 0, st>>>(oa);
   A3G_LAUNCH_DONE("k_outer", st);
   // ---- deterministic scatter into dh1 (fixed-point integer atomics)
   k_dh1_scatter<<<t.sm_count * 2, 256, 0, st>>>(t.d_dagg, t.d_amax, oa.ns, oa.cnt0, oa.sidx0, oa.f0, oa.has_layer0,

@@ -62,6 +62,7 @@ struct TrainerState {
   std::vector<cudaEvent_t> ev_h1, ev_dw1;  // pairs around the tcgen05 h1 / dW1 GEMMs (timing)
   double last_h1_ms = 0, last_dw1_ms = 0;
   uint64_t last_gemm_launches = 0;
+  bool last_seeds_on_device = false;  // the last train_steps call range-checked device seeds
   bool timing = true;
   double last_total_ms = 0, last_agg_ms = 0, last_agg_bytes = 0;
   uint64_t last_agg_launches = 0;

@@ -34,15 +34,17 @@ CONFIGS = {
            "reddit-shaped synthetic 233K nodes / 112.8M edges, 602-d f32, fanout [15,10,5], batch 1024/GPU, "
            "full feature cache"),
     "c1": (100_000, 3, 128, [10, 5], 1024, 0.2,
-           "power-law synthetic 100K nodes / 0.9M edges, 128-d f32, fanout [10,5], batch 1024/GPU, 20% cache"),
+           "power-law synthetic 100K nodes / 0.9M edges, 128-d f32, fanout [10,5], batch 1024/GPU, 20% cache "
+           "(the sampling bias set; feature placement per --store)"),
     "c3": (2_450_000, 9, 100, [15, 10, 5], 4096, 0.2,
            "ogbn-products-shaped synthetic 2.45M nodes / 65M edges, 100-d f32, fanout [15,10,5], batch 4096/GPU, "
-           "20% cache"),
+           "20% cache (the sampling bias set; feature placement per --store)"),
     # papers-scale: topology from the host generator at feat_dim 1, the 128-d
     # features synthesized on the device in bf16 (a3g_graph_synthesize_features)
     "c5": (111_000_000, 5, 128, [15, 10, 5], 8192, 0.2,
            "ogbn-papers100M-shaped synthetic 111M nodes / 1.6B edges, 128-d bf16 (device-synthesized), "
-           "fanout [15,10,5], batch 8192/GPU, 20% cache bias, whole table in HBM"),
+           "fanout [15,10,5], batch 8192/GPU, 20% cache (the sampling bias set; feature placement per --store: "
+           "--store cache = the stated 20% in HBM with pinned-host spill)"),
 }
 SYNTH = {"c5"}  # configs whose features are synthesized on the device (bf16)
 HIDDEN, CLASSES, LR, BASE_SEED = 16, 4, 0.2, 1

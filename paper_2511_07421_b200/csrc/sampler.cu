@@ -35,6 +35,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 
 #include <cub/device/device_radix_sort.cuh>
 
@@ -1900,13 +1901,20 @@ static uint64_t lane_min_rows(bool dense) {
   return dense ? 8192ull : 32768ull;
 }
 
+// A3G_DIAG_SKIP=<stage>[,<stage>...] (diagnostics only, results are wrong):
+// skip a sampler stage to see what bounds the pipelined throughput.
+static bool diag_skip(const char* stage) {
+  static const char* e = std::getenv("A3G_DIAG_SKIP");
+  return e && std::strstr(e, stage) != nullptr;
+}
+
 // aux / ev_fork / ev_join: with A3G_SPLIT_CLS (long items to the lane-group
 // kernel) and A3G_SPLIT_FORK=1, the lane-group launch forks onto the arena's
 // auxiliary stream so it runs beside the lane kernel.
 template <int WM>
 void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_count, cudaStream_t st,
                           cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join) {
-  k_classify<WM><<<sm_count * 2, 256, 0, st>>>(sa);
+  if (!diag_skip("classify")) k_classify<WM><<<sm_count * 2, 256, 0, st>>>(sa);
   A3G_LAUNCH_DONE("k_classify", st);
   if (sa.f <= 32) {
     bool fork = false;
@@ -1980,11 +1988,15 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
           A3G_LAUNCH_DONE("k_stream_lane_mixed", st);
         } else {
           if (sa.f == 5)
-            k_stream_lane<W, 5><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
+          {
+            if (!diag_skip("lane")) k_stream_lane<W, 5><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
+          }
           else if (sa.f <= 8)
             k_stream_lane<W, 8><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
           else if (sa.f == 10)
-            k_stream_lane<W, 10><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
+          {
+            if (!diag_skip("lane")) k_stream_lane<W, 10><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
+          }
           else
             k_stream_lane<W, 16><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
           A3G_LAUNCH_DONE("k_stream_lane", st);
@@ -1996,7 +2008,8 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
       return e ? std::max(1, std::atoi(e)) : 2;  // r01 sweep: 2 (74 CTAs) beat 8 and 4 in the pipeline
     }();
     if (fork) A3G_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
-    k_hub_merge<WM><<<std::max(1, sm_count * merge_ctas_q / 4), kMergeThreads, kMergeSmem, st>>>(sa);
+    if (!diag_skip("merge"))
+      k_hub_merge<WM><<<std::max(1, sm_count * merge_ctas_q / 4), kMergeThreads, kMergeSmem, st>>>(sa);
     A3G_LAUNCH_DONE("k_hub_merge", st);
   }
 }
@@ -2118,8 +2131,10 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
     fa.tag = tag;
     fa.gtag = s.gtag;
     const uint32_t nb = static_cast<uint32_t>((la.cap_rows * la.f + kFinTile - 1) / kFinTile);
-    k_fin_count<<<nb, kFinThreads, 0, st>>>(fa);
-    k_fin_emit<<<nb, kFinThreads, 0, st>>>(fa);
+    if (!diag_skip("fin")) {
+      k_fin_count<<<nb, kFinThreads, 0, st>>>(fa);
+      k_fin_emit<<<nb, kFinThreads, 0, st>>>(fa);
+    }
     A3G_LAUNCH_DONE("layer finalize", st);
   }
   if (s.L) {

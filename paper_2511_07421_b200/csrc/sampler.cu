@@ -635,6 +635,45 @@ __device__ __forceinline__ void lane_argmin(const P& pol, const uint64_t (&rk)[M
   mp = mi;
 }
 
+#ifndef A3G_LANE_FUSED
+#define A3G_LANE_FUSED 1
+#endif
+// A3G_LANE_FUSED=1 variant: the slot update fused with the argmin on the
+// 32-bit key words hk = k >> 21; exact unless another slot's word is within
+// `win` of the minimum's (then lane_argmin decides).
+template <int MB, typename P>
+__device__ __forceinline__ void lane_insert(const P& pol, uint64_t (&rk)[MB], uint32_t (&hk)[MB],
+                                            uint32_t (&rp)[MB], uint32_t m, uint32_t mp_in, uint64_t kx,
+                                            uint32_t pos, uint32_t win, uint64_t& thr, uint32_t& mp) {
+  const uint32_t hx = static_cast<uint32_t>(kx >> 21);
+  uint32_t mnh = 0xffffffffu, mi = 0;
+#pragma unroll
+  for (int i = 0; i < MB; ++i) {
+    if (static_cast<uint32_t>(i) == mp_in) {
+      rk[i] = kx;
+      hk[i] = hx;
+      rp[i] = pos;
+    }
+    if (hk[i] < mnh) {
+      mnh = hk[i];
+      mi = i;
+    }
+  }
+  bool near = false;
+#pragma unroll
+  for (int i = 0; i < MB; ++i) near |= static_cast<uint32_t>(i) != mi && hk[i] - mnh <= win;
+  if (near) {
+    lane_argmin<MB>(pol, rk, m, thr, mp);
+  } else {
+    mp = mi;
+    uint64_t t = rk[0];
+#pragma unroll
+    for (int i = 1; i < MB; ++i)
+      if (static_cast<uint32_t>(i) == mi) t = rk[i];
+    thr = t;
+  }
+}
+
 template <int WM, int MB>
 __global__ void __launch_bounds__(256) k_stream_lane(SampleArgs a, const uint32_t* lists, const uint32_t* cls_count) {
   using P = typename PolOf<WM>::P;
@@ -683,6 +722,13 @@ __global__ void __launch_bounds__(256) k_stream_lane(SampleArgs a, const uint32_
     uint64_t thr;
     uint32_t mp;
     lane_argmin<MB>(pol, rk, m, thr, mp);
+#if A3G_LANE_FUSED
+    uint32_t hk[MB];
+#pragma unroll
+    for (int i = 0; i < MB; ++i) hk[i] = static_cast<uint32_t>(rk[i] >> 21);
+    const uint64_t tw = pol.tie >> 21;
+    const uint32_t win = static_cast<uint32_t>(tw < 0x7fffffffull ? tw : 0x7fffffffull) + 1u;
+#endif
     uint32_t rcnt = nf;
     // ---- replay [p0 + nf, p1) in chunks of 32 positions
     const uint32_t jb = p0 + nf;
@@ -709,18 +755,22 @@ __global__ void __launch_bounds__(256) k_stream_lane(SampleArgs a, const uint32_
           const uint64_t kx = mix64(ctr + static_cast<uint64_t>(c) * kPhi) >> 11;
           if (pol.gt(kx, thr)) {
             const uint32_t pos = jb + b + c;
+            if (seg && rcnt < kRecCap) {
+              rid[rcnt] = pos;
+              rkey[rcnt] = kx;
+            }
+            ++rcnt;
+#if A3G_LANE_FUSED
+            lane_insert<MB>(pol, rk, hk, rp, m, mp, kx, pos, win, thr, mp);
+#else
 #pragma unroll
             for (int i = 0; i < MB; ++i)
               if (static_cast<uint32_t>(i) == mp) {
                 rk[i] = kx;
                 rp[i] = pos;
               }
-            if (seg && rcnt < kRecCap) {
-              rid[rcnt] = pos;
-              rkey[rcnt] = kx;
-            }
-            ++rcnt;
             lane_argmin<MB>(pol, rk, m, thr, mp);
+#endif
           }
         }
       }

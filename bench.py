@@ -63,6 +63,12 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-units", type=int, default=3, help="batches in the bounded cpu_baseline sample")
     p.add_argument("--pipeline", type=int, default=None, help="sampling streams (0 = sequential; default: library's)")
+    p.add_argument("--comm", choices=["nccl", "host"], default="nccl",
+                   help="gradient allreduce at N>1: NCCL over NVLink (default), or the host-transport "
+                        "communicator over gloo (a3g_comm_create_host) -- with --share-device, N ranks on one GPU "
+                        "exercise the multi-process path where NCCL cannot (functional check, not a scaling number)")
+    p.add_argument("--share-device", action="store_true",
+                   help="every rank uses cuda:0 (multi-process functional check on a one-GPU box)")
     p.add_argument("--store", choices=["auto", "hbm", "cache", "sharded"], default="auto",
                    help="feature placement (DESIGN.md 5): hbm = whole table replicated in each GPU's HBM; cache = "
                         "cached rows in HBM, misses in pinned host memory (zero-copy PCIe); sharded = rank r holds "
@@ -283,10 +289,16 @@ def run_reference(args):
 def run_ours(args):
     rank, world, local = dist_env()
     import torch
+    if args.share_device:
+        local = 0
     torch.cuda.set_device(local)
+    host_comm = world > 1 and args.comm == "host"
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if host_comm:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2511_07421_b200 import cache as CA, train as T
     n, m, F, fan, B, frac, desc = CONFIGS[args.config]
     t0 = time.time()
@@ -317,7 +329,15 @@ def run_ours(args):
                 tr.store.open_peer(r, handles[r])
         dist.barrier()
     comm = None
-    if world > 1:
+    if host_comm:
+        import torch.distributed as dist
+
+        def _allreduce(buf):
+            dist.all_reduce(torch.from_numpy(buf), op=dist.ReduceOp.SUM)
+
+        comm = T.Comm.host(world, rank, _allreduce)
+        tr.set_comm(comm)
+    elif world > 1:
         import torch.distributed as dist
         uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
@@ -372,7 +392,7 @@ def run_ours(args):
     tr.set_pipeline(pipe)
     if world > 1:
         import torch.distributed as dist
-        x = torch.tensor([dev_ms, e2e_s], dtype=torch.float64, device="cuda")
+        x = torch.tensor([dev_ms, e2e_s], dtype=torch.float64, device="cpu" if host_comm else "cuda")
         dist.all_reduce(x, op=dist.ReduceOp.MAX)
         dev_ms, e2e_s = float(x[0]), float(x[1])
     if rank != 0:
@@ -432,7 +452,8 @@ def run_ours(args):
         "config": {"workload": args.config, "description": desc, "global_batch": world * B, "batch_per_gpu": B,
                    "fanouts": fan, "gamma": args.gamma, "model": f"2-layer mean-GCN (reference trainer), H={H}, C=4",
                    "hidden": H, "classes": CLASSES, "parallelism": f"dp{world}", "sampling_streams": pipe,
-                   "store": store,
+                   "store": store, "comm": ("host (gloo)" if host_comm else "nccl") if world > 1 else None,
+                   "shared_device": bool(args.share_device),
                    "l2": "inputs larger than L2 (CSR %.0f MB + features %.0f MB)" % (
                        g.num_edges * 4 / 1e6, n * F * (2 if args.config in SYNTH else 4) / 1e6),
                    "graph_gen_s": round(gen_s, 1)},

@@ -101,6 +101,13 @@ __host__ __device__ __forceinline__ double unit_of(uint64_t x) {
 // ------------------------------------------------------------ limits -------
 constexpr int kMaxLayers = 8;
 constexpr uint32_t kInv = 0xffffffffu;
+// Length classes of the stream items (sampler.cu k_item_class): quarter-octave
+// classes keep the items a warp's lanes share within 1.25x of each other's
+// length (A3G_LEN_CLASSES=8: the r01 octave classes)
+#ifndef A3G_LEN_CLASSES
+#define A3G_LEN_CLASSES 32
+#endif
+constexpr int kLenClasses = A3G_LEN_CLASSES;
 constexpr uint32_t kMaxCacheDevices = 64;  // per-device hit counters of the lookup
 
 // Device-resident per-batch counters (one struct per sampler arena).
@@ -115,7 +122,7 @@ struct BatchCounters {
   uint32_t iwork[kMaxLayers];       // stream items claimed per layer
   uint32_t hub_big[kMaxLayers];     // hubs with > 8 segments (block merge)
   uint32_t hub_small[kMaxLayers];   // hubs with 1..8 segments (warp merge)
-  uint32_t icls[kMaxLayers][8];     // stream items per length class (k_item_class)
+  uint32_t icls[kMaxLayers][kLenClasses];  // stream items per length class (k_item_class)
   uint32_t n_seeds;                 // seeds given (incl. duplicates)
   uint32_t hits, misses;            // retrieve_features accounting
   uint32_t pad;

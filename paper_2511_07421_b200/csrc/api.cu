@@ -130,7 +130,7 @@ void sampler_alloc(SamplerState& s, a3g_graph* g, a3g_cache* c, uint32_t max_see
   hb.slot_last = dalloc<uint32_t>(static_cast<size_t>(hb.seg_cap) * 32);
   hb.item_cap = hb.hub_cap + hb.seg_cap;
   hb.items = dalloc<uint4>(hb.item_cap);
-  hb.sort_keys[0] = dalloc<uint32_t>(8ull * hb.item_cap);
+  hb.sort_keys[0] = dalloc<uint32_t>(static_cast<uint64_t>(kLenClasses) * hb.item_cap);
   s.d_ctr = dalloc<BatchCounters>(1);
   A3G_CUDA(cudaMallocHost(&s.h_ctr, sizeof(BatchCounters)));
   A3G_CUDA(cudaMallocHost(&s.h_seeds, max_seeds * sizeof(uint32_t)));

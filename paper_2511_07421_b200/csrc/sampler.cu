@@ -329,11 +329,17 @@ __global__ void __launch_bounds__(256) k_classify(SampleArgs a) {
 // 0 below 64, 7 from 4096): per-class index lists built with warp-aggregated
 // atomics. The lane-group stream kernels claim items longest class first, so
 // a warp's groups carry items within 2x of each other's length.
-constexpr int kClasses = 8;
+constexpr int kClasses = kLenClasses;
 
 __device__ __forceinline__ uint32_t len_class(uint32_t len) {
   const int l2 = 31 - __clz(max(len, 1u));
-  return static_cast<uint32_t>(min(max(l2 - 5, 0), kClasses - 1));
+  if constexpr (kClasses == 8) {
+    return static_cast<uint32_t>(min(max(l2 - 5, 0), kClasses - 1));
+  } else {
+    // quarter octaves from 32: class 4 (l2 - 5) + the two bits below the leading one
+    const int q = l2 >= 2 ? static_cast<int>((len >> (l2 - 2)) & 3u) : 0;
+    return static_cast<uint32_t>(min(max(4 * (l2 - 5) + q, 0), kClasses - 1));
+  }
 }
 
 __global__ void k_item_class(const uint4* items, const uint32_t* item_count, uint32_t cap, uint32_t* lists,

@@ -92,7 +92,65 @@ __device__ __forceinline__ void ldgsts_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <typename T, int NCH, int WARPS, int S, int LPR, int HB>
+// h1 = relu(x . W1) for NR finished inner rows at once (x pre-scaled, the
+// lane's chunks): one pass over the lane's W1 words serves all NR rows, so
+// the shared-memory W1 traffic per row is 1/NR. Group g owns outputs
+// [g HG, (g+1) HG); per-lane partials, then a recursive-halving reduce over
+// the group's lanes (fixed order).
+template <int NCH, int EPC, int LPR, int HG, int NR>
+__device__ __forceinline__ void h1_rows(const float (&x)[NR][NCH][EPC], const uint32_t (&rows)[NR],
+                                        const float* w1s, uint32_t chunks, uint32_t g, uint32_t gl, uint32_t H,
+                                        float* h1) {
+  float p[NR][HG];
+#pragma unroll
+  for (int r = 0; r < NR; ++r)
+#pragma unroll
+    for (int h = 0; h < HG; ++h) p[r][h] = 0.f;
+#pragma unroll
+  for (int i = 0; i < NCH; ++i) {
+    const uint32_t q = gl + LPR * i;
+    if (q < chunks) {
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) {
+#pragma unroll
+        for (int h4 = 0; h4 < HG / 4; ++h4) {
+          const float4 w = reinterpret_cast<const float4*>(w1s)[((g * (HG / 4) + h4) * EPC + e) * chunks + q];
+#pragma unroll
+          for (int r = 0; r < NR; ++r) {
+            p[r][4 * h4] = fmaf(x[r][i][e], w.x, p[r][4 * h4]);
+            p[r][4 * h4 + 1] = fmaf(x[r][i][e], w.y, p[r][4 * h4 + 1]);
+            p[r][4 * h4 + 2] = fmaf(x[r][i][e], w.z, p[r][4 * h4 + 2]);
+            p[r][4 * h4 + 3] = fmaf(x[r][i][e], w.w, p[r][4 * h4 + 3]);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    uint32_t hidx = 0;
+    int o = LPR / 2;
+#pragma unroll
+    for (int n = HG; n > 1; n >>= 1, o >>= 1) {
+      const bool upper = (gl & static_cast<uint32_t>(o)) != 0;
+#pragma unroll
+      for (int j = 0; j < n / 2; ++j) {
+        const float send = upper ? p[r][j] : p[r][j + n / 2];
+        const float keep = upper ? p[r][j + n / 2] : p[r][j];
+        p[r][j] = keep + __shfl_xor_sync(kFull, send, o);
+      }
+      if (upper) hidx += n / 2;
+    }
+    for (; o > 0; o >>= 1) p[r][0] += __shfl_xor_sync(kFull, p[r][0], o);
+    const uint32_t h = g * HG + hidx;
+    if ((gl & static_cast<uint32_t>(LPR / HG - 1)) == 0 && h < H)
+      h1[static_cast<uint64_t>(rows[r]) * H + h] = fmaxf(p[r][0], 0.f);
+  }
+}
+
+// PAIR (with HB > 0): the h1 epilogue waits for the warp's next finished row
+// and serves both from one pass over W1 (half the shared-memory W1 reads).
+template <typename T, int NCH, int WARPS, int S, int LPR, int HB, bool PAIR = false>
 __global__ void __launch_bounds__(WARPS * 32, 1) k_agg1(const __grid_constant__ AggArgs a) {
   // LPR lanes per source row: short rows (<= 16 chunks) are copied RPI at a
   // time by lane groups; each group sums its own rows, the groups' partial
@@ -137,6 +195,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_agg1(const __grid_constant__ 
   for (int i = 0; i < NCH; ++i)
 #pragma unroll
     for (int e = 0; e < EPC; ++e) acc[i][e] = 0.f;
+  constexpr int HG = HB > 0 ? HB / RPI : 4;
+  float prev[PAIR ? 1 : 1][NCH][EPC];  // PAIR: the finished row awaiting its partner
+  uint32_t prev_row[1] = {0};
+  bool have_prev = false;
   for (;;) {
     // ---- producer: fill the ring
     while (issued - consumed < S && pj < nrows) {
@@ -222,48 +284,36 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_agg1(const __grid_constant__ 
       const float scale = c ? 1.f / static_cast<float>(c) : 1.f;
       float4* out = reinterpret_cast<float4*>(a.agg_inner + static_cast<uint64_t>(srow) * a.pitch);
       if constexpr (HB > 0) {
-        // h1 = relu(agg . W1) for this row: group g owns outputs [g HG, (g+1) HG)
-        // (every group holds the full row sums); per-lane partials over the
-        // lane's chunks, then a recursive-halving reduce over the group's lanes
-        constexpr int HG = HB / RPI;
-        float p[HG];
+        if constexpr (PAIR) {
+          if (!have_prev) {
 #pragma unroll
-        for (int h = 0; h < HG; ++h) p[h] = 0.f;
+            for (int i = 0; i < NCH; ++i)
 #pragma unroll
-        for (int i = 0; i < NCH; ++i) {
-          const uint32_t q = gl + LPR * i;
-          if (q < chunks) {
+              for (int e = 0; e < EPC; ++e) prev[0][i][e] = acc[i][e] * scale;
+            prev_row[0] = srow;
+            have_prev = true;
+          } else {
+            float xx[2][NCH][EPC];
 #pragma unroll
-            for (int e = 0; e < EPC; ++e) {
-              const float x = acc[i][e] * scale;
+            for (int i = 0; i < NCH; ++i)
 #pragma unroll
-              for (int h4 = 0; h4 < HG / 4; ++h4) {
-                const float4 w = reinterpret_cast<const float4*>(w1s)[((g * (HG / 4) + h4) * EPC + e) * chunks + q];
-                p[4 * h4] = fmaf(x, w.x, p[4 * h4]);
-                p[4 * h4 + 1] = fmaf(x, w.y, p[4 * h4 + 1]);
-                p[4 * h4 + 2] = fmaf(x, w.z, p[4 * h4 + 2]);
-                p[4 * h4 + 3] = fmaf(x, w.w, p[4 * h4 + 3]);
+              for (int e = 0; e < EPC; ++e) {
+                xx[0][i][e] = prev[0][i][e];
+                xx[1][i][e] = acc[i][e] * scale;
               }
-            }
+            const uint32_t rr[2] = {prev_row[0], srow};
+            h1_rows<NCH, EPC, LPR, HG, 2>(xx, rr, w1s, chunks, g, gl, a.H, a.h1);
+            have_prev = false;
           }
-        }
-        uint32_t hidx = 0;
-        int o = LPR / 2;
+        } else {
+          float xx[1][NCH][EPC];
 #pragma unroll
-        for (int n = HG; n > 1; n >>= 1, o >>= 1) {
-          const bool upper = (gl & static_cast<uint32_t>(o)) != 0;
+          for (int i = 0; i < NCH; ++i)
 #pragma unroll
-          for (int j = 0; j < n / 2; ++j) {
-            const float send = upper ? p[j] : p[j + n / 2];
-            const float keep = upper ? p[j + n / 2] : p[j];
-            p[j] = keep + __shfl_xor_sync(kFull, send, o);
-          }
-          if (upper) hidx += n / 2;
+            for (int e = 0; e < EPC; ++e) xx[0][i][e] = acc[i][e] * scale;
+          const uint32_t rr[1] = {srow};
+          h1_rows<NCH, EPC, LPR, HG, 1>(xx, rr, w1s, chunks, g, gl, a.H, a.h1);
         }
-        for (; o > 0; o >>= 1) p[0] += __shfl_xor_sync(kFull, p[0], o);
-        const uint32_t h = g * HG + hidx;
-        if ((gl & static_cast<uint32_t>(LPR / HG - 1)) == 0 && h < a.H)
-          a.h1[static_cast<uint64_t>(srow) * a.H + h] = fmaxf(p[0], 0.f);
       }
 #pragma unroll
       for (int i = 0; i < NCH; ++i) {
@@ -279,6 +329,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_agg1(const __grid_constant__ 
       }
       nbytes += static_cast<unsigned long long>(a.F) * 4 + (HB > 0 ? a.H * 4ull : 0ull);  // agg_inner (+h1) row
     }
+  }
+  if constexpr (HB > 0 && PAIR) {
+    if (have_prev) h1_rows<NCH, EPC, LPR, HG, 1>(prev, prev_row, w1s, chunks, g, gl, a.H, a.h1);
   }
   // algorithmic feature bytes: every DISTINCT layer-1 source row once -- the
   // layer-2 frontier is exactly the first-seen set of layer-1 sources
@@ -676,15 +729,28 @@ __global__ void k_sgd(float* w1, float* w2, float* gw, uint32_t FH, uint32_t HC,
   if (blockIdx.x == 0 && threadIdx.x == 0 && loss_slot) *loss_slot = static_cast<double>(gw[FH + HC + 1]) / n;
 }
 
-template <typename T, int N, int W, int S, int LPR, int HB>
+template <typename T, int N, int W, int S, int LPR, int HB, bool PAIR = false>
 void launch_agg_cfg(TrainerState& t, const AggArgs& aa, cudaStream_t st) {
   const size_t ring = static_cast<size_t>(W) * S * (32 / LPR) * aa.view.row_bytes;
   const size_t smem = ring + (HB > 0 ? static_cast<size_t>(aa.pitch) * HB * 4 : 0);
   if (smem > 227 * 1024) raise(A3G_ERR_PARAMETER, "feature row too wide for k_agg1's shared-memory ring");
   const int grid = t.sm_count * (smem * 2 <= 227 * 1024 && W <= 32 ? 2 : 1);
-  A3G_CUDA(cudaFuncSetAttribute(k_agg1<T, N, W, S, LPR, HB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  A3G_CUDA(cudaFuncSetAttribute(k_agg1<T, N, W, S, LPR, HB, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
-  k_agg1<T, N, W, S, LPR, HB><<<grid, W * 32, smem, st>>>(aa);
+  k_agg1<T, N, W, S, LPR, HB, PAIR><<<grid, W * 32, smem, st>>>(aa);
+}
+
+// The paired h1 epilogue (two rows per pass over W1) needs ~128 registers:
+// 16-warp CTAs. Default for long rows (LPR 32: C2 k_agg1 0.528 -> 0.541 of
+// HBM alone); short rows (LPR 8) measured slower (C3 0.347 -> 0.301).
+// A3G_AGG_PAIR=0 disables it, =16 forces it (A/B), =24 (spills) for sweeps.
+static int agg_pair(int lpr) {
+  static const int v = [] {
+    const char* e = std::getenv("A3G_AGG_PAIR");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (v < 0) return lpr == 32 ? 16 : 0;
+  return v == 16 || v == 24 ? v : 0;
 }
 
 // 24 warps per CTA (more warps beat a deeper ring: r01 sweep 8x8 63 us,
@@ -699,6 +765,20 @@ static int agg_warps() {
 
 template <typename T, int N, int LPR, int HB>
 void launch_agg_n(TrainerState& t, const AggArgs& aa, cudaStream_t st) {
+  if constexpr (HB > 0) {
+    if (agg_pair(LPR) == 16) {
+      const uint64_t ps = 16ull * (32 / LPR) * aa.view.row_bytes;
+      if (ps * 4 + static_cast<uint64_t>(aa.pitch) * HB * 4 <= 227 * 1024)
+        launch_agg_cfg<T, N, 16, 4, LPR, HB, true>(t, aa, st);
+      else
+        launch_agg_cfg<T, N, 16, 3, LPR, HB, true>(t, aa, st);
+      return;
+    }
+    if (agg_pair(LPR) == 24) {
+      launch_agg_cfg<T, N, 24, 3, LPR, HB, true>(t, aa, st);
+      return;
+    }
+  }
   if (agg_warps() == 16) {  // smaller CTA footprint (co-residence with sampling CTAs)
     const uint64_t ps = 16ull * (32 / LPR) * aa.view.row_bytes;
     if (ps * 6 <= 120 * 1024)

@@ -254,3 +254,34 @@ def test_pipeline_shapes_bit_identical(c1):
             assert np.array_equal(got[2], ref[2]), n
     with pytest.raises(Exception):
         tr.set_pipeline(9)
+
+
+def test_device_resident_seeds_are_validated(c1):
+    """Seeds already in HBM (a3g_train_steps(..., seeds_on_device=1)): an
+    out-of-range seed is clamped on the device and raises ParameterError at
+    the call's sync (sampler.cpp:92-94); gamma < 1 raises before any launch
+    (assign_weights, sampler.cpp:62); valid device seeds train as host seeds."""
+    import ctypes as C
+    import torch
+    from paper_2511_07421_b200._lib import ParameterError, check, f64p, lib, ptr, u64p
+    g = c1
+    cache = CA.build_static_cache(g, CA.CacheConfig(int(0.2 * g.num_nodes) * g.feat_dim * 4, 1))
+    tr = T.Trainer(g, cache, T.ModelSpec(g.feat_dim, 16, 4), [10, 5], max_seeds=256)
+    rs = np.array([T.sampling_seed(1, 0, s, 0) for s in range(2)], dtype=np.uint64)
+    losses = np.empty(2)
+
+    def run(seeds, gamma=8.0):
+        d = torch.from_numpy(np.ascontiguousarray(seeds, dtype=np.int32)).cuda()
+        check(lib().a3g_train_steps(tr.h, C.cast(C.c_void_p(d.data_ptr()), C.POINTER(C.c_uint32)), seeds.shape[1],
+                                    2, ptr(rs, u64p), gamma, 0, 1, ptr(losses, f64p)))
+        return losses.copy()
+
+    good = np.stack(T.plan_epoch_batches(g.train_nodes, 0, 256, 9)[:2])
+    ref = T.Trainer(g, cache, T.ModelSpec(g.feat_dim, 16, 4), [10, 5], max_seeds=256).steps(good, rs, 8.0, 0)
+    np.testing.assert_array_equal(run(good), ref)
+    bad = good.copy()
+    bad[1, 7] = g.num_nodes + 5
+    with pytest.raises(ParameterError, match="seed out of range"):
+        run(bad)
+    with pytest.raises(ParameterError, match="gamma"):
+        run(good, gamma=0.5)

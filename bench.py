@@ -368,6 +368,7 @@ def run_ours(args):
         barrier()
     tm = tr.timing()
     dev_ms = tm["total_ms"]
+    st_dev = tr.step_stats(K)
     # ---- e2e: host seeds through the C-ABI (H2D in the region, losses D2H)
     barrier()
     t1 = time.perf_counter()
@@ -425,6 +426,16 @@ def run_ours(args):
         res[name] = {"bytes_per_launch": b, "achieved": a, "peak": peak, "peak_kind": kind,
                      "frac": a / peak if peak else None}
     bound = max(res, key=lambda k: res[k]["frac"] or 0.0) if res else None
+    # the sampler's work: neighbour positions drawn per step (sum of frontier
+    # degrees, one draw per neighbour, sampler.cpp:22-27) over the step time,
+    # against the hash prefilter's measured ALU ceiling
+    pos = float(st_dev[:, T.STAT_POSITIONS].mean())
+    tpos = pos / (dev_ms / K * 1e-3) / 1e12 if dev_ms > 0 else 0.0
+    sampler = {"positions_per_step": pos, "achieved_tpos_s": tpos, "ceiling_tpos_s": 1.37,
+               "ceiling_kind": "measured hash-prefilter throughput, one B200 (tools/microbench/hash_pipes.cu)",
+               "frac": tpos / 1.37,
+               "note": "positions over the whole pipelined step time: the sampler shares the GPU with the gather "
+                       "and the dense update"}
     # the dense update on the tensor cores (H > 16): algorithmic flops of
     # h1 = agg W1 and dW1 = agg^T G (2 n_inner F H each) over their launch time
     tensor = None
@@ -471,6 +482,7 @@ def run_ours(args):
                                       "the max over resources"},
         "e2e": {"value": e2e, "unit": "seeds/s", "h2d_bytes_per_step": B * 4, "d2h_bytes_per_step": 8},
         "tensor_roofline": tensor,
+        "sampler": sampler,
         "gpu_launches": int(tm["launches_per_step"]) * K,
         "clocks": clk.summary(),
         "loss_first_last": [float(losses[0]), float(losses_e2e[-1])],

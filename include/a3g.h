@@ -50,6 +50,7 @@ enum {
   A3G_STAT_HITS = 4,   /* cache hits over unique_nodes (cache.cpp:48-68) */
   A3G_STAT_MISSES = 5,
   A3G_STAT_BAD_SEEDS = 6, /* device-resident seeds >= num_nodes (the call raised ParameterError) */
+  A3G_STAT_POSITIONS = 7, /* neighbour positions drawn: sum of frontier degrees (the sampler work) */
   A3G_STEP_STATS = 8
 };
 

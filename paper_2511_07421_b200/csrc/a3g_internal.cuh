@@ -127,6 +127,8 @@ struct BatchCounters {
   uint32_t hits, misses;            // retrieve_features accounting
   uint32_t pad;
   uint32_t bad_seeds;               // device-resident seeds >= n seen (k_check_seeds; raised after sync)
+  uint32_t pad2;
+  unsigned long long positions;     // neighbour positions drawn (sum of frontier degrees, all layers)
 };
 
 // ------------------------------------------------------------ feature store -

@@ -75,6 +75,7 @@ struct SampleArgs {
   uint32_t* small_count;  // hubs with 1..kMergeFilterWarps segments (merge_small_hub)
   uint32_t* item_count;
   uint32_t* item_work;
+  unsigned long long* positions;  // BatchCounters::positions
   uint64_t seed;
   double gamma, inv_gamma;
   uint64_t tie;
@@ -301,6 +302,12 @@ __global__ void __launch_bounds__(256) k_classify(SampleArgs a) {
         n_items = 1;
       }
     }
+    // draws of the batch: one per neighbour of every frontier row (sampler.cpp:22-27, the
+    // reference draws fill keys too; the device hashes only rows past their fill)
+    unsigned long long hp = valid ? deg : 0ull;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) hp += __shfl_xor_sync(kFull, hp, off);
+    if (lane == 0 && hp) atomicAdd(a.positions, hp);
     // ---- warp-aggregated append of the items
     uint32_t incl = n_items;
 #pragma unroll
@@ -2151,6 +2158,7 @@ void launch_sample(SamplerState& s, uint32_t n_seeds, double gamma, int kind, ui
     sa.small_count = &ctr->hub_small[l];
     sa.item_count = &ctr->items[l];
     sa.item_work = &ctr->iwork[l];
+    sa.positions = &ctr->positions;
     sa.seed = rng_seed;
     sa.gamma = gamma;
     sa.inv_gamma = 1.0 / gamma;

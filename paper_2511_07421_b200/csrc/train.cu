@@ -458,6 +458,7 @@ __global__ void k_step_stats(const BatchCounters* ctr, const uint32_t* unique, c
     out[A3G_STAT_INNER] = L >= 1 ? ctr->ucount[1] : ctr->ucount[0];
     out[A3G_STAT_SEEDS] = ctr->ucount[0];
     out[A3G_STAT_BAD_SEEDS] = ctr->bad_seeds;
+    out[A3G_STAT_POSITIONS] = ctr->positions;
     if (ctr->bad_seeds && err) atomicOr(err, 1ull);
     // misses = U - hits, derived on the host (a3g_trainer_step_stats)
   }

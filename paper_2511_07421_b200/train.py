@@ -18,7 +18,8 @@ from .graph import STORE_HBM, DeviceGraph, Graph, Store
 from .sampling import SamplerKind
 
 
-STAT_UNIQUE, STAT_EDGES, STAT_INNER, STAT_SEEDS, STAT_HITS, STAT_MISSES, STEP_STATS = 0, 1, 2, 3, 4, 5, 8
+STAT_UNIQUE, STAT_EDGES, STAT_INNER, STAT_SEEDS, STAT_HITS, STAT_MISSES, STAT_BAD_SEEDS, STAT_POSITIONS = range(8)
+STEP_STATS = 8
 
 
 @dataclass
@@ -217,7 +218,8 @@ class Trainer:
         return losses
 
     def step_stats(self, K: int) -> np.ndarray:
-        """u64[K, 8] rows (STAT_UNIQUE, EDGES, INNER, SEEDS, HITS, MISSES) of the last steps call."""
+        """u64[K, 8] rows (STAT_UNIQUE, EDGES, INNER, SEEDS, HITS, MISSES, BAD_SEEDS, POSITIONS) of the
+        last steps call."""
         out = np.zeros((K, STEP_STATS), dtype=np.uint64)
         check(lib().a3g_trainer_step_stats(self.h, ptr(out, u64p), K))
         return out

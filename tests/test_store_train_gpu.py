@@ -81,6 +81,7 @@ def test_step_stats_match_oracle_batches(orc, c1):
         assert st[i, T.STAT_EDGES] == b.total_edges()
         assert st[i, T.STAT_SEEDS] == b.num_seed_unique
         assert st[i, T.STAT_HITS] == hits and st[i, T.STAT_MISSES] == len(b.unique_nodes) - hits
+        assert st[i, T.STAT_POSITIONS] == b.keys_scanned  # one draw per neighbour of every frontier row
 
 
 def test_retrieve_features_through_store(c1):

@@ -80,24 +80,116 @@ def plan_epoch_batches(train_nodes, epoch: int, batch_size: int, seed: int):
     return [o[i:i + batch_size] for i in range(0, len(o), batch_size)]
 
 
-def sgd_step(w: np.ndarray, g: np.ndarray, lr: float) -> None:
-    """trainer.cpp:208-211 (host arrays)."""
-    w += (-lr) * g
+def sgd_step(w: np.ndarray, g: np.ndarray, lr: float, fused: int = 0) -> None:
+    """trainer.cpp:208-211 on the device (a3g_sgd_step): w += (-lr) * g in
+    place, f64; the first `fused` elements as one fused multiply-add (the
+    reference's AVX2 kernel table fuses n - n % 4), the rest rounded
+    separately (its scalar table)."""
+    w = np.asarray(w)
+    if w.dtype != np.float64 or not w.flags.c_contiguous:
+        raise ParameterError("sgd_step: weights must be a contiguous f64 array")
+    gg = np.ascontiguousarray(g, dtype=np.float64)
+    if gg.size != w.size:
+        raise ParameterError("sgd_step: shape mismatch")
+    check(lib().a3g_sgd_step(0, ptr(w, f64p), ptr(gg, f64p), w.size, int(fused), float(lr)))
 
 
 def sync_gradients(grads):
-    """trainer.cpp:213-229: element-wise mean of a list of (gw1, gw2)."""
+    """trainer.cpp:213-229 on the device (a3g_mean_gradients): element-wise
+    mean of a list of (gw1, gw2), summed in list order then x (1/k)."""
     if not grads:
         raise ParameterError("sync_gradients: empty gradient list")
-    s1 = np.zeros_like(grads[0][0])
-    s2 = np.zeros_like(grads[0][1])
-    for a, b in grads:
-        if a.shape != s1.shape or b.shape != s2.shape:
+    out = []
+    for part in (0, 1):
+        arrs = [np.ascontiguousarray(gr[part], dtype=np.float64) for gr in grads]
+        if any(a.shape != arrs[0].shape for a in arrs):
             raise ParameterError("sync_gradients: shape mismatch")
-        s1 += a
-        s2 += b
-    inv = 1.0 / len(grads)
-    return s1 * inv, s2 * inv
+        res = np.empty_like(arrs[0])
+        ptrs = (f64p * len(arrs))(*[ptr(a, f64p) for a in arrs])
+        check(lib().a3g_mean_gradients(0, ptrs, len(arrs), res.size, ptr(res, f64p)))
+        out.append(res)
+    return out[0], out[1]
+
+
+class BatchModel:
+    """trainer.cpp:34-239 on an explicit batch (a3g_batch_model_*): the
+    reference's SampleBatch + the feats the caller gathered, through the
+    pipeline's own device kernels."""
+
+    def __init__(self, spec: ModelSpec, device: int = 0):
+        h = vp()
+        check(lib().a3g_batch_model_create(device, spec.feat_dim, spec.hidden_dim, spec.num_classes, C.byref(h)))
+        self.h, self.spec = h, spec
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().a3g_batch_model_destroy(self.h)
+        except Exception:
+            pass
+
+    def load(self, batch, feats, seed_labels=None) -> int:
+        layers = list(batch.layers)[:2]
+        L = len(layers)
+        keep = []
+        ne = np.array([len(d) for d, _ in layers] + [0], dtype=np.uint64)
+        D = (u32p * max(L, 1))()
+        S = (u32p * max(L, 1))()
+        for i, (d, s_) in enumerate(layers):
+            d = np.ascontiguousarray(d, dtype=np.uint32)
+            s_ = np.ascontiguousarray(s_, dtype=np.uint32)
+            keep += [d, s_]
+            D[i], S[i] = ptr(d, u32p), ptr(s_, u32p)
+        f = np.ascontiguousarray(feats, dtype=np.float32)
+        lab = None if seed_labels is None else np.ascontiguousarray(seed_labels, dtype=np.uint32)
+        ni = C.c_uint64()
+        check(lib().a3g_batch_model_load(self.h, len(batch.unique_nodes), batch.num_seed_unique, L, ptr(ne, u64p), D,
+                                         S, ptr(f, C.POINTER(C.c_float)), None if lab is None else ptr(lab, u32p),
+                                         C.byref(ni)))
+        return ni.value
+
+    def run(self, w1, w2):
+        a = np.ascontiguousarray(w1, dtype=np.float64)
+        b = np.ascontiguousarray(w2, dtype=np.float64)
+        loss = C.c_double()
+        g1, g2 = np.empty_like(a), np.empty_like(b)
+        check(lib().a3g_batch_model_run(self.h, ptr(a, f64p), ptr(b, f64p), C.byref(loss), ptr(g1, f64p),
+                                        ptr(g2, f64p)))
+        return loss.value, (g1, g2)
+
+
+def forward(model, batch, feats, spec: ModelSpec, device: int = 0) -> dict:
+    """trainer.cpp:59-137 on the device: the ForwardResult arrays (inner_nodes,
+    inner_pos, inner_deg, outer_deg, agg_inner, h1, agg_outer, logits)."""
+    bm = BatchModel(spec, device)
+    ni = bm.load(batch, feats)
+    bm.run(*model)
+    F, H, Cc = spec.feat_dim, spec.hidden_dim, spec.num_classes
+    ns, U = batch.num_seed_unique, len(batch.unique_nodes)
+    out = dict(inner_nodes=np.empty(ni, np.uint32), inner_pos=np.empty(U, np.int32), inner_deg=np.empty(ni, np.uint32),
+               outer_deg=np.empty(ns, np.uint32), agg_inner=np.empty(ni * F), h1=np.empty(ni * H),
+               agg_outer=np.empty(ns * H), logits=np.empty(ns * Cc))
+    check(lib().a3g_batch_model_forward(bm.h, ptr(out["inner_nodes"], u32p), ptr(out["inner_pos"], i32p),
+                                        ptr(out["inner_deg"], u32p), ptr(out["outer_deg"], u32p),
+                                        ptr(out["agg_inner"], f64p), ptr(out["h1"], f64p),
+                                        ptr(out["agg_outer"], f64p), ptr(out["logits"], f64p)))
+    return out
+
+
+def backward(model, batch, feats, seed_labels, spec: ModelSpec, device: int = 0):
+    """trainer.cpp:139-206 on the device (the forward is recomputed there):
+    (loss, (gw1, gw2))."""
+    if len(seed_labels) != batch.num_seed_unique:
+        raise ParameterError("backward: seed_labels size mismatch")
+    bm = BatchModel(spec, device)
+    bm.load(batch, feats, seed_labels)
+    return bm.run(*model)
+
+
+def grad_on_batch(model, g: Graph, batch, feats, spec: ModelSpec, device: int = 0):
+    """trainer.cpp:231-239: labels of the unique seeds from the graph, then backward."""
+    labels = g.labels[np.asarray(batch.unique_nodes[:batch.num_seed_unique], dtype=np.int64)]
+    return backward(model, batch, feats, labels, spec, device)
 
 
 class Trainer:

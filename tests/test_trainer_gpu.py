@@ -227,3 +227,46 @@ def test_sgd_lr_zero_keeps_weights(c1):
     tr.step(np.arange(256), lr=0.0)
     w2 = tr.get_weights()
     assert np.array_equal(w[0], w2[0]) and np.array_equal(w[1], w2[1])
+
+
+def test_explicit_batch_model_api(orc, c1):
+    """trainer.cpp:59-239 on the caller's own batch (the drop-in's forward /
+    backward / grad_on_batch path, a3g_batch_model_*): the oracle's batch and
+    rows in, ForwardResult index arrays identical to the oracle's, values and
+    gradients within 1e-3; sgd_step / sync_gradients on the device are
+    bit-identical to the reference's scalar arithmetic."""
+    g = c1
+    cache = CA.build_static_cache(g, CA.CacheConfig(int(0.2 * g.num_nodes) * g.feat_dim * 4, 1))
+    seeds = np.arange(0, 60_000, 71, dtype=np.uint32)
+    b = orc.sample_khop(g, seeds, [10, 5], 8.0, 0, 31, cache.device_map)
+    feats = np.ascontiguousarray(g.features[b.unique_nodes])
+    spec = T.ModelSpec(128, 16, 4)
+    w1, w2 = T.init_model(spec, 1)
+    labels = g.labels[b.unique_nodes[:b.num_seed_unique]]
+    ref = orc.grad_on_edges(128, 16, 4, w1, w2, len(b.unique_nodes), b.num_seed_unique, b.layers, feats, labels)
+    fwd = T.forward((w1, w2), b, feats, spec)
+    # inner nodes: unique seeds, then first-seen layer-0 sources (trainer.cpp:76-89)
+    want_inner = list(range(b.num_seed_unique))
+    seen = set(want_inner)
+    for s_ in b.layers[0][1]:
+        if int(s_) not in seen:
+            seen.add(int(s_))
+            want_inner.append(int(s_))
+    assert np.array_equal(fwd["inner_nodes"], np.array(want_inner, np.uint32))
+    assert np.array_equal(fwd["outer_deg"], np.bincount(b.layers[0][0], minlength=b.num_seed_unique)[:b.num_seed_unique])
+    assert rel_err(fwd["logits"], ref["logits"]) < TOL
+    loss, (g1, g2) = T.backward((w1, w2), b, feats, labels, spec)
+    assert abs(loss - ref["loss"]) <= TOL * abs(ref["loss"])
+    assert rel_err(g1, ref["gw1"]) < TOL and rel_err(g2, ref["gw2"]) < TOL
+    loss2, (h1, h2) = T.grad_on_batch((w1, w2), g, b, feats, spec)
+    assert loss2 == loss and np.array_equal(h1, g1)
+    # device sync / SGD vs the reference's scalar table: sum in order, x 1/k; w + (-lr) g
+    a1, a2 = T.init_model(spec, 11)
+    c1_, c2_ = T.init_model(spec, 12)
+    m1, m2 = T.sync_gradients([(a1, a2), (c1_, c2_), (a1, a2)])
+    assert np.array_equal(m1, ((0.0 + a1) + c1_ + a1) * (1.0 / 3.0)) and np.array_equal(m2, ((0.0 + a2) + c2_ + a2) * (1.0 / 3.0))
+    w = w1.copy()
+    T.sgd_step(w, m1, 0.2)
+    assert np.array_equal(w, w1 + (-0.2) * m1)
+    with pytest.raises(Exception):
+        T.sync_gradients([])

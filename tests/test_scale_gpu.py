@@ -111,6 +111,15 @@ def test_c3_products_shaped(orc, c3, gamma):
 def c5():
     g = G.generate_power_law(111_000_000, 5, 2.5, 1, 1)
     assert g.num_edges == 1_607_919_973  # SURVEY 8(d) probe of the reference generator
+    # bit-identical to the compiled reference's own 1.6B-edge graph (sha256 of
+    # every array, tests/golden/make_generator_hashes.py: 2021 s single-threaded)
+    import hashlib
+    import json
+    import os
+    rec = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                                      "generator_hashes.json")))["c5"]
+    for arr in ("row_offsets", "col_indices", "features", "labels", "train_mask", "test_mask"):
+        assert hashlib.sha256(memoryview(np.ascontiguousarray(getattr(g, arr))).cast("B")).hexdigest() == rec[arr], arr
     return g
 
 

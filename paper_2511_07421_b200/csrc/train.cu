@@ -341,6 +341,181 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_agg1(const __grid_constant__ 
   if (lane == 0 && nbytes) atomicAdd(a.bytes, nbytes);
 }
 
+// Long rows (one row per warp step, LPR 32): the same gather + mean + fused
+// h1 epilogue with each source row moved by ONE TMA bulk copy
+// (cp.async.bulk, completion on the slot's mbarrier) that lane 0 issues,
+// instead of per-lane 16-byte LDGSTS with their per-chunk address and
+// predicate work. The slot's (row, count|last) record travels through shared
+// memory beside it (written before the arrive, read after the wait), so the
+// per-source-row work is one shuffle + one bulk issue on the producer side and
+// one barrier poll + the lane's chunk sums on the consumer side. The warp's
+// __syncwarp before each refill orders every lane's reads of the slots being
+// reused before lane 0's next copy into them (consumer release).
+// source id of a layer-1 slot beyond the first 32 (out of line: rare)
+__device__ __noinline__ uint32_t agg_src_far(const uint32_t* S1, int32_t pk, uint32_t f1, uint32_t t) {
+  return __ldg(S1 + static_cast<uint64_t>(pk) * f1 + t);
+}
+
+template <typename T, int NCH, int WARPS, int S, int HB, bool PAIR, bool IDENT>
+__global__ void __launch_bounds__(WARPS * 32, 1) k_agg1_tma(const __grid_constant__ AggArgs a) {
+  static_assert((S & (S - 1)) == 0, "ring depth must be a power of two");
+  using Ch = Chunk<T>;
+  constexpr int EPC = Ch::EPC;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t bars[WARPS * S];
+  __shared__ uint2 smeta[WARPS * S];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t rb = a.view.row_bytes;  // == chunks * 16
+  const uint32_t n_inner = *a.n_inner;
+  const uint32_t chunks = a.pitch / EPC;
+  const uint32_t gw = blockIdx.x * WARPS + warp, nw = gridDim.x * WARPS;
+  float* w1s = reinterpret_cast<float*>(smem + static_cast<size_t>(WARPS) * S * rb);
+  for (int i = threadIdx.x; i < WARPS * S; i += WARPS * 32) ptx::mbar_init(&bars[i], 1);
+  ptx::fence_mbar_init();
+  if constexpr (HB > 0) {
+    // W1 [F][H] -> [h/4][e][q][h%4] (feature f = q EPC + e), zero padded to
+    // the pitch and to HB outputs; source order (f, h): no divisions
+    for (uint32_t i = threadIdx.x; i < a.pitch * HB; i += WARPS * 32) {
+      const uint32_t f = i / HB, h = i % HB, q = f / EPC, e = f % EPC;
+      w1s[(((h >> 2) * EPC + e) * chunks + q) * 4 + (h & 3)] =
+          (f < a.F && h < a.H) ? __ldg(a.w1 + static_cast<size_t>(f) * a.H + h) : 0.f;
+    }
+  }
+  __syncthreads();
+  // the warp's ring, barriers and slot records as shared-window addresses
+  const uint32_t ring_s = ptx::smem_u32(smem) + static_cast<uint32_t>(warp) * S * rb;
+  const uint32_t bar_s = ptx::smem_u32(bars) + static_cast<uint32_t>(warp) * S * 8;
+  const uint32_t meta_s = ptx::smem_u32(smeta) + static_cast<uint32_t>(warp) * S * 8;
+  const uint32_t lane_s = ring_s + static_cast<uint32_t>(lane) * 16;  // this lane's chunk q = lane of slot 0
+  const uint32_t nrows = gw < n_inner ? (n_inner - gw + nw - 1) / nw : 0;
+  const uint8_t* base0 = a.view.base[0];
+  unsigned long long nbytes = 0;
+  uint32_t pj = 0, pt = 0, pc = 0, batch = ~0u, src_lane = 0, r = 0;
+  int32_t meta_k = -1, pk = -1;
+  uint32_t meta_c = 0;
+  bool row_ready = false;
+  uint32_t issued = 0, consumed = 0;
+  float acc[NCH][EPC];
+#pragma unroll
+  for (int i = 0; i < NCH; ++i)
+#pragma unroll
+    for (int e = 0; e < EPC; ++e) acc[i][e] = 0.f;
+  constexpr int HG = HB > 0 ? HB : 4;
+  float prev[1][NCH][EPC];
+  uint32_t prev_row[1] = {0};
+  bool have_prev = false;
+  for (;;) {
+    __syncwarp();  // consumer release of the slots refilled below
+    while (issued - consumed < S && pj < nrows) {
+      if (!row_ready) {
+        r = gw + pj * nw;
+        if ((pj >> 5) != batch) {
+          batch = pj >> 5;
+          const uint32_t rr = gw + (batch * 32 + lane) * nw;
+          meta_k = -1;
+          meta_c = 0;
+          if (batch * 32 + lane < nrows && a.has_layer1) {
+            meta_k = __ldg(a.inv1 + rr);
+            meta_c = meta_k >= 0 ? __ldg(a.cnt1 + meta_k) : 0u;
+          }
+        }
+        pk = __shfl_sync(kFull, meta_k, pj & 31);
+        pc = __shfl_sync(kFull, meta_c, pj & 31);
+        src_lane = lane < static_cast<int>(pc) ? __ldg(a.S1 + static_cast<uint64_t>(pk) * a.f1 + lane) : 0u;
+        if (pc == 0) src_lane = __ldg(a.unique + r);  // self-fallback: own features (trainer.cpp:102-107)
+        nbytes += pc ? static_cast<unsigned long long>(pc) * 4 + 8 : static_cast<unsigned long long>(a.F) * sizeof(T) + 4;
+        row_ready = true;
+      }
+      uint32_t v = __shfl_sync(kFull, src_lane, pt & 31);
+      if (pt >= 32) [[unlikely]]
+        v = agg_src_far(a.S1, pk, a.f1, pt);  // fanout > 32
+      const bool last = pt + 1 >= (pc ? pc : 1u);
+      if (lane == 0) {
+        const uint32_t slot = issued & (S - 1);
+        ptx::sts_v2(meta_s + slot * 8, r, pc | (last ? 0x80000000u : 0u));
+        const uint8_t* src = IDENT ? base0 + static_cast<uint64_t>(v) * rb : row_ptr(a.view, v);
+        ptx::mbar_arrive_expect_tx_s(bar_s + slot * 8, rb);
+        ptx::bulk_g2s_s(ring_s + slot * rb, src, rb, bar_s + slot * 8);
+      }
+      ++issued;
+      if (last) {
+        ++pj;
+        pt = 0;
+        row_ready = false;
+      } else {
+        ++pt;
+      }
+    }
+    if (consumed == issued) break;
+    const uint32_t slot = consumed & (S - 1);
+    ptx::mbar_wait_s(bar_s + slot * 8, (consumed / S) & 1u);
+    const uint2 md = ptx::lds_v2(meta_s + slot * 8);
+    const uint32_t row_s = lane_s + slot * rb;
+#pragma unroll
+    for (int i = 0; i < NCH; ++i) {
+      const uint32_t q = lane + 32 * i;
+      if (q < chunks) Ch::add(acc[i], ptx::lds_v4(row_s + 512 * i));
+    }
+    ++consumed;
+    if (md.y & 0x80000000u) {
+      const uint32_t srow = md.x, c = md.y & 0x7fffffffu;
+      const float scale = c ? 1.f / static_cast<float>(c) : 1.f;
+      float4* out = reinterpret_cast<float4*>(a.agg_inner + static_cast<uint64_t>(srow) * a.pitch);
+      if constexpr (HB > 0) {
+        if constexpr (PAIR) {
+          if (!have_prev) {
+#pragma unroll
+            for (int i = 0; i < NCH; ++i)
+#pragma unroll
+              for (int e = 0; e < EPC; ++e) prev[0][i][e] = acc[i][e] * scale;
+            prev_row[0] = srow;
+            have_prev = true;
+          } else {
+            float xx[2][NCH][EPC];
+#pragma unroll
+            for (int i = 0; i < NCH; ++i)
+#pragma unroll
+              for (int e = 0; e < EPC; ++e) {
+                xx[0][i][e] = prev[0][i][e];
+                xx[1][i][e] = acc[i][e] * scale;
+              }
+            const uint32_t rr[2] = {prev_row[0], srow};
+            h1_rows<NCH, EPC, 32, HG, 2>(xx, rr, w1s, chunks, 0, lane, a.H, a.h1);
+            have_prev = false;
+          }
+        } else {
+          float xx[1][NCH][EPC];
+#pragma unroll
+          for (int i = 0; i < NCH; ++i)
+#pragma unroll
+            for (int e = 0; e < EPC; ++e) xx[0][i][e] = acc[i][e] * scale;
+          const uint32_t rr[1] = {srow};
+          h1_rows<NCH, EPC, 32, HG, 1>(xx, rr, w1s, chunks, 0, lane, a.H, a.h1);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NCH; ++i) {
+        const uint32_t q = lane + 32 * i;
+        if (q < chunks) {
+#pragma unroll
+          for (int e = 0; e < EPC; e += 4)
+            out[q * (EPC / 4) + e / 4] = make_float4(acc[i][e] * scale, acc[i][e + 1] * scale,
+                                                     acc[i][e + 2] * scale, acc[i][e + 3] * scale);
+        }
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) acc[i][e] = 0.f;
+      }
+      nbytes += static_cast<unsigned long long>(a.F) * 4 + (HB > 0 ? a.H * 4ull : 0ull);  // agg_inner (+h1) row
+    }
+  }
+  if constexpr (HB > 0 && PAIR) {
+    if (have_prev) h1_rows<NCH, EPC, 32, HG, 1>(prev, prev_row, w1s, chunks, 0, lane, a.H, a.h1);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && a.n_distinct)
+    nbytes += *a.n_distinct * static_cast<unsigned long long>(a.F) * sizeof(T);
+  if (lane == 0 && nbytes) atomicAdd(a.bytes, nbytes);
+}
+
 // dW1 = agg_inner^T . G, G = dh1 * [h1 > 0] (trainer.cpp:203-204), on the
 // CUDA cores: an HBM-bound skinny product (N = H <= 32) -- one pass over
 // agg_inner at full bandwidth beats staging 3-term bf16 operands for tcgen05
@@ -764,8 +939,41 @@ static int agg_warps() {
   return v;
 }
 
+// TMA bulk-copy gather for long rows (default; A3G_AGG_TMA=0 selects the
+// per-lane LDGSTS kernel for A/B).
+static bool agg_tma() {
+  static const bool v = [] {
+    const char* e = std::getenv("A3G_AGG_TMA");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return v;
+}
+
+template <typename T, int N, int HB>
+bool launch_agg_tma(TrainerState& t, const AggArgs& aa, cudaStream_t st) {
+  constexpr int W = N <= 8 ? 16 : 8;
+  constexpr int S = N <= 5 ? 4 : 2;
+  const size_t ring = static_cast<size_t>(W) * S * aa.view.row_bytes;
+  const size_t smem = ring + (HB > 0 ? static_cast<size_t>(aa.pitch) * HB * 4 : 0);
+  const size_t stat = static_cast<size_t>(W) * S * (sizeof(uint64_t) + sizeof(uint2));
+  if (smem + stat > 227 * 1024) return false;
+  if (aa.view.loc == nullptr) {
+    A3G_CUDA(cudaFuncSetAttribute(k_agg1_tma<T, N, W, S, HB, (HB > 0), true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k_agg1_tma<T, N, W, S, HB, (HB > 0), true><<<t.sm_count, W * 32, smem, st>>>(aa);
+  } else {
+    A3G_CUDA(cudaFuncSetAttribute(k_agg1_tma<T, N, W, S, HB, (HB > 0), false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k_agg1_tma<T, N, W, S, HB, (HB > 0), false><<<t.sm_count, W * 32, smem, st>>>(aa);
+  }
+  return true;
+}
+
 template <typename T, int N, int LPR, int HB>
 void launch_agg_n(TrainerState& t, const AggArgs& aa, cudaStream_t st) {
+  if constexpr (LPR == 32) {
+    if (agg_tma() && launch_agg_tma<T, N, HB>(t, aa, st)) return;
+  }
   if constexpr (HB > 0) {
     if (agg_pair(LPR) == 16) {
       const uint64_t ps = 16ull * (32 / LPR) * aa.view.row_bytes;

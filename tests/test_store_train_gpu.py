@@ -38,9 +38,15 @@ def _steps(tr, g, K=4, B=512, gamma=8.0):
     return losses, tr.get_weights(), tr.step_stats(K)
 
 
-@pytest.mark.parametrize("feat_dtype", [0, 1])
-def test_store_policies_bit_identical(c1, feat_dtype):
-    g = c1
+@pytest.fixture(scope="module")
+def c1w():
+    """Long rows (300-d: the TMA bulk-copy gather) for the store tiers."""
+    return G.generate_power_law(60_000, 3, 2.5, 300, 1)
+
+
+@pytest.mark.parametrize("feat_dtype,wide", [(0, False), (1, False), (0, True)])
+def test_store_policies_bit_identical(c1, c1w, feat_dtype, wide):
+    g = c1w if wide else c1
     spec = T.ModelSpec(g.feat_dim, 16, 4)
     cache2 = CA.build_static_cache(g, CA.CacheConfig(int(0.1 * g.num_nodes) * g.feat_dim * 4, 2))
     base = T.Trainer(g, cache2, spec, [10, 5], max_seeds=512, feat_dtype=feat_dtype)

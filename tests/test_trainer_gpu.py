@@ -99,6 +99,48 @@ def test_wide_feature_rows(orc):
     _grad_case(orc, g, cache, seeds, [10, 5], 8.0, 0, 17, H=64)
 
 
+@pytest.mark.parametrize("F,feat_dtype,H", [(300, 0, 16), (602, 0, 16), (600, 1, 16), (300, 0, 64)])
+def test_long_rows_tma_gather(orc, F, feat_dtype, H):
+    """Rows of more than 32 16-byte chunks take k_agg1_tma (one TMA bulk copy
+    per source row, per-slot mbarriers; H <= 16 with the fused h1 epilogue,
+    H = 64 without): loss and gradients within the same 1e-3 of the oracle,
+    f32 and bf16 rows."""
+    g = G.generate_power_law(40_000, 4, 2.5, F, 5)
+    cache = CA.build_static_cache(g, CA.CacheConfig(int(0.2 * g.num_nodes) * g.feat_dim * 4, 1))
+    batches = T.plan_epoch_batches(g.train_nodes, 0, 1024, orc.hash2(1, 0))
+    _grad_case(orc, g, cache, batches[1], [15, 10], 8.0, 0, T.sampling_seed(1, 0, 1, 0), H=H,
+               feat_dtype=feat_dtype)
+
+
+def test_long_rows_tma_matches_ldgsts_bitwise():
+    """The TMA gather sums the same rows in the same order as the per-lane
+    LDGSTS kernel (A3G_AGG_TMA=0): losses and weights after 4 steps are
+    bit-identical (separate processes: the switch is read once)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import json, numpy as np\n"
+        "from paper_2511_07421_b200 import cache as CA, graph as G, train as T\n"
+        "g = G.generate_power_law(40_000, 4, 2.5, 602, 5)\n"
+        "c = CA.build_static_cache(g, CA.CacheConfig(int(0.2 * g.num_nodes) * g.feat_dim * 4, 1))\n"
+        "tr = T.Trainer(g, c, T.ModelSpec(602, 16, 4), [15, 10, 5], max_seeds=1024)\n"
+        "b = T.plan_epoch_batches(g.train_nodes, 0, 1024, 77)[:4]\n"
+        "off = np.cumsum([0] + [len(x) for x in b]).astype(np.uint64)\n"
+        "l = tr.steps_v(np.concatenate(b), off, [T.sampling_seed(1, 0, s, 0) for s in range(4)], 8.0, 0)\n"
+        "w1, w2 = tr.get_weights()\n"
+        "print(json.dumps([np.asarray(l).tobytes().hex(), np.asarray(w1).tobytes().hex(), np.asarray(w2).tobytes().hex()]))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for v in ("1", "0"):
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                           env=dict(os.environ, A3G_AGG_TMA=v))
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1]
+
+
 @pytest.mark.parametrize("H", [48, 64, 128, 256])
 def test_wide_hidden_on_tcgen05(orc, c1, H):
     """Realistic hidden widths (e.g. 256): h1 and dW1 run

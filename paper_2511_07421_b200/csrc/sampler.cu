@@ -808,6 +808,162 @@ __global__ void __launch_bounds__(256) k_stream_lane(SampleArgs a, const uint32_
   }
 }
 
+// k_stream_lane with the lane reservoirs in shared memory, slot-major per
+// CTA ([slot][thread]: a warp's 32 lanes touch 32 consecutive words, no bank
+// conflicts). The slot update is one dynamic-index store instead of a select
+// over all MB register slots, and the argmin scans the 32-bit key words with a
+// running second minimum, so the near-tie test needs no second pass. Same
+// candidates, same replay order, same results (default for fanouts <= 10;
+// A3G_LANE_SMEM=0 selects the register reservoirs for A/B). Measured: C2 step
+// -4%, C3 -6%, C5 -3% (profiles/r02_sampler_experiments.md).
+template <int MB>
+struct LaneSmem {
+  uint64_t rk[MB][256];
+  uint32_t hk[MB][256];
+  uint32_t rp[MB][256];
+};
+
+template <int MB, typename P>
+__device__ __forceinline__ void lane_argmin_s(const P& pol, const LaneSmem<MB>& R, int t, uint32_t m, uint64_t& thr,
+                                              uint32_t& mp) {
+  uint64_t rk[MB];
+#pragma unroll
+  for (int i = 0; i < MB; ++i) rk[i] = R.rk[i][t];
+  lane_argmin<MB>(pol, rk, m, thr, mp);
+}
+
+// HS: shift of the 32-bit key word (21 for 53-bit integer keys, 32 for the
+// bits of positive fp64 keys)
+template <int MB, int HS = 21, typename P>
+__device__ __forceinline__ void lane_insert_s(const P& pol, LaneSmem<MB>& R, int t, uint32_t m, uint32_t mp_in,
+                                              uint64_t kx, uint32_t pos, uint32_t win, uint64_t& thr, uint32_t& mp) {
+  R.rk[mp_in][t] = kx;
+  R.hk[mp_in][t] = static_cast<uint32_t>(kx >> HS);
+  R.rp[mp_in][t] = pos;
+  uint32_t mnh = 0xffffffffu, mn2 = 0xffffffffu, mi = 0;
+#pragma unroll
+  for (int i = 0; i < MB; ++i) {
+    const uint32_t h = R.hk[i][t];
+    mn2 = min(mn2, max(mnh, h));
+    if (h < mnh) {
+      mnh = h;
+      mi = i;
+    }
+  }
+  if (mn2 - mnh <= win) {  // another slot within the window: exact order decides
+    lane_argmin_s<MB>(pol, R, t, m, thr, mp);
+  } else {
+    mp = mi;
+    thr = R.rk[mi][t];
+  }
+}
+
+template <int WM, int MB>
+__global__ void __launch_bounds__(256) k_stream_lane_s(SampleArgs a, const uint32_t* lists, const uint32_t* cls_count) {
+  using P = typename PolOf<WM>::P;
+  __shared__ LaneSmem<MB> R;
+  const int lane = threadIdx.x & 31, t = threadIdx.x;
+  const uint32_t nitems = min(*a.item_count, a.hub.item_cap);
+  const uint32_t m = a.f;
+  const P pol = PolOf<WM>::make(a);
+  const uint32_t wstride = gridDim.x * (blockDim.x >> 5) * 32;
+  const uint32_t ibase = a.split_cls >= 0 ? items_from_class(cls_count, a.split_cls) : 0u;
+  const uint64_t tw = pol.tie >> 21;
+  const uint32_t win = static_cast<uint32_t>(tw < 0x7fffffffull ? tw : 0x7fffffffull) + 1u;
+  for (uint32_t base = ibase + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < nitems;
+       base += wstride) {
+    const uint32_t ii = base + lane;
+    const bool live = ii < nitems;
+    uint4 im = make_uint4(0, 0, 0, kInv);
+    uint32_t dst = 0;
+    uint64_t beg = 0;
+    if (live) {
+      im = a.hub.items[item_of(lists, cls_count, a.hub.item_cap, ii)];
+      dst = __ldg(a.front + im.x);
+      beg = __ldg(a.ro + dst);
+    }
+    const uint64_t key = hash2(a.seed, hash2(a.layer, dst));
+    const bool seg = im.w != kInv;
+    const uint32_t p0 = im.y, p1 = live ? im.z : im.y;
+    uint32_t* rid = a.hub.rec_id + static_cast<uint64_t>(seg ? im.w : 0) * kRecCap;
+    uint64_t* rkey = a.hub.rec_key + static_cast<uint64_t>(seg ? im.w : 0) * kRecCap;
+    // ---- fill (sampler.cpp:30-33)
+    const uint32_t nf = min(m, p1 - p0);
+#pragma unroll
+    for (int i = 0; i < MB; ++i) {
+      uint64_t k = ~0ull;
+      uint32_t p = 0;
+      if (static_cast<uint32_t>(i) < nf) {
+        k = draw(key, static_cast<uint64_t>(p0) + i + 1) >> 11;
+        p = p0 + i;
+        if (seg) {
+          rid[i] = p;
+          rkey[i] = k;
+        }
+      }
+      R.rk[i][t] = k;
+      R.hk[i][t] = static_cast<uint32_t>(k >> 21);
+      R.rp[i][t] = p;
+    }
+    uint64_t thr;
+    uint32_t mp;
+    lane_argmin_s<MB>(pol, R, t, m, thr, mp);
+    uint32_t rcnt = nf;
+    // ---- replay [p0 + nf, p1) in chunks of 32 positions
+    const uint32_t jb = p0 + nf;
+    const uint32_t len = p1 > jb ? p1 - jb : 0u;
+    uint32_t wlen = len;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) wlen = max(wlen, __shfl_xor_sync(kFull, wlen, off));
+    uint64_t ctr = key + (static_cast<uint64_t>(jb) + 1) * kPhi;
+    for (uint32_t b = 0; b < wlen; b += 32, ctr += 32 * kPhi) {
+      const uint32_t thi = pre_bound(static_cast<uint32_t>(thr >> 21));
+      uint32_t cm = 0;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        uint32_t l3;
+        const uint32_t h4 = mix64_pre(ctr + static_cast<uint64_t>(c) * kPhi, l3);
+        cm |= static_cast<uint32_t>(h4 >= thi) << c;
+      }
+      const uint32_t rem = len > b ? len - b : 0u;
+      if (rem < 32) cm &= (1u << rem) - 1u;
+      while (__any_sync(kFull, cm != 0)) {
+        if (cm) {
+          const int c = __ffs(cm) - 1;
+          cm &= cm - 1;
+          const uint64_t kx = mix64(ctr + static_cast<uint64_t>(c) * kPhi) >> 11;
+          if (pol.gt(kx, thr)) {
+            const uint32_t pos = jb + b + c;
+            if (seg && rcnt < kRecCap) {
+              rid[rcnt] = pos;
+              rkey[rcnt] = kx;
+            }
+            ++rcnt;
+            lane_insert_s<MB>(pol, R, t, m, mp, kx, pos, win, thr, mp);
+          }
+        }
+      }
+    }
+    if (!live) continue;
+    if (seg) {
+      a.hub.rec_cnt[im.w] = rcnt;
+      a.hub.tau[im.w] = thr;
+      a.hub.tau_ok[im.w] = (p1 - p0 >= m) ? 1u : 0u;
+    } else {
+      const uint32_t* nb = a.col + beg;
+      const uint64_t row0 = static_cast<uint64_t>(im.x) * m;
+#pragma unroll
+      for (int i = 0; i < MB; ++i)
+        if (static_cast<uint32_t>(i) < m) {
+          const uint32_t id = __ldg(nb + R.rp[i][t]);
+          a.S[row0 + i] = id;
+          mark_first(a.first, id, a.tag, static_cast<uint32_t>(row0 + i));
+        }
+      a.cnt[im.x] = m;
+    }
+  }
+}
+
 // Lower filter bound lo <= thr^gamma of cached candidates (a cached key
 // pow(u, 1/gamma) can beat thr only if u >= lo). Integer gamma <= 64: binary
 // powering (<= 12 correctly rounded products, relative error < 1.4e-15) with a
@@ -965,6 +1121,142 @@ __global__ void __launch_bounds__(256) k_stream_lane_mixed(SampleArgs a, const u
       for (int i = 0; i < MB; ++i)
         if (static_cast<uint32_t>(i) < m) {
           const uint32_t id = __ldg(nb + rp[i]);
+          a.S[row0 + i] = id;
+          mark_first(a.first, id, a.tag, static_cast<uint32_t>(row0 + i));
+        }
+      a.cnt[im.x] = m;
+    }
+  }
+}
+
+// k_stream_lane_mixed with the lane reservoirs in shared memory (as
+// k_stream_lane_s; A/B: A3G_LANE_SMEM).
+template <int MB>
+__global__ void __launch_bounds__(256) k_stream_lane_mixed_s(SampleArgs a, const uint32_t* lists,
+                                                           const uint32_t* cls_count) {
+  __shared__ LaneSmem<MB> R;
+  const int lane = threadIdx.x & 31, tid = threadIdx.x;
+  const uint32_t nitems = min(*a.item_count, a.hub.item_cap);
+  const uint32_t m = a.f;
+  const double ig = a.inv_gamma, gamma = a.gamma;
+  const bool gint = gamma == floor(gamma) && gamma <= 64.0;  // lane_gamma_lo by multiplications
+  const uint32_t* eb = a.ebits;
+  const rsv::PolUnit ipol{};
+  // grid sized to the layer's item bound: one batch of 32 items per warp
+  // (short-lived CTAs let the high-priority compute stream's kernels in)
+  const uint32_t wstride = gridDim.x * (blockDim.x >> 5) * 32;
+  const uint32_t ibase = a.split_cls >= 0 ? items_from_class(cls_count, a.split_cls) : 0u;
+  for (uint32_t base = ibase + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < nitems;
+       base += wstride) {
+    const uint32_t ii = base + lane;
+    const bool live = ii < nitems;
+    uint4 im = make_uint4(0, 0, 0, kInv);
+    uint32_t dst = 0;
+    uint64_t beg = 0;
+    if (live) {
+      im = a.hub.items[item_of(lists, cls_count, a.hub.item_cap, ii)];
+      dst = __ldg(a.front + im.x);
+      beg = __ldg(a.ro + dst);
+    }
+    const uint64_t key = hash2(a.seed, hash2(a.layer, dst));
+    const bool seg = im.w != kInv;
+    const uint32_t p0 = im.y, p1 = live ? im.z : im.y;
+    uint32_t* rid = a.hub.rec_id + static_cast<uint64_t>(seg ? im.w : 0) * kRecCap;
+    uint64_t* rkey = a.hub.rec_key + static_cast<uint64_t>(seg ? im.w : 0) * kRecCap;
+    auto ebit = [&](uint64_t e) { return (__ldg(eb + (e >> 5)) >> (e & 31)) & 1u; };
+    // ---- fill (sampler.cpp:30-33)
+    const uint32_t nf = min(m, p1 - p0);
+#pragma unroll
+    for (int i = 0; i < MB; ++i) {
+      uint64_t kb = static_cast<uint64_t>(__double_as_longlong(INFINITY));
+      uint32_t p = 0;
+      if (static_cast<uint32_t>(i) < nf) {
+        const uint32_t j = p0 + i;
+        const double u = unit_of(draw(key, static_cast<uint64_t>(j) + 1));
+        const double k = ebit(beg + j) ? pow(u, ig) : u;
+        kb = static_cast<uint64_t>(__double_as_longlong(k));
+        p = j;
+        if (seg) {
+          rid[i] = j;
+          rkey[i] = kb;
+        }
+      }
+      R.rk[i][tid] = kb;
+      R.hk[i][tid] = static_cast<uint32_t>(kb >> 32);
+      R.rp[i][tid] = p;
+    }
+    uint64_t thrb;
+    uint32_t mp;
+    lane_argmin_s<MB>(ipol, R, tid, m, thrb, mp);
+    uint32_t rcnt = nf;
+    const uint32_t jb = p0 + nf;
+    const uint32_t len = p1 > jb ? p1 - jb : 0u;
+    uint32_t wlen = len;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) wlen = max(wlen, __shfl_xor_sync(kFull, wlen, off));
+    uint64_t ctr = key + (static_cast<uint64_t>(jb) + 1) * kPhi;
+    for (uint32_t b = 0; b < wlen; b += 32, ctr += 32 * kPhi) {
+      const double thr = __longlong_as_double(static_cast<long long>(thrb));
+      double lo = lane_gamma_lo(thr, gamma, gint);
+      const uint32_t b_thr = pre_bound(lo_hi_word(thr)), b_lo = pre_bound(lo_hi_word(lo));
+      const uint32_t rem = len > b ? len - b : 0u;
+      uint32_t cb = 0;
+      if (rem) {
+        const uint64_t e0 = beg + jb + b;
+        cb = __funnelshift_r(__ldg(eb + (e0 >> 5)), __ldg(eb + (e0 >> 5) + 1), static_cast<uint32_t>(e0 & 31));
+      }
+      uint32_t cm = 0;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        uint32_t l3;
+        const uint32_t h4 = mix64_pre(ctr + static_cast<uint64_t>(c) * kPhi, l3);
+        cm |= static_cast<uint32_t>(h4 >= (((cb >> c) & 1u) ? b_lo : b_thr)) << c;
+      }
+      if (rem < 32) cm &= (1u << rem) - 1u;
+      while (__any_sync(kFull, cm != 0)) {
+        if (cm) {
+          const int c = __ffs(cm) - 1;
+          cm &= cm - 1;
+          const double t = __longlong_as_double(static_cast<long long>(thrb));
+          const double uu = unit_of(mix64(ctr + static_cast<uint64_t>(c) * kPhi));
+          double k = uu;
+          bool ins;
+          if ((cb >> c) & 1u) {
+            ins = uu >= lo;  // lo follows every insertion (cheap for integer gamma)
+            if (ins) {
+              k = pow(uu, ig);
+              ins = k > t;
+            }
+          } else {
+            ins = uu > t;
+          }
+          if (ins) {
+            const uint32_t pos = jb + b + c;
+            const uint64_t kb = static_cast<uint64_t>(__double_as_longlong(k));
+            if (seg && rcnt < kRecCap) {
+              rid[rcnt] = pos;
+              rkey[rcnt] = kb;
+            }
+            ++rcnt;
+            // high words order positive doubles; equal high words: exact argmin
+            lane_insert_s<MB, 32>(ipol, R, tid, m, mp, kb, pos, 0u, thrb, mp);
+            if (gint) lo = lane_gamma_lo(__longlong_as_double(static_cast<long long>(thrb)), gamma, true);
+          }
+        }
+      }
+    }
+    if (!live) continue;
+    if (seg) {
+      a.hub.rec_cnt[im.w] = rcnt;
+      a.hub.tau[im.w] = thrb;
+      a.hub.tau_ok[im.w] = (p1 - p0 >= m) ? 1u : 0u;
+    } else {
+      const uint32_t* nb = a.col + beg;
+      const uint64_t row0 = static_cast<uint64_t>(im.x) * m;
+#pragma unroll
+      for (int i = 0; i < MB; ++i)
+        if (static_cast<uint32_t>(i) < m) {
+          const uint32_t id = __ldg(nb + R.rp[i][tid]);
           a.S[row0 + i] = id;
           mark_first(a.first, id, a.tag, static_cast<uint32_t>(row0 + i));
         }
@@ -2040,7 +2332,18 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
       if (fork) A3G_CUDA(cudaEventRecord(ev_join, aux));
       if (lane) {  // register reservoirs sized to the fanout (exact sizes for the common 5 / 10)
         if (WM == 2) {
-          if (sa.f == 5)
+          static const bool lane_smem_m = [] {  // shared-memory reservoirs (default; =0: registers, A/B)
+            const char* e = std::getenv("A3G_LANE_SMEM");
+            return !(e && std::atoi(e) == 0);
+          }();
+          if (lane_smem_m && sa.f <= 10) {
+            if (sa.f == 5)
+              k_stream_lane_mixed_s<5><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
+            else if (sa.f <= 8)
+              k_stream_lane_mixed_s<8><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
+            else
+              k_stream_lane_mixed_s<10><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
+          } else if (sa.f == 5)
             k_stream_lane_mixed<5><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
           else if (sa.f <= 8)
             k_stream_lane_mixed<8><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
@@ -2050,7 +2353,18 @@ void launch_layer_kernels(const SampleArgs& sa, uint64_t rows_bound, int sm_coun
             k_stream_lane_mixed<16><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
           A3G_LAUNCH_DONE("k_stream_lane_mixed", st);
         } else {
-          if (sa.f == 5)
+          static const bool lane_smem = [] {  // shared-memory reservoirs (default; =0: registers, A/B)
+            const char* e = std::getenv("A3G_LANE_SMEM");
+            return !(e && std::atoi(e) == 0);
+          }();
+          if (lane_smem && sa.f <= 10) {
+            if (sa.f == 5)
+              k_stream_lane_s<W, 5><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
+            else if (sa.f <= 8)
+              k_stream_lane_s<W, 8><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
+            else
+              k_stream_lane_s<W, 10><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
+          } else if (sa.f == 5)
           {
             if (!diag_skip("lane")) k_stream_lane<W, 5><<<lane_grid, 256, 0, st>>>(sl, lists, sa.cls_count);
           }

@@ -1,5 +1,5 @@
 # r02 final evidence: full GPU suite, smoke, bench lines (C2 default with cpu_baseline, reference arm),
-# launch lists (C2, C3), ncu --set full of k_agg1 and the sampler's lane kernel
+# launch lists (C2, C3), ncu --set full of k_agg1 (k_agg1_tma at C2) and the sampler's lane kernel
 mkdir -p gpurun_out/final
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/final/smi.txt 2>&1
 timeout 1800 python -m pytest tests -m gpu -q --timeout 1500 -rA > gpurun_out/final/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/final/pytest_gpu.txt
@@ -13,6 +13,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --c
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv --log-file gpurun_out/final/launches_c3.csv python bench.py --config c3 --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_agg1 -s 3 -c 1 -o gpurun_out/final/prof_k_agg1 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 python tools/ncu_summary.py gpurun_out/final/prof_k_agg1.ncu-rep > gpurun_out/final/prof_k_agg1.txt 2>/dev/null
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stream_lane_s -s 6 -c 1 -o gpurun_out/final/prof_lane python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+python tools/ncu_summary.py gpurun_out/final/prof_lane.ncu-rep > gpurun_out/final/prof_lane.txt 2>/dev/null
 python tools/kernel_table.py gpurun_out/final/launches_c2.csv > gpurun_out/final/launches_c2.txt 2>/dev/null
 python tools/kernel_table.py gpurun_out/final/launches_c3.csv > gpurun_out/final/launches_c3.txt 2>/dev/null
 ncu -i gpurun_out/final/prof_k_agg1.ncu-rep --page raw --csv 2>/dev/null | python -c "

@@ -832,29 +832,35 @@ __device__ __forceinline__ void lane_argmin_s(const P& pol, const LaneSmem<MB>& 
   lane_argmin<MB>(pol, rk, m, thr, mp);
 }
 
-// HS: shift of the 32-bit key word (21 for 53-bit integer keys, 32 for the
-// bits of positive fp64 keys)
+// Packed slot word: the top 28 bits of the key's 32-bit word (HS: 21 for
+// 53-bit integer keys, 32 for the bits of positive fp64 keys) over the slot
+// index, so one unsigned min yields the minimum's bucket and its first slot.
+template <int HS>
+__device__ __forceinline__ uint32_t slot_word(uint64_t k, uint32_t i) {
+  return (static_cast<uint32_t>(k >> HS) & ~15u) | i;
+}
+
+// win: buckets (units of 2^(HS+4)) within which another slot may hold an
+// equal or smaller key in exact order -- then the exact argmin decides.
 template <int MB, int HS = 21, typename P>
 __device__ __forceinline__ void lane_insert_s(const P& pol, LaneSmem<MB>& R, int t, uint32_t m, uint32_t mp_in,
                                               uint64_t kx, uint32_t pos, uint32_t win, uint64_t& thr, uint32_t& mp) {
+  static_assert(MB <= 16, "slot index in 4 bits");
   R.rk[mp_in][t] = kx;
-  R.hk[mp_in][t] = static_cast<uint32_t>(kx >> HS);
+  R.hk[mp_in][t] = slot_word<HS>(kx, mp_in);
   R.rp[mp_in][t] = pos;
-  uint32_t mnh = 0xffffffffu, mn2 = 0xffffffffu, mi = 0;
+  uint32_t mn = 0xffffffffu, mn2 = 0xffffffffu;
 #pragma unroll
   for (int i = 0; i < MB; ++i) {
-    const uint32_t h = R.hk[i][t];
-    mn2 = min(mn2, max(mnh, h));
-    if (h < mnh) {
-      mnh = h;
-      mi = i;
-    }
+    const uint32_t w = R.hk[i][t];
+    mn2 = min(mn2, max(mn, w));
+    mn = min(mn, w);
   }
-  if (mn2 - mnh <= win) {  // another slot within the window: exact order decides
+  if ((mn2 >> 4) - (mn >> 4) <= win) {  // another slot within the window: exact order decides
     lane_argmin_s<MB>(pol, R, t, m, thr, mp);
   } else {
-    mp = mi;
-    thr = R.rk[mi][t];
+    mp = mn & 15u;
+    thr = R.rk[mp][t];
   }
 }
 
@@ -868,8 +874,8 @@ __global__ void __launch_bounds__(256) k_stream_lane_s(SampleArgs a, const uint3
   const P pol = PolOf<WM>::make(a);
   const uint32_t wstride = gridDim.x * (blockDim.x >> 5) * 32;
   const uint32_t ibase = a.split_cls >= 0 ? items_from_class(cls_count, a.split_cls) : 0u;
-  const uint64_t tw = pol.tie >> 21;
-  const uint32_t win = static_cast<uint32_t>(tw < 0x7fffffffull ? tw : 0x7fffffffull) + 1u;
+  const uint64_t tw = pol.tie >> 25;  // the tie window in slot-word buckets
+  const uint32_t win = static_cast<uint32_t>(tw < 0x7ffffffull ? tw : 0x7ffffffull) + 1u;
   for (uint32_t base = ibase + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < nitems;
        base += wstride) {
     const uint32_t ii = base + lane;
@@ -902,7 +908,7 @@ __global__ void __launch_bounds__(256) k_stream_lane_s(SampleArgs a, const uint3
         }
       }
       R.rk[i][t] = k;
-      R.hk[i][t] = static_cast<uint32_t>(k >> 21);
+      R.hk[i][t] = slot_word<21>(k, i);
       R.rp[i][t] = p;
     }
     uint64_t thr;
@@ -1182,7 +1188,7 @@ __global__ void __launch_bounds__(256) k_stream_lane_mixed_s(SampleArgs a, const
         }
       }
       R.rk[i][tid] = kb;
-      R.hk[i][tid] = static_cast<uint32_t>(kb >> 32);
+      R.hk[i][tid] = slot_word<32>(kb, i);
       R.rp[i][tid] = p;
     }
     uint64_t thrb;

@@ -944,9 +944,10 @@ a3g_status a3g_train_steps_v(a3g_trainer* tr, const uint32_t* seeds, const uint6
     A3G_CUDA(cudaStreamWaitEvent(t.s_samp, t.ev_t0, 0));
     const uint32_t* dseeds = seeds;
     if (!on_device) {  // H2D of every step's seeds (inside the timed region)
-      if (total > t.seed_buf_cap) {  // grow geometrically: reallocation (a device sync) stays rare
+      if (total > t.seed_buf_cap) {  // grow geometrically: reallocation (a device sync) stays rare;
+        // the first allocation covers 256 batches (a short warm-up call sizes it for long ones)
         const uint64_t cap = std::max<uint64_t>(total, std::max<uint64_t>(2 * t.seed_buf_cap,
-                                                                          64ull * t.max_seeds));
+                                                                          256ull * t.max_seeds));
         dfree(t.d_seed_buf);
         if (t.h_seed_stage) cudaFreeHost(t.h_seed_stage);
         t.h_seed_stage = nullptr;

@@ -73,7 +73,9 @@ def parse():
                    help="feature placement (DESIGN.md 5): hbm = whole table replicated in each GPU's HBM; cache = "
                         "cached rows in HBM, misses in pinned host memory (zero-copy PCIe); sharded = rank r holds "
                         "the rows the cache places on device r, peers read over NVLink (cudaIpc), misses on the "
-                        "host. auto: hbm at N=1, sharded at N>1")
+                        "host. auto: hbm (replicated) whenever the table fits in a quarter of one GPU's HBM -- "
+                        "every BASELINE config does, even C5's 28 GB of bf16 rows -- so weak scaling moves no "
+                        "feature bytes over NVLink; sharded otherwise")
     return p.parse_args()
 
 
@@ -306,7 +308,10 @@ def run_ours(args):
     gen_s = time.time() - t0
     synth = args.config in SYNTH
     Fh = 1 if synth else F  # host feat_dim (the cache's node_cost, cache.cpp:20, scales the same set)
-    store = args.store if args.store != "auto" else ("sharded" if world > 1 else "hbm")
+    table_bytes = n * F * (2 if synth else 4)
+    hbm_bytes = torch.cuda.get_device_properties(local).total_memory
+    store = args.store if args.store != "auto" else ("hbm" if world == 1 or table_bytes * 4 <= hbm_bytes
+                                                     else "sharded")
     from paper_2511_07421_b200 import graph as Gm
     # Appendix B: the ratio is the aggregate cached fraction; per-device volume
     # ratio*n*F*4/N over N devices caches the same set for every N

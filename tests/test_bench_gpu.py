@@ -44,7 +44,7 @@ def test_bench_one_gpu_contract_keys():
 def test_bench_two_ranks_sharded_store_host_comm():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2", "--config", "c1", "--steps",
-           "5", "--warmup", "3", "--no-cpu-baseline", "--comm", "host", "--share-device"]
+           "5", "--warmup", "3", "--no-cpu-baseline", "--comm", "host", "--share-device", "--store", "sharded"]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-3000:])
     d = _json_line(r.stdout)
@@ -53,3 +53,15 @@ def test_bench_two_ranks_sharded_store_host_comm():
     assert d["config"]["global_batch"] == 2 * d["config"]["batch_per_gpu"]
     res = d["roofline"]["resources"]
     assert "hbm_local" in res and "nvlink_peer" in res  # the other rank's shard is read through the peer path
+
+
+def test_bench_two_ranks_default_placement_replicates():
+    """--store auto at N > 1: the table fits one GPU, so every rank holds it (weak scaling moves
+    only the gradient allreduce between GPUs)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2", "--config", "c1", "--steps",
+           "5", "--warmup", "3", "--no-cpu-baseline", "--comm", "host", "--share-device"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-3000:])
+    d = _json_line(r.stdout)
+    assert d["n_gpus"] == 2 and d["config"]["store"] == "hbm" and d["value"] > 0

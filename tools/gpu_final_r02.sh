@@ -15,6 +15,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ag
 python tools/ncu_summary.py gpurun_out/final/prof_k_agg1.ncu-rep > gpurun_out/final/prof_k_agg1.txt 2>/dev/null
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stream_lane_s -s 6 -c 1 -o gpurun_out/final/prof_lane python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 python tools/ncu_summary.py gpurun_out/final/prof_lane.ncu-rep > gpurun_out/final/prof_lane.txt 2>/dev/null
+python tools/ncu_lines.py gpurun_out/final/prof_lane.ncu-rep k_stream_lane 40 > gpurun_out/final/prof_lane_lines.txt 2>/dev/null
+python tools/ncu_lines.py gpurun_out/final/prof_k_agg1.ncu-rep k_agg1 40 > gpurun_out/final/prof_k_agg1_lines.txt 2>/dev/null
 python tools/kernel_table.py gpurun_out/final/launches_c2.csv > gpurun_out/final/launches_c2.txt 2>/dev/null
 python tools/kernel_table.py gpurun_out/final/launches_c3.csv > gpurun_out/final/launches_c3.txt 2>/dev/null
 ncu -i gpurun_out/final/prof_k_agg1.ncu-rep --page raw --csv 2>/dev/null | python -c "
@@ -25,3 +27,5 @@ for row in r[2:]:
 " > gpurun_out/final/k_agg1_traffic.txt
 tail -3 gpurun_out/final/pytest_gpu.txt; tail -1 gpurun_out/final/smoke.txt
 for f in gpurun_out/final/bench_*.json gpurun_out/final/ref_c2.json; do echo "== $f"; tail -1 $f | cut -c1-300; done
+# the reports stay on the box (gpurun copies back at most 64 MiB); summaries above
+rm -f gpurun_out/final/*.ncu-rep

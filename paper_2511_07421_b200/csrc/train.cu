@@ -949,19 +949,9 @@ static bool agg_tma() {
   return v;
 }
 
-static int agg_tma_w() {  // A/B: A3G_AGG_TMA_W=12 (12-warp CTAs: 168 registers per thread)
-  static const int v = [] {
-    const char* e = std::getenv("A3G_AGG_TMA_W");
-    return e && std::atoi(e) == 12 ? 12 : 16;
-  }();
-  return v;
-}
-
-template <typename T, int N, int HB, int W = (N <= 8 ? 16 : 8)>
+template <typename T, int N, int HB>
 bool launch_agg_tma(TrainerState& t, const AggArgs& aa, cudaStream_t st) {
-  if constexpr (W == 16 && N <= 5 && HB > 0) {
-    if (agg_tma_w() == 12) return launch_agg_tma<T, N, HB, 12>(t, aa, st);
-  }
+  constexpr int W = N <= 8 ? 16 : 8;
   constexpr int S = N <= 5 ? 4 : 2;
   const size_t ring = static_cast<size_t>(W) * S * aa.view.row_bytes;
   const size_t smem = ring + (HB > 0 ? static_cast<size_t>(aa.pitch) * HB * 4 : 0);

@@ -1138,7 +1138,9 @@ __global__ void __launch_bounds__(256) k_stream_lane_mixed(SampleArgs a, const u
 // k_stream_lane_mixed with the lane reservoirs in shared memory (as
 // k_stream_lane_s; A/B: A3G_LANE_SMEM).
 template <int MB>
-__global__ void __launch_bounds__(256) k_stream_lane_mixed_s(SampleArgs a, const uint32_t* lists,
+// four resident CTAs per SM (64 registers): C5 step -2%, C3 unchanged; the
+// same bound on k_stream_lane_s spills and measured 5% slower at C2
+__global__ void __launch_bounds__(256, 4) k_stream_lane_mixed_s(SampleArgs a, const uint32_t* lists,
                                                            const uint32_t* cls_count) {
   __shared__ LaneSmem<MB> R;
   const int lane = threadIdx.x & 31, tid = threadIdx.x;

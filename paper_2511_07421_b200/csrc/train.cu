@@ -480,7 +480,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_agg1_tma(const __grid_constan
                 xx[1][i][e] = acc[i][e] * scale;
               }
             const uint32_t rr[2] = {prev_row[0], srow};
-            h1_rows<NCH, EPC, 32, HG, 2>(xx, rr, w1s, chunks, 0, lane, a.H, a.h1);
+            // two passes of HG/2 outputs: half the partial sums live at once (no
+            // spills, fewer rematerialised addresses; the butterfly order per output
+            // is unchanged, so h1 is bit-identical): k_agg1 alone 0.595 -> 0.617
+            h1_rows<NCH, EPC, 32, HG / 2, 2>(xx, rr, w1s, chunks, 0, lane, a.H, a.h1);
+            h1_rows<NCH, EPC, 32, HG / 2, 2>(xx, rr, w1s, chunks, 1, lane, a.H, a.h1);
             have_prev = false;
           }
         } else {

@@ -72,10 +72,34 @@ int kind_of(const SamplerConfig& c) {
   return c.kind == sampling::SamplerKind::uniform_baseline ? A3G_SAMPLER_UNIFORM : A3G_SAMPLER_WEIGHTED;
 }
 
+// middle element (odd count) or the mean of the two middle ones
 double median(std::vector<double> v) {
-  std::sort(v.begin(), v.end());
-  const std::size_t n = v.size();
-  return n % 2 == 1 ? v[n / 2] : 0.5 * (v[n / 2 - 1] + v[n / 2]);
+  const auto mid = v.begin() + static_cast<std::ptrdiff_t>(v.size() / 2);
+  std::nth_element(v.begin(), mid, v.end());
+  if (v.size() & 1u) return *mid;
+  return 0.5 * (*std::max_element(v.begin(), mid) + *mid);
+}
+
+// The ExecResult fields every execution path reports (pipeline_exec.cpp:
+// 278-291): epochs per second over the wall time, the analytic memory model
+// on the measured batch / model bytes, the capacity check, accuracy and the
+// cache hit rate.
+ExecResult finish_result(double seconds, std::uint32_t epochs, std::uint64_t batch_bytes, std::uint64_t model_bytes,
+                         const ResolvedDesign& d, const PlatformSpec& platform, double accuracy, std::uint64_t hits,
+                         std::uint64_t misses) {
+  ExecResult r;
+  r.elapsed_seconds = seconds;
+  r.metrics.throughput_eps = seconds > 0.0 ? epochs / seconds : 0.0;
+  r.batch_bytes_max = batch_bytes;
+  r.model_bytes = model_bytes;
+  r.memory = analytic_memory(d.mode, d.workers, d.cache_volume, batch_bytes, model_bytes,
+                             platform.runtime_overhead_bytes);
+  r.metrics.memory_bytes = static_cast<double>(r.memory.peak_total);
+  r.within_capacity = r.memory.peak_total <= platform.gpu_mem_capacity;
+  r.metrics.accuracy = accuracy;
+  const std::uint64_t lookups = hits + misses;
+  r.hit_rate = lookups ? static_cast<double>(hits) / static_cast<double>(lookups) : 0.0;
+  return r;
 }
 
 }  // namespace
@@ -98,7 +122,7 @@ StageCosts profile_stage_costs(const Graph& g, const ResolvedDesign& design, con
     for (const auto& b : batches[w]) max_seeds = std::max<std::uint32_t>(max_seeds, static_cast<std::uint32_t>(b.size()));
     make_trainer(tw[w], lg, s.ctxs.empty() ? s.cache : s.ctxs[w].cache, spec, sampler_base, max_seeds, 1);
   }
-  std::vector<double> ts, tb, tt;
+  std::vector<double> t_samp, t_gather, t_comp;  // seconds per probe
   for (std::uint32_t i = 0; i < probe_iters; ++i) {
     // the probe units of pipeline_exec.cpp:151: (0, i % steps, i % u)
     const std::uint32_t step = i % static_cast<std::uint32_t>(steps), w = i % u;
@@ -107,16 +131,16 @@ StageCosts profile_stage_costs(const Graph& g, const ResolvedDesign& design, con
     b200::check(a3g_trainer_profile_step(tw[w].h, seeds.data(), static_cast<std::uint32_t>(seeds.size()),
                                          design.bias_rate, kind_of(sampler_base),
                                          train::sampling_seed(sampler_base.rng_seed, 0, step, w), ms));
-    ts.push_back(ms[0] * 1e-3);
-    tb.push_back(ms[1] * 1e-3);
-    tt.push_back(ms[2] * 1e-3);
+    t_samp.push_back(ms[0] * 1e-3);
+    t_gather.push_back(ms[1] * 1e-3);
+    t_comp.push_back(ms[2] * 1e-3);
   }
-  StageCosts costs;
-  costs.t_sample = median(ts) * s.sample_multiplier;
-  costs.t_batch = median(tb);
-  costs.t_train = median(tt);
-  costs.iters_per_epoch = static_cast<std::uint64_t>(steps) * u;
-  return costs;
+  StageCosts out;
+  out.t_sample = median(t_samp) * s.sample_multiplier;
+  out.t_batch = median(t_gather);
+  out.t_train = median(t_comp);
+  out.iters_per_epoch = static_cast<std::uint64_t>(steps) * u;
+  return out;
 }
 
 ExecResult execute_pipeline(const Graph& g, const ResolvedDesign& design, const PlatformSpec& platform,
@@ -132,21 +156,9 @@ ExecResult execute_pipeline(const Graph& g, const ResolvedDesign& design, const 
     const auto t0 = Clock::now();
     const auto run = b200::train_partitioned(g, spec, cfg, s.cache, design.partitions, graph::PartitionMethod::hash,
                                              B, opts.epochs, opts.model_seed);
-    ExecResult result;
-    result.elapsed_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
-    result.metrics.throughput_eps =
-        result.elapsed_seconds > 0.0 ? static_cast<double>(opts.epochs) / result.elapsed_seconds : 0.0;
-    result.batch_bytes_max = run.rep.max_batch_bytes;
-    result.model_bytes = spec.param_bytes() + run.rep.max_activation_bytes;
-    result.memory = analytic_memory(design.mode, design.workers, design.cache_volume, result.batch_bytes_max,
-                                    result.model_bytes, platform.runtime_overhead_bytes);
-    result.metrics.memory_bytes = static_cast<double>(result.memory.peak_total);
-    result.within_capacity = result.memory.peak_total <= platform.gpu_mem_capacity;
-    result.metrics.accuracy = run.rep.test_accuracy;
-    result.hit_rate = run.hits + run.misses > 0
-                          ? static_cast<double>(run.hits) / static_cast<double>(run.hits + run.misses)
-                          : 0.0;
-    return result;
+    const double secs = std::chrono::duration<double>(Clock::now() - t0).count();
+    return finish_result(secs, opts.epochs, run.rep.max_batch_bytes, spec.param_bytes() + run.rep.max_activation_bytes,
+                         design, platform, run.rep.test_accuracy, run.hits, run.misses);
   }
   Trainer t;
   make_trainer(t, g, s.cache, spec, sampler_base, static_cast<std::uint32_t>(std::min<std::size_t>(B, s.train_nodes.size())),
@@ -183,19 +195,11 @@ ExecResult execute_pipeline(const Graph& g, const ResolvedDesign& design, const 
   // pipeline_exec.cpp:25-30): a model of a slower sampler. Here sampling runs
   // on the GPU for real and overlaps compute, so the executor does not pad;
   // profile_stage_costs keeps the multiplier on t_sample for the analytic model.
-  ExecResult result;
-  result.elapsed_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
-  result.metrics.throughput_eps =
-      result.elapsed_seconds > 0.0 ? static_cast<double>(opts.epochs) / result.elapsed_seconds : 0.0;
-  result.batch_bytes_max = max_batch_bytes;
-  result.model_bytes = spec.param_bytes() + max_act_bytes;
-  result.memory = analytic_memory(design.mode, design.workers, design.cache_volume, max_batch_bytes,
-                                  result.model_bytes, platform.runtime_overhead_bytes);
-  result.metrics.memory_bytes = static_cast<double>(result.memory.peak_total);
-  result.within_capacity = result.memory.peak_total <= platform.gpu_mem_capacity;
-  b200::check(a3g_evaluate_full_graph(t.h, g.test_mask.data(), &result.metrics.accuracy));
-  result.hit_rate = hits + misses > 0 ? static_cast<double>(hits) / static_cast<double>(hits + misses) : 0.0;
-  return result;
+  const double secs = std::chrono::duration<double>(Clock::now() - t0).count();
+  double accuracy = 0.0;
+  b200::check(a3g_evaluate_full_graph(t.h, g.test_mask.data(), &accuracy));
+  return finish_result(secs, opts.epochs, max_batch_bytes, spec.param_bytes() + max_act_bytes, design, platform,
+                       accuracy, hits, misses);
 }
 
 }  // namespace a3gnn::pipeline

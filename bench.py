@@ -25,6 +25,11 @@ import time
 
 import numpy as np
 
+# nine CUDA streams drive the pipeline: more hardware work queues than the
+# default 8 keep them from serialising behind each other (set before any CUDA
+# context exists; liba3g_b200.so asks for the same when it loads first)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 

@@ -34,6 +34,17 @@ void set_error(const std::string& msg);
 }
 
 namespace {
+// The pipeline drives nine streams (eight sampling streams and the compute
+// stream); with the default 8 hardware work queues two of them share a queue and serialise behind each other's kernels. Ask for 32
+// when the library loads before the process creates its CUDA context (a
+// preset value wins; a context that already exists keeps its own). C2 step
+// 0.288 -> 0.277 ms at 100 steps (profiles/r02_sampler_experiments.md).
+struct HwQueues {
+  HwQueues() { setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0); }
+} g_hw_queues;
+}  // namespace
+
+namespace {
 thread_local std::string g_err;
 template <typename T>
 T* dalloc(size_t count) {

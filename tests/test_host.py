@@ -4,6 +4,7 @@ golden vectors; every symbol declared in include/a3g.h is exported."""
 import os
 import re
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -95,6 +96,20 @@ def test_library_is_sm100a():
 
 def test_version_string():
     assert b"sm_100a" in _lib.lib().a3g_version()
+
+
+def test_library_requests_hardware_queues():
+    """Loading the library asks for 32 CUDA hardware work queues (the pipeline's nine streams)
+    unless the process preset the variable: checked in a fresh process, through libc."""
+    code = ("import ctypes, os\n"
+            "os.environ.pop('CUDA_DEVICE_MAX_CONNECTIONS', None)\n"
+            "libc = ctypes.CDLL(None); libc.unsetenv(b'CUDA_DEVICE_MAX_CONNECTIONS')\n"
+            "libc.getenv.restype = ctypes.c_char_p\n"
+            "ctypes.CDLL(%r)\n"
+            "print(libc.getenv(b'CUDA_DEVICE_MAX_CONNECTIONS').decode())\n") % _lib.LIB_PATH
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr[-1000:]
+    assert out.stdout.strip() == "32"
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c3"])

@@ -356,7 +356,8 @@ def run_ours(args):
         comm = T.Comm(bytes(uid.cpu().numpy().tobytes()), world, rank, local)
         tr.set_comm(comm)
     W, K = args.warmup, args.steps
-    pipe = args.pipeline if args.pipeline is not None else 8
+    # the library's default depth (trainer.cuh): 12 sampling streams for batches of <= 2048 seeds, else 8
+    pipe = args.pipeline if args.pipeline is not None else (12 if B <= 2048 else 8)
     tr.set_pipeline(pipe)
     from paper_2511_07421_b200 import dp
     gbatches, gseeds = dp.global_batches(g.train_nodes, B, world, W + 3 * K, BASE_SEED)

@@ -219,8 +219,9 @@ a3g_status a3g_trainer_set_weights(a3g_trainer* t, const double* w1, const doubl
 a3g_status a3g_trainer_get_weights(a3g_trainer* t, double* w1, double* w2);
 /* Pipeline shape of a3g_train_steps[_v] (pipeline_exec.cpp:219-276 modes):
  * 0 = sequential (sampling and compute on one stream, Mode::sequential);
- * n = 1..8 sampling streams running n batches' samplers concurrently ahead of
- * the compute stream (n + 1 arenas, allocated on first use). Default 8.
+ * n = 1..12 sampling streams running n batches' samplers concurrently ahead of
+ * the compute stream (n + 1 arenas, allocated on first use). Default 12 for
+ * trainers of <= 2048 seeds per batch, else 8.
  * Results are identical for every shape (schedule only, pipeline.hpp:107-109). */
 a3g_status a3g_trainer_set_pipeline(a3g_trainer* t, int sampling_streams);
 /* Attach a communicator for the data-parallel gradient sum (NULL detaches). */

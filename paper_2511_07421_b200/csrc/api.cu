@@ -740,6 +740,8 @@ a3g_status a3g_trainer_create(a3g_graph* g, a3g_cache* c, uint32_t max_seeds, co
       t.L = L;
       t.lr = lr;
       t.max_seeds = max_seeds;
+      t.pipe_streams = max_seeds <= TrainerState::kSmallBatch ? TrainerState::kDefaultStreamsSmall
+                                                               : TrainerState::kDefaultStreams;
       t.sm_count = sm_count_of(g->device);
       t.fanouts.assign(fanouts, fanouts + L);
       t.tc_gemms = std::getenv("A3G_TC_GEMMS") != nullptr;

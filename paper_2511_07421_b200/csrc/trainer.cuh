@@ -13,9 +13,15 @@ struct TrainerState {
   // concurrently (the sampler's many small latency-bound kernels interleave)
   // while compute consumes in order; an arena is reused only after its step's
   // compute. Arenas beyond the first are allocated on first use.
-  static constexpr int kArenas = 9;
-  static constexpr int kSampStreams = 8;
+  // default depth by batch size: small batches (<= 2048 seeds) are sampled by
+  // short, latency-bound kernel chains and fill the GPU better with 12 in
+  // flight (C2 step -5% against 8 with 32 hardware queues); large batches keep
+  // 8 (C3 neutral, C5 +4% at 12)
+  static constexpr int kSampStreams = 12;
+  static constexpr int kArenas = kSampStreams + 1;
   static constexpr int kDefaultStreams = 8;
+  static constexpr int kDefaultStreamsSmall = 12;
+  static constexpr uint32_t kSmallBatch = 2048;
   a3g_sampler* smp[kArenas] = {};
   uint32_t F = 0, H = 0, C = 0, pitch = 0, L = 0, max_seeds = 0;
   double lr = 0.2;

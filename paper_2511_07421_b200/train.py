@@ -268,7 +268,8 @@ class Trainer:
         check(lib().a3g_trainer_set_weights(self.h, ptr(a, f64p), ptr(b, f64p)))
 
     def set_pipeline(self, sampling_streams: int):
-        """0 = sequential (Mode::sequential), 1..8 concurrent sampling streams."""
+        """0 = sequential (Mode::sequential), 1..12 concurrent sampling streams (default: 12 for
+        batches of <= 2048 seeds, else 8)."""
         check(lib().a3g_trainer_set_pipeline(self.h, int(sampling_streams)))
 
     def set_comm(self, comm):

@@ -242,17 +242,17 @@ def test_device_feature_synthesis_matches_generator(feat_dtype):
 
 
 def test_pipeline_shapes_bit_identical(c1):
-    """Sequential mode and 1..8 concurrent sampling streams only change the
+    """Sequential mode and 1..12 concurrent sampling streams only change the
     schedule (pipeline.hpp:107-109): losses, weights and per-step statistics
     are bit-identical for every shape, over more steps than arenas."""
     g = c1
     spec = T.ModelSpec(g.feat_dim, 16, 4)
     cache = CA.build_static_cache(g, CA.CacheConfig(int(0.2 * g.num_nodes) * g.feat_dim * 4, 1))
     ref = None
-    for n in (0, 1, 2, 4, 8):
+    for n in (0, 1, 2, 4, 8, 12):
         tr = T.Trainer(g, cache, spec, [10, 5], max_seeds=512)
         tr.set_pipeline(n)
-        got = _steps(tr, g, K=11)
+        got = _steps(tr, g, K=15)
         if ref is None:
             ref = got
         else:
@@ -260,7 +260,7 @@ def test_pipeline_shapes_bit_identical(c1):
             assert all(np.array_equal(a, b) for a, b in zip(got[1], ref[1])), n
             assert np.array_equal(got[2], ref[2]), n
     with pytest.raises(Exception):
-        tr.set_pipeline(9)
+        tr.set_pipeline(13)
 
 
 def test_device_resident_seeds_are_validated(c1):
